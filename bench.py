@@ -1,0 +1,482 @@
+#!/usr/bin/env python
+"""bench.py -- V-trace + loss + grad trajectory-steps/s and HBM GB/s on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` (torchrun for
+N > 1, one rank per GPU, NCCL) prints ONE JSON line on rank 0.
+
+A "step" is one learner update's hot path over one batch: the fused
+vtrace_loss_and_grad kernel on this rank's [T, B, A] trajectories (all SURVEY
+8(a) rows a1-a12), plus, for N > 1, the NCCL all-reduce of the 8 fp64 partial
+sums (row a13, issued on a side stream so it overlaps the next step's kernel).
+Weak scaling: every rank owns its own B = 8192 trajectories (the paper's
+synchronous learners each consume their own batch).
+
+Workload (default): BASELINE.json configs[3], "large": T=100, B=8192, A=18,
+bf16 logits, clip[-1,1] rewards; inputs resident in HBM, rotated over R copies
+so every step reads cold data (R x working set >= 4 x L2).
+
+``--impl reference``: the CPU oracle (oracle/, the only reference this tier
+has) timed on the host cores on bounded column samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+METRIC = "V-trace+loss+grad trajectory-steps/s and HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "trajectory-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="large")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the config's B is the GLOBAL batch")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(world, local):
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc is None:
+            return
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+
+    def summary(self, t0=None, t1=None):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ts, line in self.lines:
+            if t0 is not None and (ts < t0 or ts > t1 + 0.06):
+                continue
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def load_traffic(config_name: str):
+    """dram bytes per launch of the fused kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config_name)
+    except (OSError, ValueError):
+        return None
+
+
+def algorithmic_bytes(T, B, A, elem):
+    """Bytes the method must move per call: read both logits rows,
+    a, r, gamma, V; write dlogits, dV; plus the bootstrap row and 64 B partials."""
+    return T * B * (3 * A * elem + 20) + 4 * B + 64
+
+
+def make_rank_inputs(cfg, rank, world, strong):
+    from paper_1802_01561_b200 import workload as wl
+    if strong:
+        full = wl.make_inputs(cfg.name)
+        per = cfg.B // world
+        return wl.column_slice(full, rank * per, (rank + 1) * per)
+    return wl.make_inputs(cfg.name, seed=cfg.seed + 7919 * rank)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args):
+    world, rank, local = dist_env()
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    import paper_1802_01561_b200 as pkg
+    from paper_1802_01561_b200 import vtrace as vt
+    from paper_1802_01561_b200 import workload as wl
+
+    cfg = wl.CONFIGS[args.config]
+    inp = make_rank_inputs(cfg, rank, world, args.strong)
+    T, B, A = inp["T"], inp["B"], inp["A"]
+    elem = 2 if inp["dtype"] == wl.DTYPE_BF16 else 4
+    host = pkg.tensors_from_workload(inp, "cpu", pin=True)
+    base = {k: v.to("cuda", non_blocking=True) for k, v in host.items()}
+    in_bytes = sum(v.numel() * v.element_size() for v in base.values())
+    out_bytes = T * B * A * elem + T * B * 4 + 64
+    working = in_bytes + out_bytes
+    R = max(1, math.ceil(4 * L2_BYTES / working))
+    sets = [base] + [{k: v.clone() for k, v in base.items()} for _ in range(R - 1)]
+    outs = [{"grad_target_logits": torch.empty(T, B, A, dtype=base["target_logits"].dtype,
+                                               device="cuda"),
+             "grad_values": torch.empty(T, B, dtype=torch.float32, device="cuda"),
+             "partials": torch.zeros(8, dtype=torch.float64, device="cuda")} for _ in range(R)]
+    ws = pkg.Workspace(T, B, A, inp["dtype"])
+    kw = dict(reward_mode=inp["reward_mode"], baseline_cost=wl.BASELINE_COST,
+              entropy_cost=wl.ENTROPY_COST, rho_bar=wl.RHO_BAR, c_bar=wl.C_BAR)
+    s_main = torch.cuda.Stream()
+    s_comm = torch.cuda.Stream()
+
+    def step(i):
+        o = outs[i % R]
+        x = sets[i % R]
+        pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw)
+        if world > 1:
+            s_comm.wait_stream(s_main)
+            with torch.cuda.stream(s_comm):
+                dist.all_reduce(o["partials"])
+
+    # eager warm-up (also creates the NCCL communicator before any capture)
+    with torch.cuda.stream(s_main):
+        for i in range(max(args.warmup, 1)):
+            step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # graphs of C steps (C a multiple of R) + a remainder graph: exactly K steps
+    K = args.steps
+    C = R * max(1, math.ceil(min(K, 100) / R))
+    n_full, rem = divmod(K, C)
+    graph_mode = "cuda-graph"
+
+    def capture(nsteps):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s_main):
+            for i in range(nsteps):
+                step(i)
+            if world > 1:
+                s_main.wait_stream(s_comm)
+        return g
+
+    try:
+        g_full = capture(C) if n_full else None
+        g_rem = capture(rem) if rem else None
+    except Exception as e:  # noqa: BLE001
+        graph_mode = f"eager ({type(e).__name__} in capture)"
+        g_full = g_rem = None
+    torch.cuda.synchronize()
+
+    def run_timed_body():
+        if g_full is None and g_rem is None:
+            with torch.cuda.stream(s_main):
+                for i in range(K):
+                    step(i)
+                if world > 1:
+                    s_main.wait_stream(s_comm)
+        else:
+            with torch.cuda.stream(s_main):
+                for _ in range(n_full):
+                    g_full.replay()
+                if g_rem is not None:
+                    g_rem.replay()
+
+    # warm the graphs (untimed) with W more steps' worth of replays
+    if g_full is not None or g_rem is not None:
+        with torch.cuda.stream(s_main):
+            (g_rem or g_full).replay()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    tw0 = time.time()
+    ev0.record(s_main)
+    run_timed_body()
+    ev1.record(s_main)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    barrier(world)
+    if sampler:
+        sampler.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    elapsed_max = max_over_ranks(elapsed_ms, world)
+
+    # kernel-only timing for the roofline: the same kernels, no collective
+    Kk = min(K, 2000)
+    gk = None
+    try:
+        gk = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gk, stream=s_main):
+            for i in range(min(Kk, C)):
+                o = outs[i % R]
+                x = sets[i % R]
+                pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw)
+    except Exception:  # noqa: BLE001
+        gk = None
+    torch.cuda.synchronize()
+    reps = max(1, Kk // min(Kk, C))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for _ in range(reps):
+            gk.replay()
+    e1.record(s_main)
+    torch.cuda.synchronize()
+    kernel_ms = e0.elapsed_time(e1) / (reps * min(Kk, C))
+
+    # end-to-end through the public host-input API
+    e2e = None
+    if not args.no_e2e:
+        Ke = args.e2e_steps
+        part_h = torch.zeros(8, dtype=torch.float64).pin_memory()
+        o = outs[0]
+        with torch.cuda.stream(s_main):
+            pkg.loss_and_grad_from_host(host, sets[0], o, ws, part_h, **kw)
+        torch.cuda.synchronize()
+        barrier(world)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(s_main)
+        with torch.cuda.stream(s_main):
+            for i in range(Ke):
+                pkg.loss_and_grad_from_host(host, sets[i % R], o, ws, part_h, **kw)
+                if world > 1:
+                    dist.all_reduce(o["partials"])
+        eb.record(s_main)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(ea.elapsed_time(eb), world) / Ke
+        e2e = {"value": T * B * world / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 64,
+               "ms_per_step": e2e_ms}
+
+    # status check (data errors would void the run)
+    code, idx = pkg.read_device_status(ws)
+    if code != 0:
+        raise SystemExit(f"device status reported data error {code} at row {idx}")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(inp, args.cpu_seconds)
+
+    if rank != 0:
+        return
+    ms_per_step = elapsed_max / K
+    value = T * B * world / (ms_per_step * 1e-3)
+    peak, peak_src = load_peak()
+    alg = algorithmic_bytes(T, B, A, elem)
+    achieved = alg / (kernel_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.config)
+    clocks = sampler.summary(tw0, tw1) if sampler else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+        "dtype": "bf16 logits; f64 row sums / ratio / scan, f32 gradient epilogue"
+                 if elem == 2 else "f32 logits; f64 row sums / ratio / scan, f32 epilogue",
+        "data": "synthetic (seeded, DMLab/Atari-shaped; DESIGN.md input recipe)",
+        "config": {"workload": cfg.name, "T": T, "B_per_gpu": B, "A": A,
+                   "logits_dtype": "bf16" if elem == 2 else "fp32",
+                   "global_batch": B * world, "seq_len": T, "parallelism": f"dp{world}",
+                   "l2": f"inputs rotated over {R} HBM-resident copies "
+                         f"({R} x {working / 1e6:.1f} MB >= 4 x L2)",
+                   "timing": graph_mode,
+                   "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream)"
+                   if world > 1 else "none"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "vtrace_fused_kernel", "kernel_ms": kernel_ms,
+                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+        "gpu_launches": K,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the oracle on the host cores
+
+
+def cpu_baseline(inp, seconds):
+    import oracle
+    from paper_1802_01561_b200 import workload as wl
+    T, B = inp["T"], inp["B"]
+    small = wl.column_slice(inp, 0, min(B, 64))
+    t0 = time.perf_counter()
+    oracle.loss_and_grad(small, reward_mode=inp["reward_mode"])
+    dt = time.perf_counter() - t0
+    rate_cols = small["B"] / max(dt, 1e-6)
+    ncols = int(max(1, min(B, rate_cols * seconds)))
+    sample = wl.column_slice(inp, 0, ncols)
+    t0 = time.perf_counter()
+    oracle.loss_and_grad(sample, reward_mode=inp["reward_mode"])
+    dt = time.perf_counter() - t0
+    return {"value": T * ncols / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"columns [0,{ncols}) of the {inp['T']}x{B} batch (T={T}), "
+                      f"oracle.loss_and_grad single-threaded fp64, {dt:.1f} s",
+            "host_cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle
+    import oracle
+    from paper_1802_01561_b200 import workload as wl
+    cfg = wl.CONFIGS[args.config]
+    inp = wl.make_inputs(cfg.name)
+    T, B = inp["T"], inp["B"]
+    # size each step's column sample so the whole run takes ~1-2 minutes
+    probe = wl.column_slice(inp, 0, min(B, 32))
+    t0 = time.perf_counter()
+    oracle.loss_and_grad(probe, reward_mode=inp["reward_mode"])
+    per_col = (time.perf_counter() - t0) / probe["B"]
+    budget = 90.0 / max(1, args.steps + args.warmup)
+    ncols = int(max(1, min(B, budget / max(per_col, 1e-9))))
+    sample = wl.column_slice(inp, 0, ncols)
+    for _ in range(args.warmup):
+        oracle.loss_and_grad(sample, reward_mode=inp["reward_mode"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.loss_and_grad(sample, reward_mode=inp["reward_mode"])
+    dt = time.perf_counter() - t0
+    value = args.steps * T * ncols / dt
+    desc = (f"each step: oracle.loss_and_grad (fp64, single-threaded) on columns [0,{ncols}) "
+            f"of the {T}x{B} '{cfg.name}' batch")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "T": T, "B_sample": ncols, "A": inp["A"],
+                       "global_batch": ncols, "seq_len": T, "parallelism": "cpu-1core"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": desc, "host_cpu": _cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,197 @@
+/* vtrace.h -- C ABI of the B200-native IMPALA V-trace learner hot path.
+ *
+ * Implements, on one NVIDIA B200 (sm_100a), the learner-side computation of
+ * Espeholt et al., "IMPALA: Scalable Distributed Deep-RL with Importance
+ * Weighted Actor-Learner Architectures", arxiv 1802.01561, Section 4:
+ *
+ *   log pi(a_t|x_t), log mu(a_t|x_t) from full logits rows
+ *   rho_t = min(rho_bar, pi/mu), c_t = lambda min(c_bar, pi/mu)  P:196 (Eq.1), P:225 (Remark 2)
+ *   delta_t V = rho_t (r_t + gamma_t V(x_{t+1}) - V(x_t))
+ *   v_s = V(x_s) + delta_s V + gamma_s c_s (v_{s+1} - V(x_{s+1})) P:222 (Remark 1)
+ *   q_s = r_s + gamma_s v_{s+1};  pg_adv_s = rho_s (q_s - V(x_s)) P:242
+ *   L = -sum pg_adv log pi(a) + c_v 1/2 sum (v - V)^2 - c_e sum H
+ *   dL/dz^pi and dL/dV (v, q, pg_adv, rho held constant)
+ *
+ * Notation follows Section 4: t in [0,T) is time, b in [0,B) is the trajectory
+ * (batch column), j in [0,A) the action.  The episode-end convention (the paper
+ * is silent) is gamma_t = gamma (1 - done_t): a discount of 0 cuts both the
+ * bootstrap term of delta_t and the trace (reading c1).  v_T is the
+ * bootstrap value V(x_T) (reading c2).  All sums run over batch AND time.
+ *
+ * Conventions for every call:
+ *  - All array pointers are CUDA DEVICE pointers, C-contiguous, time-major:
+ *    logits [T][B][A] (A fastest), per-step arrays [T][B], bootstrap [B].
+ *  - Every call is asynchronous on `stream`, allocates nothing, never
+ *    synchronises the host (except vtrace_read_device_status), and is CUDA-graph
+ *    capturable.  The caller owns all memory; outputs must not alias inputs.
+ *  - Host-checkable problems are reported by the return value before anything
+ *    is launched or written.  Problems in the DATA (bad action index, non-finite
+ *    values, discount outside [0,1]) cannot be seen by the host: the kernel
+ *    records the smallest offending row (t*B + b, or T*B + b for bootstrap[b])
+ *    with its kind in the workspace status word, keeps every memory access in
+ *    bounds (the action index is clamped for the gather), and leaves the
+ *    outputs of bad rows unspecified.  Read it with vtrace_read_device_status.
+ *  - The workspace (size from vtrace_workspace_bytes) must be initialised once
+ *    with vtrace_workspace_init before its first use; it carries the decoupled
+ *    look-back flags, per-tile partial sums and the status word across calls
+ *    (epoch-tagged: no per-call memset).  Calls that may run concurrently need
+ *    distinct workspaces.
+ *  - Requires an sm_100 device (B200).  No CPU fallback exists.
+ */
+#ifndef VTRACE_B200_H_
+#define VTRACE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* vt_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  VT_OK = 0,
+  VT_ERR_INVALID_ARG = 1, /* a required pointer is NULL                                 */
+  VT_ERR_SHAPE = 2,       /* T, B or A <= 0, A > VT_MAX_ACTIONS, or T*B*A overflows     */
+  VT_ERR_DTYPE = 3,       /* logits dtype not VT_FLOAT32 / VT_BFLOAT16                   */
+  VT_ERR_PARAM = 4,       /* thresholds <= 0 or NaN, c_bar > rho_bar, lambda not
+                             in [0,1], unknown reward mode, non-finite costs      */
+  VT_ERR_ALIGNMENT = 5,   /* a pointer is not aligned to its element size               */
+  VT_ERR_WORKSPACE = 6,   /* workspace NULL, too small, or not 256-byte aligned         */
+  VT_ERR_CUDA = 7,        /* a CUDA runtime call or launch failed                        */
+  VT_ERR_DEVICE = 8       /* current device is not compute capability 10.0 (sm_100)    */
+} vt_status;
+
+typedef enum { VT_FLOAT32 = 0, VT_BFLOAT16 = 1 } vt_dtype;
+
+/* Reward transform applied to r_t before use (P:834 / P:944: clip to [-1,1];
+ * P:819 / P:835: optimistic asymmetric clipping for DMLab-30). */
+typedef enum {
+  VT_REWARD_NONE = 0,
+  VT_REWARD_CLIP_UNIT = 1, /* min(1, max(-1, r))                          */
+  VT_REWARD_ASYM_TANH = 2  /* 0.3 min(tanh r, 0) + 5.0 max(tanh r, 0)       */
+} vt_reward_mode;
+
+/* Data-error kinds recorded in the device status word. */
+typedef enum {
+  VT_DATA_OK = 0,
+  VT_DATA_ACTION = 1,   /* a_t outside [0, A)                              */
+  VT_DATA_LOGITS = 2,   /* a non-finite logit in the row (either policy)   */
+  VT_DATA_REWARD = 3,   /* non-finite reward                               */
+  VT_DATA_VALUE = 4,    /* non-finite V(x_t) or bootstrap                  */
+  VT_DATA_DISCOUNT = 5  /* discount non-finite or outside [0, 1]           */
+} vt_data_error;
+
+#define VT_MAX_ACTIONS 2048
+
+typedef struct {
+  float clip_rho_threshold;    /* rho_bar; +INFINITY = no truncation         */
+  float clip_c_threshold;      /* c_bar; must be <= clip_rho_threshold       */
+  float clip_pg_rho_threshold; /* truncation of the rho_s in the PG term;
+                                  the paper uses rho_bar (reading c4)                */
+  float lambda_;               /* Remark 2, in [0, 1]; 1 = plain V-trace     */
+  int32_t reward_mode;         /* vt_reward_mode                                     */
+} vt_vtrace_params;
+
+typedef struct {
+  float baseline_cost; /* c_v: "baseline loss scaling" 0.5 */
+  float entropy_cost;  /* c_e: entropy regulariser 0.01           */
+} vt_loss_weights;
+
+/* Indices into the double partials[VT_P_COUNT] output (sums over this call's
+ * batch and time; shards of one global batch add up elementwise). */
+enum {
+  VT_P_PG_LOSS = 0,       /* -sum pg_adv_t log pi(a_t|x_t)                       */
+  VT_P_BASELINE_LOSS = 1, /* 1/2 sum (v_t - V(x_t))^2                            */
+  VT_P_ENTROPY_SUM = 2,   /* sum_t H_t, H = -sum_j pi_j log pi_j                 */
+  VT_P_TOTAL_LOSS = 3,    /* PG + c_v BASELINE - c_e ENTROPY                    */
+  VT_P_SUMSQ_DLOGITS = 4, /* sum of squared dL/dz^pi (fp32 values before the
+                             store rounding)                                     */
+  VT_P_SUMSQ_DVALUES = 5, /* sum of squared dL/dV                                */
+  VT_P_SUM_RHO = 6,       /* sum of truncated rho_t                              */
+  VT_P_N_RHO_CLIPPED = 7, /* number of steps with pi/mu > rho_bar                */
+  VT_P_COUNT = 8
+};
+
+/* Bytes of device workspace needed for a (T, B, A, dtype) problem.  0 on bad
+ * arguments.  The size depends only on these four numbers. */
+size_t vtrace_workspace_bytes(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype);
+
+/* One-time initialisation of a workspace (stream-ordered memset). */
+vt_status vtrace_workspace_init(void* workspace, size_t workspace_bytes, vt_stream_t stream);
+
+/* V-trace targets and policy-gradient advantages (Section 4.1-4.2).
+ *   behaviour_policy_logits  z^mu [T][B][A]  logits of the actors' policy mu
+ *   target_policy_logits     z^pi [T][B][A]  logits of the learner's policy pi
+ *   actions                  a_t  [T][B]     int32 in [0, A)
+ *   discounts                gamma_t [T][B]  fp32 in [0,1]; gamma (1 - done_t)
+ *   rewards                  r_t  [T][B]     fp32, raw (p->reward_mode applied here)
+ *   values                   V(x_t) [T][B]   fp32
+ *   bootstrap_value          V(x_T) [B]      fp32
+ * Outputs (fp32 [T][B]): vs = v_t (required), pg_advantages (required),
+ *   log_rhos = log(pi/mu)(a_t), target_action_log_probs, behaviour_action_log_probs
+ *   (each nullable).  Logits are fp32 or bf16 (bf16 values are used exactly).
+ *   Pointers must be aligned to their element size. */
+vt_status vtrace_from_logits(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype,
+                             const void* behaviour_policy_logits,
+                             const void* target_policy_logits, const int32_t* actions,
+                             const float* discounts, const float* rewards,
+                             const float* values, const float* bootstrap_value,
+                             const vt_vtrace_params* params, float* vs, float* pg_advantages,
+                             float* log_rhos, float* target_action_log_probs,
+                             float* behaviour_action_log_probs, void* workspace,
+                             size_t workspace_bytes, vt_stream_t stream);
+
+/* Fused V-trace + actor-critic loss + gradients (Section 4.2, summed per P:789).
+ * Same seven inputs as vtrace_from_logits.  Outputs:
+ *   grad_target_logits [T][B][A] in the logits dtype (bf16: round-to-nearest-even)
+ *       dL/dz^pi_j = pg_adv (pi_j - 1[j=a_t]) + c_e pi_j (log pi_j + H_t)
+ *   grad_values [T][B] fp32: dL/dV(x_t) = c_v (V(x_t) - v_t)
+ *   partials [VT_P_COUNT] double (device): this call's sums (deterministic:
+ *       fixed-order reduction, bitwise reproducible run to run)
+ *   vs, pg_advantages [T][B] fp32: nullable.
+ * No gradient flows to z^mu, the bootstrap value or the rewards (reading c10). */
+vt_status vtrace_loss_and_grad(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype,
+                               const void* behaviour_policy_logits,
+                               const void* target_policy_logits, const int32_t* actions,
+                               const float* discounts, const float* rewards,
+                               const float* values, const float* bootstrap_value,
+                               const vt_vtrace_params* params, const vt_loss_weights* weights,
+                               void* grad_target_logits, float* grad_values, double* partials,
+                               float* vs, float* pg_advantages, void* workspace,
+                               size_t workspace_bytes, vt_stream_t stream);
+
+/* End-to-end variant for inputs that live in HOST memory (the actors' queue):
+ * copies the seven host inputs (pinned memory recommended) into the caller's
+ * device staging buffers with cudaMemcpyAsync, runs vtrace_loss_and_grad, and
+ * copies the partials back to host `partials_host`.  Gradients stay on the
+ * device (they feed the network backward).  Asynchronous on `stream`; the host
+ * values are valid after the stream is synchronised.  d_* are device buffers of
+ * the inputs' sizes. */
+vt_status vtrace_loss_and_grad_from_host(
+    int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype, const void* h_behaviour_logits,
+    const void* h_target_logits, const int32_t* h_actions, const float* h_discounts,
+    const float* h_rewards, const float* h_values, const float* h_bootstrap_value,
+    void* d_behaviour_logits, void* d_target_logits, int32_t* d_actions, float* d_discounts,
+    float* d_rewards, float* d_values, float* d_bootstrap_value,
+    const vt_vtrace_params* params, const vt_loss_weights* weights, void* grad_target_logits,
+    float* grad_values, double* partials_device, double* partials_host, void* workspace,
+    size_t workspace_bytes, vt_stream_t stream);
+
+/* Reads and clears the device status word: *code = vt_data_error of the
+ * smallest offending row (VT_DATA_OK if none), *first_bad_flat_index = that
+ * row (-1 if none).  Synchronises `stream` (the only call that does). */
+vt_status vtrace_read_device_status(void* workspace, int32_t* code,
+                                    int64_t* first_bad_flat_index, vt_stream_t stream);
+
+/* Static, NUL-terminated description of a status code. */
+const char* vtrace_status_string(vt_status status);
+
+/* Library ABI version (major*10000 + minor*100 + patch). */
+int32_t vtrace_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VTRACE_B200_H_ */

@@ -1,0 +1,259 @@
+// vtrace_kernels.cuh -- fused V-trace + actor-critic loss + gradient kernel for sm_100a.
+//
+// One CTA processes one work unit = (column group of BC=8 trajectories) x
+// (time chunk of Tc steps).  Units are handed out by an atomic ticket in
+// REVERSE time order, so the unit holding the later chunk of a column group
+// always started earlier; the reverse V-trace recursion (Remark 1)
+// crosses chunk boundaries through a decoupled look-back on per-unit
+// affine aggregates (G, D):  A_start = D + G * A_end  with A = v - V.
+//
+// Phases inside a unit:
+//   a1  stage: TMA 2D tile loads of z^pi, z^mu [Tc][BC*A] and a, r, gamma, V [Tc][BC]
+//       into shared memory (one mbarrier), or plain loads for unaligned shapes
+//   a3-a6  per row (thread per row): max, accurate sum of exp for both policies,
+//       importance ratio pi/mu at a_t in fp64, lse of pi (fp32) for the epilogue
+//   a2,a7-a9  per column (warp per column, lanes over time): reward transform,
+//       delta_t, segment affine aggregates, warp suffix scan, look-back carry,
+//       v_t, q_t, pg_adv_t -- all fp64
+//   a10-a11  per row: pi_j, log pi_j, entropy, dL/dz^pi written in place over
+//       the z^pi tile, then one TMA 2D store; dL/dV from the scan warps
+//   a12  per-unit fp64 partials; the last CTA reduces them in a fixed order
+//
+// Precision: every quantity that feeds the recursion (sum_j exp, the ratio,
+// delta, the scan) is carried well beyond fp32 (fp64 or compensated fp32);
+// the gradient epilogue is fp32 (its outputs are fp32/bf16).  See DESIGN.md.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace vtb200 {
+
+constexpr int BC = 8;          // trajectories (columns) per unit
+constexpr int NWARPS = 8;      // one warp per column in the scan phase
+constexpr int NTHREADS = NWARPS * 32;
+constexpr int NPART = 8;
+
+enum ExpMode { EXP_F64 = 0, EXP_MUFU = 1 };
+
+struct alignas(16) WsHeader {
+  unsigned int ticket;
+  unsigned int done;
+  unsigned int epoch;
+  unsigned int pad0;
+  unsigned long long status;  // (row << 8) | kind, atomicMin; ~0ull = clean
+  unsigned long long pad1[5];
+};
+
+// Decoupled look-back record of one (unit, column): published by lane 0 of
+// the column's warp.  flag = (epoch << 2) | state; state 1 = aggregate (G, D)
+// of the chunk, state 2 = inclusive carry (A = v - V at the chunk's first step).
+struct alignas(16) ColRec {
+  unsigned int flag;
+  unsigned int pad;
+  double G, D, incl;
+};
+static_assert(sizeof(ColRec) == 32, "ColRec layout");
+
+struct Params {
+  long long T, B;
+  int A, Tc, K, G, units;
+  int has_lr, has_lp, has_lm;
+  const void* mu;
+  const void* pi;
+  const int* actions;
+  const float* disc;
+  const float* rew;
+  const float* val;
+  const float* boot;
+  float* vs;
+  float* pg_adv;
+  float* log_rhos;
+  float* lp_out;
+  float* lm_out;
+  void* dlogits;
+  float* dvalues;
+  double* partials;
+  double rho_bar, c_bar, pg_rho_bar, lambda;
+  double c_v, c_e;
+  int reward_mode;
+  WsHeader* ws;
+  ColRec* recs;
+  double* unit_partials;
+};
+
+struct TmaMaps {
+  CUtensorMap mu, pi, a, r, g, v, dz;
+};
+
+// ---------------------------------------------------------------------------
+// small PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y,
+                                             const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_store_commit_and_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ double shfl_down_d(double v, int off) {
+  return __shfl_down_sync(0xffffffffu, v, off);
+}
+
+// ---------------------------------------------------------------------------
+// logits element access
+
+template <typename LT>
+struct Elem;
+template <>
+struct Elem<float> {
+  static constexpr int bytes = 4;
+  static __device__ __forceinline__ float get(const float* p, int i) { return p[i]; }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+  static constexpr int bytes = 2;
+  static __device__ __forceinline__ float get(const __nv_bfloat16* p, int i) {
+    return __bfloat162float(p[i]);
+  }
+};
+
+// Loads a row of A_CT logits from shared memory into registers (exact upcast).
+template <typename LT, int A_CT>
+__device__ __forceinline__ void load_row(const LT* row, float (&z)[A_CT]) {
+  if constexpr (sizeof(LT) == 2 && (A_CT % 2) == 0) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+#pragma unroll
+    for (int k = 0; k < A_CT / 2; ++k) {
+      uint32_t x = w[k];
+      z[2 * k] = __uint_as_float(x << 16);
+      z[2 * k + 1] = __uint_as_float(x & 0xffff0000u);
+    }
+  } else if constexpr (sizeof(LT) == 4 && (A_CT % 2) == 0) {
+    // rows of even length start 8-byte aligned
+    const float2* w = reinterpret_cast<const float2*>(row);
+#pragma unroll
+    for (int k = 0; k < A_CT / 2; ++k) {
+      float2 x = w[k];
+      z[2 * k] = x.x;
+      z[2 * k + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < A_CT; ++j) z[j] = Elem<LT>::get(row, j);
+  }
+}
+
+// fp64 exp for x <= 0 (clamped at -700).  Cody-Waite reduction
+// x = n ln2 + r, |r| <= ln2/2, then a degree-6 polynomial fitted to exp on
+// that interval (max relative error 1.9e-9; the path needs ~1e-8).
+__device__ __forceinline__ double exp64_nonpos(double x) {
+  const double LOG2E = 1.4426950408889634;
+  const double LN2_HI = 6.93147180369123816490e-01;
+  const double LN2_LO = 1.90821492927058770002e-10;
+  const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
+  x = fmax(x, -700.0);
+  double t = fma(x, LOG2E, MAGIC);
+  double n = t - MAGIC;
+  int ni = __double2loint(t);
+  double r = fma(-n, LN2_HI, x);
+  r = fma(-n, LN2_LO, r);
+  double p = 1.38294205944386960e-03;
+  p = fma(p, r, 8.37477152027917178e-03);
+  p = fma(p, r, 4.16683580330002093e-02);
+  p = fma(p, r, 1.66664208321203350e-01);
+  p = fma(p, r, 4.99999914930370937e-01);
+  p = fma(p, r, 1.00000003612590005e+00);
+  p = fma(p, r, 1.00000000059202110e+00);
+  // scale by 2^n: add n to the exponent field (p in [0.7, 1.5], n >= -1010)
+  int hi = __double2hiint(p) + (ni << 20);
+  return __hiloint2double(hi, __double2loint(p));
+}
+
+// Compensated fp32 exp for MUFU mode: e = 2^{(z - m) log2 e} via ex2.approx,
+// with the fp32 rounding of the argument (and, for fp32 logits, of z - m)
+// corrected to first order.  Returns e (fp32).
+template <bool EXACT_DIFF>
+__device__ __forceinline__ float exp_mufu(float z, float m) {
+  const float L = 1.44269502f;       // fp32(log2 e)
+  const float L_LO = 1.925963e-08f;  // log2 e - L
+  const float LN2 = 0.693147182f;
+  float d = z - m;
+  float y = d * L;
+  float y_lo = fmaf(d, L, -y);
+  y_lo = fmaf(d, L_LO, y_lo);
+  if constexpr (!EXACT_DIFF) {
+    float bb = d - z;  // TwoSum error of the fp32 difference
+    float d_lo = (z - (d - bb)) + (-m - bb);
+    y_lo = fmaf(d_lo, L, y_lo);
+  }
+  float e = ex2_approx(y);
+  return fmaf(e, y_lo * LN2, e);
+}
+
+}  // namespace vtb200

@@ -1,0 +1,294 @@
+"""Thin Python binding of the C ABI in include/vtrace.h (argument marshalling only).
+
+Every computation runs in libvtrace.so's CUDA kernels; this module only turns
+torch tensors into pointers and the current CUDA stream into a handle.  There
+is no CPU fallback: if the library is missing or the device is not an sm_100
+B200, calls raise.
+
+Names follow the C ABI: ``workspace_bytes``, ``Workspace`` (alloc + init),
+``from_logits``, ``loss_and_grad``, ``loss_and_grad_from_host``,
+``read_device_status``, ``status_string``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import workload as _wl
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvtrace.so")
+
+VT_FLOAT32 = 0
+VT_BFLOAT16 = 1
+P_PG_LOSS, P_BASELINE_LOSS, P_ENTROPY_SUM, P_TOTAL_LOSS = 0, 1, 2, 3
+P_SUMSQ_DLOGITS, P_SUMSQ_DVALUES, P_SUM_RHO, P_N_RHO_CLIPPED = 4, 5, 6, 7
+P_COUNT = 8
+PARTIAL_NAMES = ("pg_loss", "baseline_loss", "entropy_sum", "total_loss", "sumsq_dlogits",
+                 "sumsq_dvalues", "sum_rho", "n_rho_clipped")
+DATA_ERRORS = {0: "ok", 1: "action", 2: "logits", 3: "reward", 4: "value", 5: "discount"}
+
+EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_from_logits",
+                    "vtrace_loss_and_grad", "vtrace_loss_and_grad_from_host",
+                    "vtrace_read_device_status", "vtrace_status_string", "vtrace_version")
+
+
+class VtraceError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {status_string(status)} (status {status})")
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("clip_rho_threshold", ctypes.c_float), ("clip_c_threshold", ctypes.c_float),
+                ("clip_pg_rho_threshold", ctypes.c_float), ("lambda_", ctypes.c_float),
+                ("reward_mode", ctypes.c_int32)]
+
+
+class _Weights(ctypes.Structure):
+    _fields_ = [("baseline_cost", ctypes.c_float), ("entropy_cost", ctypes.c_float)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads libvtrace.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_1802_01561_b200._build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    i64 = ctypes.c_int64
+    lib.vtrace_workspace_bytes.argtypes = [i64, i64, i64, ctypes.c_int]
+    lib.vtrace_workspace_bytes.restype = ctypes.c_size_t
+    lib.vtrace_workspace_init.argtypes = [P, ctypes.c_size_t, P]
+    lib.vtrace_workspace_init.restype = ctypes.c_int
+    lib.vtrace_from_logits.argtypes = [i64, i64, i64, ctypes.c_int] + [P] * 7 + [
+        ctypes.POINTER(_Params)] + [P] * 5 + [P, ctypes.c_size_t, P]
+    lib.vtrace_from_logits.restype = ctypes.c_int
+    lib.vtrace_loss_and_grad.argtypes = [i64, i64, i64, ctypes.c_int] + [P] * 7 + [
+        ctypes.POINTER(_Params), ctypes.POINTER(_Weights)] + [P] * 5 + [P, ctypes.c_size_t, P]
+    lib.vtrace_loss_and_grad.restype = ctypes.c_int
+    lib.vtrace_loss_and_grad_from_host.argtypes = [i64, i64, i64, ctypes.c_int] + [P] * 14 + [
+        ctypes.POINTER(_Params), ctypes.POINTER(_Weights)] + [P] * 4 + [P, ctypes.c_size_t, P]
+    lib.vtrace_loss_and_grad_from_host.restype = ctypes.c_int
+    lib.vtrace_read_device_status.argtypes = [P, ctypes.POINTER(ctypes.c_int32),
+                                              ctypes.POINTER(ctypes.c_int64), P]
+    lib.vtrace_read_device_status.restype = ctypes.c_int
+    lib.vtrace_status_string.argtypes = [ctypes.c_int]
+    lib.vtrace_status_string.restype = ctypes.c_char_p
+    lib.vtrace_version.argtypes = []
+    lib.vtrace_version.restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+def status_string(status: int) -> str:
+    return load_library().vtrace_status_string(int(status)).decode()
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise VtraceError(status, where)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return VT_FLOAT32
+    if t.dtype == torch.bfloat16:
+        return VT_BFLOAT16
+    raise TypeError(f"logits must be float32 or bfloat16, got {t.dtype}")
+
+
+def params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=0) -> _Params:
+    return _Params(float(rho_bar), float(c_bar),
+                   float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
+                   int(reward_mode))
+
+
+def workspace_bytes(T: int, B: int, A: int, dtype_code: int) -> int:
+    return int(load_library().vtrace_workspace_bytes(T, B, A, dtype_code))
+
+
+class Workspace:
+    """Device workspace for (T, B, A, dtype): allocated once, initialised once."""
+
+    def __init__(self, T, B, A, dtype_code, device=None):
+        n = workspace_bytes(T, B, A, dtype_code)
+        if n == 0:
+            raise ValueError("bad shape for workspace")
+        self.device = torch.device(device if device is not None else "cuda")
+        self.nbytes = n
+        self.buf = torch.empty(n + 256, dtype=torch.uint8, device=self.device)
+        off = (-self.buf.data_ptr()) % 256
+        self.tensor = self.buf[off:off + n]
+        _check(load_library().vtrace_workspace_init(_ptr(self.tensor), n, _stream(self.device)),
+               "vtrace_workspace_init")
+
+    @property
+    def ptr(self):
+        return _ptr(self.tensor)
+
+
+def _shapes(behaviour_logits, target_logits, actions):
+    if behaviour_logits.dim() != 3 or target_logits.shape != behaviour_logits.shape:
+        raise ValueError("logits must be [T, B, A] and equal shapes")
+    T, B, A = target_logits.shape
+    if actions.shape != (T, B):
+        raise ValueError("actions must be [T, B]")
+    return T, B, A
+
+
+def _contig(*ts):
+    for t in ts:
+        if t is not None and not t.is_contiguous():
+            raise ValueError("all tensors must be contiguous")
+        if t is not None and not t.is_cuda:
+            raise ValueError("all tensors must be CUDA tensors")
+
+
+def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, values,
+                bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
+                reward_mode=0, workspace: Workspace | None = None, with_log_probs=True,
+                out: dict | None = None):
+    """vtrace_from_logits.  Returns dict of fp32 [T, B] tensors: vs,
+    pg_advantages (+ log_rhos, target_action_log_probs, behaviour_action_log_probs)."""
+    lib = load_library()
+    T, B, A = _shapes(behaviour_logits, target_logits, actions)
+    dt = _dtype_code(target_logits)
+    dev = target_logits.device
+    _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
+    ws = workspace if workspace is not None else Workspace(T, B, A, dt, dev)
+    if out is None:
+        out = {k: torch.empty(T, B, dtype=torch.float32, device=dev) for k in ("vs", "pg_advantages")}
+        if with_log_probs:
+            for k in ("log_rhos", "target_action_log_probs", "behaviour_action_log_probs"):
+                out[k] = torch.empty(T, B, dtype=torch.float32, device=dev)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode)
+    st = lib.vtrace_from_logits(
+        T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
+        _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), _ptr(out["vs"]),
+        _ptr(out["pg_advantages"]), _ptr(out.get("log_rhos")),
+        _ptr(out.get("target_action_log_probs")), _ptr(out.get("behaviour_action_log_probs")),
+        ws.ptr, ws.nbytes, _stream(dev))
+    _check(st, "vtrace_from_logits")
+    return out
+
+
+def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, values,
+                  bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
+                  reward_mode=0, baseline_cost=0.5, entropy_cost=0.01,
+                  workspace: Workspace | None = None, with_targets=True, out: dict | None = None):
+    """vtrace_loss_and_grad.  Returns dict: grad_target_logits [T,B,A] (logits
+    dtype), grad_values [T,B] fp32, partials [8] fp64 (device), and, if
+    with_targets, vs and pg_advantages [T,B] fp32."""
+    lib = load_library()
+    T, B, A = _shapes(behaviour_logits, target_logits, actions)
+    dt = _dtype_code(target_logits)
+    dev = target_logits.device
+    _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
+    ws = workspace if workspace is not None else Workspace(T, B, A, dt, dev)
+    if out is None:
+        out = {"grad_target_logits": torch.empty_like(target_logits),
+               "grad_values": torch.empty(T, B, dtype=torch.float32, device=dev),
+               "partials": torch.empty(P_COUNT, dtype=torch.float64, device=dev)}
+        if with_targets:
+            out["vs"] = torch.empty(T, B, dtype=torch.float32, device=dev)
+            out["pg_advantages"] = torch.empty(T, B, dtype=torch.float32, device=dev)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode)
+    w = _Weights(float(baseline_cost), float(entropy_cost))
+    st = lib.vtrace_loss_and_grad(
+        T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
+        _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), ctypes.byref(w),
+        _ptr(out["grad_target_logits"]), _ptr(out["grad_values"]), _ptr(out["partials"]),
+        _ptr(out.get("vs")), _ptr(out.get("pg_advantages")), ws.ptr, ws.nbytes, _stream(dev))
+    _check(st, "vtrace_loss_and_grad")
+    return out
+
+
+def loss_and_grad_from_host(host: dict, dev_in: dict, out: dict, workspace: Workspace,
+                            partials_host: torch.Tensor, *, rho_bar=1.0, c_bar=1.0,
+                            pg_rho_bar=None, lambda_=1.0, reward_mode=0, baseline_cost=0.5,
+                            entropy_cost=0.01):
+    """vtrace_loss_and_grad_from_host: ``host`` holds pinned CPU tensors of the
+    seven inputs, ``dev_in`` same-shaped device staging tensors, ``out`` the
+    device outputs (grad_target_logits, grad_values, partials);
+    ``partials_host`` a pinned float64 [8] tensor filled asynchronously."""
+    lib = load_library()
+    T, B, A = host["target_logits"].shape
+    dt = _dtype_code(host["target_logits"])
+    dev = dev_in["target_logits"].device
+    names = ("behaviour_logits", "target_logits", "actions", "discounts", "rewards", "values",
+             "bootstrap_value")
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode)
+    w = _Weights(float(baseline_cost), float(entropy_cost))
+    st = lib.vtrace_loss_and_grad_from_host(
+        T, B, A, dt, *[_ptr(host[k]) for k in names], *[_ptr(dev_in[k]) for k in names],
+        ctypes.byref(p), ctypes.byref(w), _ptr(out["grad_target_logits"]),
+        _ptr(out["grad_values"]), _ptr(out["partials"]), _ptr(partials_host), workspace.ptr,
+        workspace.nbytes, _stream(dev))
+    _check(st, "vtrace_loss_and_grad_from_host")
+
+
+def read_device_status(workspace: Workspace):
+    """Synchronising read-and-clear of the data-error status: (kind, first_bad_row)."""
+    code = ctypes.c_int32(0)
+    idx = ctypes.c_int64(-1)
+    _check(load_library().vtrace_read_device_status(workspace.ptr, ctypes.byref(code),
+                                                     ctypes.byref(idx),
+                                                     _stream(workspace.device)),
+           "vtrace_read_device_status")
+    return int(code.value), int(idx.value)
+
+
+def version() -> int:
+    return int(load_library().vtrace_version())
+
+
+# ---------------------------------------------------------------------------
+# marshalling of the synthetic workload dicts (numpy, library layout) to tensors
+
+INPUT_NAMES = ("behaviour_logits", "target_logits", "actions", "discounts", "rewards", "values",
+               "bootstrap_value")
+
+
+def tensors_from_workload(inp: dict, device="cuda", pin: bool = False) -> dict:
+    """numpy workload dict -> torch tensors (bf16 logits from their uint16 bits)."""
+    out = {}
+    for k in INPUT_NAMES:
+        a = inp[k]
+        if k.endswith("logits") and inp["dtype"] == _wl.DTYPE_BF16:
+            t = torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(a))
+        if device == "cpu":
+            out[k] = t.pin_memory() if pin else t.clone()
+        else:
+            out[k] = t.to(device)
+    return out
+
+
+def call_kwargs(inp: dict) -> dict:
+    """Method parameters that a workload dict implies (reward transform)."""
+    return {"reward_mode": int(inp.get("reward_mode", 0))}
+
+
+__all__ = ["workspace_bytes", "Workspace", "from_logits", "loss_and_grad",
+           "loss_and_grad_from_host", "read_device_status", "status_string", "version",
+           "tensors_from_workload", "VtraceError", "load_library"]
+

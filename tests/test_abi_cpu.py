@@ -1,0 +1,113 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every function that
+include/vtrace.h declares, and rejects host-checkable bad arguments before
+touching the device (no compute calls here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1802_01561_b200 as pkg
+from paper_1802_01561_b200 import vtrace as vt
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "vtrace.h")
+
+
+def _declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(vtrace_[a-z_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1802_01561_b200 import _build
+    _build.build()
+    return vt.load_library()
+
+
+def test_header_declares_the_boundary():
+    names = _declared_functions()
+    for required in ("vtrace_from_logits", "vtrace_loss_and_grad", "vtrace_workspace_bytes",
+                     "vtrace_read_device_status", "vtrace_status_string"):
+        assert required in names
+    assert set(names) == set(vt.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+    out = os.popen(f"nm -D --defined-only {vt.LIB_PATH}").read()
+    for name in _declared_functions():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a_only(lib):
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {vt.LIB_PATH}").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out), out
+
+
+def test_status_strings(lib):
+    for s in range(9):
+        assert pkg.status_string(s)
+    assert pkg.status_string(0) == "ok"
+    assert pkg.version() >= 100
+
+
+def test_workspace_bytes(lib):
+    assert pkg.workspace_bytes(0, 1, 1, 0) == 0
+    assert pkg.workspace_bytes(5, 2, 3, 7) == 0
+    assert pkg.workspace_bytes(5, 2, 3, 0) > 256
+    big = pkg.workspace_bytes(100, 8192, 18, 1)
+    assert big > pkg.workspace_bytes(100, 4096, 18, 1)
+    # depends only on (T, B, A, dtype)
+    assert big == pkg.workspace_bytes(100, 8192, 18, 1)
+
+
+def _call_loss(lib, T=4, B=8, A=3, dt=0, ptr=0x10000, params=None, weights=None, ws=0x20000,
+               ws_bytes=1 << 20, nulls=()):
+    P = [ctypes.c_void_p(ptr)] * 7
+    for i in nulls:
+        P[i] = None
+    p = params if params is not None else vt.params()
+    w = weights if weights is not None else vt._Weights(0.5, 0.01)
+    outs = [ctypes.c_void_p(ptr)] * 3 + [None, None]
+    return lib.vtrace_loss_and_grad(T, B, A, dt, *P, ctypes.byref(p), ctypes.byref(w), *outs,
+                                    ctypes.c_void_p(ws), ws_bytes, None)
+
+
+def test_host_checks_return_before_launch(lib):
+    assert _call_loss(lib, nulls=(0,)) == 1          # VT_ERR_INVALID_ARG
+    assert _call_loss(lib, nulls=(6,)) == 1
+    assert _call_loss(lib, T=0) == 2                 # VT_ERR_SHAPE
+    assert _call_loss(lib, A=5000) == 2
+    assert _call_loss(lib, dt=3) == 3                # VT_ERR_DTYPE
+    assert _call_loss(lib, params=vt.params(rho_bar=1.0, c_bar=2.0)) == 4  # c_bar > rho_bar
+    assert _call_loss(lib, params=vt.params(lambda_=1.5)) == 4
+    assert _call_loss(lib, params=vt.params(rho_bar=float("nan"))) == 4
+    assert _call_loss(lib, params=vt.params(reward_mode=9)) == 4
+    assert _call_loss(lib, weights=vt._Weights(float("inf"), 0.01)) == 4
+    assert _call_loss(lib, ptr=0x10002) == 5         # VT_ERR_ALIGNMENT (fp32 data)
+    assert _call_loss(lib, ws_bytes=16) == 6         # VT_ERR_WORKSPACE
+    assert _call_loss(lib, ws=0x20010) == 6          # workspace not 256-aligned
+
+
+def test_from_logits_requires_outputs(lib):
+    P = [ctypes.c_void_p(0x10000)] * 7
+    p = vt.params()
+    st = lib.vtrace_from_logits(4, 8, 3, 0, *P, ctypes.byref(p), None, None, None, None, None,
+                                ctypes.c_void_p(0x20000), 1 << 20, None)
+    assert st == 1
+
+
+def test_binding_has_no_cpu_fallback(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    x = torch.zeros(2, 2, 3)
+    with pytest.raises((ValueError, RuntimeError, AssertionError)):
+        pkg.loss_and_grad(x, x, torch.zeros(2, 2, dtype=torch.int32), torch.zeros(2, 2),
+                          torch.zeros(2, 2), torch.zeros(2, 2), torch.zeros(2))

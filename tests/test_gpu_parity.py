@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle,
+element by element, on the same seeded inputs.  Tolerances are the ones
+BASELINE.json's north_star states: fp32 outputs rtol 1e-5 / atol 1e-6; bf16
+gradient store rtol 2e-2 / atol 1e-6; partial sums rel 1e-5; integer and
+bit-level properties exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1802_01561_b200 as pkg
+from paper_1802_01561_b200 import vtrace as vt
+from paper_1802_01561_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+NAMES = vt.INPUT_NAMES
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1802_01561_b200 import _build
+    _build.build()
+
+
+def _dev(inp):
+    return pkg.tensors_from_workload(inp, "cuda")
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64) if t.dtype != torch.float64 else t.cpu().numpy()
+
+
+def assert_close(name, got, ref, rtol, atol):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (name, got.shape, ref.shape)
+    err = np.abs(got - ref)
+    bad = err > atol + rtol * np.abs(ref)
+    if bad.any():
+        i = np.unravel_index(np.argmax(err / (atol + rtol * np.abs(ref))), ref.shape)
+        raise AssertionError(
+            f"{name}: {int(bad.sum())}/{bad.size} outside tol (rtol={rtol}, atol={atol}); "
+            f"worst at {i}: got {got[i]!r} ref {ref[i]!r}; max abs err {err.max():.3e}")
+
+
+def run_both(inp, **kw):
+    dev = _dev(inp)
+    args = [dev[k] for k in NAMES]
+    rm = inp.get("reward_mode", 0)
+    lg = pkg.loss_and_grad(*args, reward_mode=rm, **kw)
+    fl = pkg.from_logits(*args, reward_mode=rm, **{k: v for k, v in kw.items()
+                                                    if k not in ("baseline_cost", "entropy_cost")})
+    torch.cuda.synchronize()
+    okw = {k: v for k, v in kw.items()}
+    ref_l = oracle.loss_and_grad(inp, reward_mode=rm, **okw)
+    ref_f = oracle.from_logits(inp, reward_mode=rm, **{k: v for k, v in okw.items()
+                                                        if k not in ("baseline_cost", "entropy_cost")})
+    return lg, fl, ref_l, ref_f
+
+
+def check_all(inp, lg, fl, ref_l, ref_f):
+    bf16 = inp["dtype"] == wl.DTYPE_BF16
+    assert_close("vs", _np(lg["vs"]), ref_l["vs"], 1e-5, 1e-6)
+    assert_close("pg_advantages", _np(lg["pg_advantages"]), ref_l["pg_advantages"], 1e-5, 1e-6)
+    assert_close("grad_values", _np(lg["grad_values"]), ref_l["grad_values"], 1e-5, 1e-6)
+    assert_close("grad_target_logits", _np(lg["grad_target_logits"]), ref_l["grad_target_logits"],
+                 2e-2 if bf16 else 1e-5, 1e-6)
+    parts = lg["partials"].cpu().numpy()
+    rp = ref_l["partials"]
+    for i, n in enumerate(vt.PARTIAL_NAMES):
+        if n == "n_rho_clipped":
+            assert abs(parts[i] - rp[i]) <= max(1.0, 1e-5 * rp[i]), (n, parts[i], rp[i])
+        else:
+            assert abs(parts[i] - rp[i]) <= 1e-5 * abs(rp[i]) + 1e-9, (n, parts[i], rp[i])
+    for k in ("vs", "pg_advantages", "log_rhos", "target_action_log_probs",
+              "behaviour_action_log_probs"):
+        assert_close("from_logits." + k, _np(fl[k]), ref_f[k], 1e-5, 1e-6)
+
+
+@pytest.mark.parametrize("name", ["toy", "atari", "dmlab", "large", "stress"])
+def test_parity_full_size(name):
+    """All five BASELINE configs at full size, every element."""
+    inp = wl.inputs_for(name)
+    lg, fl, ref_l, ref_f = run_both(inp)
+    check_all(inp, lg, fl, ref_l, ref_f)
+
+
+@pytest.mark.parametrize("T,B,A,dtype", [
+    (1, 1, 1, 0), (1, 8, 18, 1), (3, 5, 7, 0), (37, 13, 9, 1), (65, 24, 18, 0),
+    (130, 40, 18, 1), (200, 16, 4, 0), (64, 64, 33, 1), (7, 3, 2, 1), (300, 9, 9, 0),
+    (129, 8, 18, 1), (59, 1000, 9, 0)])
+def test_parity_shapes(T, B, A, dtype):
+    """Ragged tiles (B % 8 != 0), T across chunk boundaries, runtime-A path,
+    generic (unaligned) path, A = 1."""
+    inp = wl.make_inputs("atari", seed=T * 1000 + B * 10 + A, T=T, B=B, A=A, dtype=dtype)
+    lg, fl, ref_l, ref_f = run_both(inp)
+    check_all(inp, lg, fl, ref_l, ref_f)
+
+
+@pytest.mark.parametrize("kw", [dict(rho_bar=2.0, c_bar=1.0), dict(rho_bar=float("inf"), c_bar=1.0),
+                                dict(lambda_=0.5), dict(lambda_=0.0),
+                                dict(rho_bar=1.0, c_bar=0.5, pg_rho_bar=0.8),
+                                dict(baseline_cost=0.25, entropy_cost=0.1)])
+def test_parity_params(kw):
+    inp = wl.make_inputs("dmlab", seed=77, B=48)
+    lg, fl, ref_l, ref_f = run_both(inp, **kw)
+    check_all(inp, lg, fl, ref_l, ref_f)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_reward_modes(mode):
+    inp = wl.make_inputs("atari", seed=5 + mode, B=64)
+    inp["reward_mode"] = mode
+    lg, fl, ref_l, ref_f = run_both(inp)
+    check_all(inp, lg, fl, ref_l, ref_f)
+
+
+def test_on_policy_log_rho_exactly_zero_and_nstep():
+    """pi == mu bitwise => log rho == 0 bitwise, vs = n-step return."""
+    inp = wl.make_inputs("large", seed=3, B=256)
+    inp["behaviour_logits"] = inp["target_logits"].copy()
+    dev = _dev(inp)
+    fl = pkg.from_logits(*[dev[k] for k in NAMES], reward_mode=inp["reward_mode"])
+    assert torch.count_nonzero(fl["log_rhos"]).item() == 0
+    ref = oracle.from_logits(inp, reward_mode=inp["reward_mode"])
+    assert_close("vs", _np(fl["vs"]), ref["vs"], 1e-5, 1e-6)
+
+
+def test_actions_and_discounts_bit_exact_roles():
+    """Gather index: distinct per-action logits make a wrong index visible in
+    target_action_log_probs; terminal steps (discount exactly 0) cut the trace."""
+    inp = wl.make_inputs("atari", seed=11, B=40)
+    A = inp["A"]
+    inp["target_logits"] = (np.arange(A, dtype=np.float32)[None, None, :] * 0.37 +
+                            inp["target_logits"] * 0).astype(np.float32)
+    dev = _dev(inp)
+    fl = pkg.from_logits(*[dev[k] for k in NAMES], reward_mode=inp["reward_mode"])
+    ref = oracle.from_logits(inp, reward_mode=inp["reward_mode"])
+    assert_close("lp", _np(fl["target_action_log_probs"]), ref["target_action_log_probs"], 1e-5,
+                 1e-6)
+
+
+def test_terminal_cut_bitwise():
+    inp = wl.make_inputs("dmlab", seed=21, B=16, T=80)
+    inp["discounts"][30, :] = 0.0
+    dev = _dev(inp)
+    a = pkg.from_logits(*[dev[k] for k in NAMES], reward_mode=inp["reward_mode"])
+    inp2 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    inp2["rewards"][31:] = 0.5
+    inp2["values"][31:] = -2.0
+    inp2["bootstrap_value"][:] = 9.0
+    dev2 = _dev(inp2)
+    b = pkg.from_logits(*[dev2[k] for k in NAMES], reward_mode=inp["reward_mode"])
+    assert torch.equal(a["vs"][:31], b["vs"][:31])
+    assert torch.equal(a["pg_advantages"][:31], b["pg_advantages"][:31])
+
+
+def test_deterministic_bitwise():
+    inp = wl.make_inputs("large", seed=4, B=2048)
+    dev = _dev(inp)
+    args = [dev[k] for k in NAMES]
+    ws = pkg.Workspace(inp["T"], inp["B"], inp["A"], inp["dtype"])
+    o1 = pkg.loss_and_grad(*args, workspace=ws, reward_mode=1)
+    o1 = {k: v.clone() for k, v in o1.items()}
+    o2 = pkg.loss_and_grad(*args, workspace=ws, reward_mode=1)
+    for k in o1:
+        assert torch.equal(o1[k], o2[k]), k
+
+
+def test_shard_equals_slice_bitwise():
+    """A learner's column shard gives bitwise the matching slice of the full run
+    (tile shapes depend only on T, A and dtype)."""
+    inp = wl.make_inputs("stress", seed=8, B=256, T=300)
+    full = pkg.loss_and_grad(*[_dev(inp)[k] for k in NAMES], reward_mode=inp["reward_mode"])
+    for b0, b1 in [(0, 128), (128, 256), (64, 192)]:
+        sh = wl.column_slice(inp, b0, b1)
+        o = pkg.loss_and_grad(*[_dev(sh)[k] for k in NAMES], reward_mode=inp["reward_mode"])
+        for k in ("grad_target_logits", "grad_values", "vs", "pg_advantages"):
+            assert torch.equal(o[k], full[k][:, b0:b1]), (k, b0, b1)
+
+
+def test_partials_of_shards_add_up():
+    inp = wl.make_inputs("large", seed=9, B=1024)
+    full = pkg.loss_and_grad(*[_dev(inp)[k] for k in NAMES], reward_mode=1)["partials"].cpu()
+    tot = torch.zeros(8, dtype=torch.float64)
+    for b0 in range(0, 1024, 256):
+        sh = wl.column_slice(inp, b0, b0 + 256)
+        tot += pkg.loss_and_grad(*[_dev(sh)[k] for k in NAMES], reward_mode=1)["partials"].cpu()
+    tot[3] = tot[0] + 0.5 * tot[1] - 0.01 * tot[2]
+    np.testing.assert_allclose(tot.numpy(), full.numpy(), rtol=1e-12)
+
+
+def test_data_errors_reported():
+    inp = wl.make_inputs("atari", seed=12, B=32)
+    ws = pkg.Workspace(inp["T"], inp["B"], inp["A"], inp["dtype"])
+    dev = _dev(inp)
+    pkg.loss_and_grad(*[dev[k] for k in NAMES], workspace=ws, reward_mode=1)
+    assert pkg.read_device_status(ws) == (0, -1)
+    bad = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    bad["actions"][7, 3] = 18
+    bad["discounts"][9, 1] = 1.5
+    bad["rewards"][2, 30] = np.nan
+    dev = _dev(bad)
+    pkg.loss_and_grad(*[dev[k] for k in NAMES], workspace=ws, reward_mode=1)
+    assert pkg.read_device_status(ws) == (3, 2 * 32 + 30)   # smallest row: reward at (2, 30)
+    assert pkg.read_device_status(ws) == (0, -1)            # read clears
+    bad2 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    bad2["target_logits"][5, 4, 2] = np.inf
+    bad2["bootstrap_value"][1] = np.nan
+    dev = _dev(bad2)
+    pkg.from_logits(*[dev[k] for k in NAMES], workspace=ws)
+    assert pkg.read_device_status(ws) == (2, 5 * 32 + 4)
+    bad3 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    bad3["bootstrap_value"][1] = np.nan
+    dev = _dev(bad3)
+    pkg.from_logits(*[dev[k] for k in NAMES], workspace=ws)
+    assert pkg.read_device_status(ws) == (4, 20 * 32 + 1)
+
+
+def test_from_host_path_matches():
+    inp = wl.make_inputs("large", seed=13, B=512)
+    host = pkg.tensors_from_workload(inp, "cpu", pin=True)
+    dev_in = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    T, B, A = inp["T"], inp["B"], inp["A"]
+    out = {"grad_target_logits": torch.empty(T, B, A, dtype=torch.bfloat16, device="cuda"),
+           "grad_values": torch.empty(T, B, device="cuda"),
+           "partials": torch.empty(8, dtype=torch.float64, device="cuda")}
+    ph = torch.zeros(8, dtype=torch.float64).pin_memory()
+    ws = pkg.Workspace(T, B, A, inp["dtype"])
+    pkg.loss_and_grad_from_host(host, dev_in, out, ws, ph, reward_mode=1)
+    torch.cuda.synchronize()
+    ref = oracle.loss_and_grad(inp, reward_mode=1)
+    np.testing.assert_allclose(ph.numpy()[:7], ref["partials"][:7], rtol=1e-5)
+
+
+def test_graph_capture_replay():
+    inp = wl.make_inputs("large", seed=14, B=1024)
+    dev = _dev(inp)
+    args = [dev[k] for k in NAMES]
+    ws = pkg.Workspace(inp["T"], inp["B"], inp["A"], inp["dtype"])
+    out = pkg.loss_and_grad(*args, workspace=ws, reward_mode=1)
+    ref = {k: v.clone() for k, v in out.items()}
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            pkg.loss_and_grad(*args, workspace=ws, reward_mode=1, out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        for v in out.values():
+            v.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for k in ref:
+            assert torch.equal(out[k], ref[k]), k
