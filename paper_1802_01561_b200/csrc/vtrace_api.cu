@@ -84,7 +84,7 @@ __device__ __forceinline__ void row_stats(const LT* zrow, int A, int a, float& m
 //   dz_j = pi_j (pg + c_e (logp_j + H))            for j != a
 //   dz_a = -pg sum_{j != a} pi_j + c_e pi_a (logp_a + H)
 // (pi_a - 1 is formed as -sum of the other pi_j: no cancellation).
-// Writes dz in place over the row; returns H, log pi(a), sum dz^2.
+// Writes dz to dzrow; returns H, log pi(a), sum dz^2.
 template <typename T>
 __device__ __forceinline__ T store_cvt(float x);
 template <>
@@ -97,8 +97,8 @@ __device__ __forceinline__ __nv_bfloat16 store_cvt<__nv_bfloat16>(float x) {
 }
 
 template <typename LT, int A_CT>
-__device__ __forceinline__ void row_epilogue(LT* zrow, int A, int a, float lse, float pg,
-                                             float ce, float& H_out, float& lpa_out,
+__device__ __forceinline__ void row_epilogue(const LT* zrow, LT* dzrow, int A, int a, float lse,
+                                             float pg, float ce, float& H_out, float& lpa_out,
                                              float& sq_out) {
   const float L = 1.44269504088896341f;
   if constexpr (A_CT > 0) {
@@ -118,7 +118,7 @@ __device__ __forceinline__ void row_epilogue(LT* zrow, int A, int a, float lse, 
     }
     float sq = 0.f;
     if constexpr (sizeof(LT) == 2 && (A_CT % 2) == 0) {
-      uint32_t* w = reinterpret_cast<uint32_t*>(zrow);
+      uint32_t* w = reinterpret_cast<uint32_t*>(dzrow);
 #pragma unroll
       for (int k = 0; k < A_CT / 2; ++k) {
         float d0 = p[2 * k] * fmaf(ce, lp[2 * k] + H, pg);
@@ -136,7 +136,7 @@ __device__ __forceinline__ void row_epilogue(LT* zrow, int A, int a, float lse, 
         float d = p[j] * fmaf(ce, lp[j] + H, pg);
         if (j == a) d = fmaf(-pg, rest, ce * pa * (lpa + H));
         sq = fmaf(d, d, sq);
-        zrow[j] = store_cvt<LT>(d);
+        dzrow[j] = store_cvt<LT>(d);
       }
     }
     H_out = H;
@@ -159,7 +159,7 @@ __device__ __forceinline__ void row_epilogue(LT* zrow, int A, int a, float lse, 
       float d = pj * fmaf(ce, lpj + H, pg);
       if (j == a) d = fmaf(-pg, rest, ce * pa * (lpa + H));
       sq = fmaf(d, d, sq);
-      zrow[j] = store_cvt<LT>(d);
+      dzrow[j] = store_cvt<LT>(d);
     }
     H_out = H;
     lpa_out = lpa;
@@ -185,16 +185,53 @@ __device__ __forceinline__ void record_bad(WsHeader* ws, long long row, int kind
 __device__ __forceinline__ size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
 
 // ---------------------------------------------------------------------------
-// The fused kernel.  Template: logits type, compile-time A (0 = runtime),
-// LOSS (loss_and_grad) vs targets only, TMA staging vs plain loads, exp mode.
+// Shared-memory layout of one CTA (host and device agree on it).
+//   NSTAGE input stages: z^pi, z^mu [Tc][8*A] (logits dtype), a, r, gamma, V [Tc][8]
+//   per-unit row statistics: ratio (f64), lse, vs, pg_adv (f32)
+//   one dlogits staging tile [Tc][8*A] (TMA-stored while the next unit runs)
+
+constexpr int NSTAGE = 2;
+
+struct Layout {
+  size_t pi, mu, a, r, g, v, stage, ratio, lse, vs, pg, dz, total;
+};
+
+__host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
+
+__host__ __device__ inline Layout make_layout(int nrow, int A, int elem) {
+  Layout L;
+  size_t off = 0;
+  L.pi = off; off = a128(off + (size_t)nrow * A * elem);
+  L.mu = off; off = a128(off + (size_t)nrow * A * elem);
+  L.a = off;  off = a128(off + (size_t)nrow * 4);
+  L.r = off;  off = a128(off + (size_t)nrow * 4);
+  L.g = off;  off = a128(off + (size_t)nrow * 4);
+  L.v = off;  off = a128(off + (size_t)nrow * 4);
+  L.stage = off;
+  off = NSTAGE * L.stage;
+  L.ratio = off; off = a128(off + (size_t)nrow * 8);
+  L.lse = off;   off = a128(off + (size_t)nrow * 4);
+  L.vs = off;    off = a128(off + (size_t)nrow * 4);
+  L.pg = off;    off = a128(off + (size_t)nrow * 4);
+  L.dz = off;    off = a128(off + (size_t)nrow * A * elem);
+  L.total = off;
+  return L;
+}
+
+// ---------------------------------------------------------------------------
+// The fused kernel.  Persistent CTAs loop over work units handed out by an
+// atomic ticket (reverse time order); a 2-stage TMA ring prefetches the next
+// unit's tiles while the current unit is computed.  Template: logits type,
+// compile-time A (0 = runtime), LOSS (loss_and_grad) vs targets only, TMA
+// staging vs plain loads, exp mode.
 
 template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE>
 __global__ void __launch_bounds__(NTHREADS)
     vtrace_fused_kernel(const Params P, const __grid_constant__ TmaMaps maps) {
   constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m exact in fp32 for bf16 inputs
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int s_unit;
+  __shared__ __align__(8) uint64_t bar[NSTAGE];
+  __shared__ int s_unit[NSTAGE];
   __shared__ unsigned int s_epoch;
   __shared__ int s_last;
   __shared__ double s_red[NWARPS][NPART];
@@ -204,303 +241,325 @@ __global__ void __launch_bounds__(NTHREADS)
   const int Tc = P.Tc;
   const int nrow = Tc * BC;
   const long long T = P.T, B = P.B;
+  const Layout L = make_layout(nrow, A, (int)sizeof(LT));
+  double* ratio_s = reinterpret_cast<double*>(smem + L.ratio);
+  float* lse_s = reinterpret_cast<float*>(smem + L.lse);
+  float* vs_s = reinterpret_cast<float*>(smem + L.vs);
+  float* pg_s = reinterpret_cast<float*>(smem + L.pg);
+  LT* dz_t = reinterpret_cast<LT*>(smem + L.dz);
 
-  // shared-memory carve-up (all tiles 128-byte aligned, dense box layout)
-  size_t off = 0;
-  LT* pi_t = reinterpret_cast<LT*>(smem + off);
-  off = align128(off + (size_t)nrow * A * sizeof(LT));
-  LT* mu_t = reinterpret_cast<LT*>(smem + off);
-  off = align128(off + (size_t)nrow * A * sizeof(LT));
-  int* a_t = reinterpret_cast<int*>(smem + off);
-  off = align128(off + (size_t)nrow * 4);
-  float* r_t = reinterpret_cast<float*>(smem + off);
-  off = align128(off + (size_t)nrow * 4);
-  float* g_t = reinterpret_cast<float*>(smem + off);
-  off = align128(off + (size_t)nrow * 4);
-  float* v_t = reinterpret_cast<float*>(smem + off);
-  off = align128(off + (size_t)nrow * 4);
-  double* ratio_s = reinterpret_cast<double*>(smem + off);
-  off = align128(off + (size_t)nrow * 8);
-  float* lse_s = reinterpret_cast<float*>(smem + off);
-  off = align128(off + (size_t)nrow * 4);
-  float* vs_s = reinterpret_cast<float*>(smem + off);
-  off = align128(off + (size_t)nrow * 4);
-  float* pg_s = reinterpret_cast<float*>(smem + off);
+  // thread 0: claim the next unit for stage `st` and start its TMA loads
+  auto claim_and_load = [&](int st) {
+    const int u = (int)atomicAdd(&P.ws->ticket, 1u);
+    s_unit[st] = u;
+    if constexpr (USE_TMA) {
+      if (u < P.units) {
+        const int kc = P.K - 1 - u / P.G;
+        const int t0 = kc * Tc;
+        const int b0 = (u % P.G) * BC;
+        unsigned char* sb = smem + (size_t)st * L.stage;
+        const uint32_t bytes =
+            (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) + 4 * (size_t)nrow * 4);
+        mbar_expect_tx(&bar[st], bytes);
+        tma_load_2d(sb + L.pi, &maps.pi, b0 * A, t0, &bar[st]);
+        tma_load_2d(sb + L.mu, &maps.mu, b0 * A, t0, &bar[st]);
+        tma_load_2d(sb + L.a, &maps.a, b0, t0, &bar[st]);
+        tma_load_2d(sb + L.r, &maps.r, b0, t0, &bar[st]);
+        tma_load_2d(sb + L.g, &maps.g, b0, t0, &bar[st]);
+        tma_load_2d(sb + L.v, &maps.v, b0, t0, &bar[st]);
+      }
+    }
+  };
 
   if (tid == 0) {
-    s_unit = (int)atomicAdd(&P.ws->ticket, 1u);
     s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch);
     if constexpr (USE_TMA) {
-      mbar_init(&bar, 1);
+      for (int st = 0; st < NSTAGE; ++st) mbar_init(&bar[st], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int st = 0; st < NSTAGE; ++st) claim_and_load(st);
   }
   __syncthreads();
-  const int u = s_unit;
   const unsigned int epoch = s_epoch & 0x3fffffffu;
-  const int kchunk = P.K - 1 - u / P.G;  // reverse time order of tickets
-  const int grp = u % P.G;
-  const int t0 = kchunk * Tc;
-  const int tlen = (int)min((long long)Tc, T - t0);
-  const long long b0 = (long long)grp * BC;
-  const int blen = (int)min((long long)BC, B - b0);
-
-  // ---- a1: stage the unit's tiles -------------------------------------------------
-  if constexpr (USE_TMA) {
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) + 4 * (size_t)nrow * 4);
-      mbar_expect_tx(&bar, bytes);
-      tma_load_2d(pi_t, &maps.pi, (int)(b0 * A), t0, &bar);
-      tma_load_2d(mu_t, &maps.mu, (int)(b0 * A), t0, &bar);
-      tma_load_2d(a_t, &maps.a, (int)b0, t0, &bar);
-      tma_load_2d(r_t, &maps.r, (int)b0, t0, &bar);
-      tma_load_2d(g_t, &maps.g, (int)b0, t0, &bar);
-      tma_load_2d(v_t, &maps.v, (int)b0, t0, &bar);
-    }
-    mbar_wait(&bar, 0);
-  } else {
-    const LT* gpi = reinterpret_cast<const LT*>(P.pi);
-    const LT* gmu = reinterpret_cast<const LT*>(P.mu);
-    const int rowlen = BC * A;
-    for (int i = tid; i < nrow * A; i += NTHREADS) {
-      const int tl = i / rowlen, rem = i - tl * rowlen, bl = rem / A, j = rem - bl * A;
-      LT zp = store_cvt<LT>(0.f), zm = store_cvt<LT>(0.f);
-      if (tl < tlen && bl < blen) {
-        const long long gi = (((long long)(t0 + tl)) * B + b0 + bl) * A + j;
-        zp = gpi[gi];
-        zm = gmu[gi];
-      }
-      pi_t[i] = zp;
-      mu_t[i] = zm;
-    }
-    for (int i = tid; i < nrow; i += NTHREADS) {
-      const int tl = i / BC, bl = i - tl * BC;
-      int av = 0;
-      float rv = 0.f, gv = 0.f, vv = 0.f;
-      if (tl < tlen && bl < blen) {
-        const long long gi = ((long long)(t0 + tl)) * B + b0 + bl;
-        av = P.actions[gi];
-        rv = P.rew[gi];
-        gv = P.disc[gi];
-        vv = P.val[gi];
-      }
-      a_t[i] = av;
-      r_t[i] = rv;
-      g_t[i] = gv;
-      v_t[i] = vv;
-    }
-    __syncthreads();
-  }
-
-  // per-thread partial sums (fp64)
-  double acc_pg = 0, acc_v = 0, acc_H = 0, acc_dz = 0, acc_dv = 0, acc_rho = 0, acc_clip = 0;
-
-  // ---- a3-a6: per-row statistics of both policies ---------------------------------
-  for (int r = tid; r < nrow; r += NTHREADS) {
-    const int tl = r >> 3, bl = r & 7;
-    if (tl >= tlen || bl >= blen) continue;
-    const long long row = (long long)(t0 + tl) * B + b0 + bl;
-    const int a_raw = a_t[r];
-    const int a = min(max(a_raw, 0), A - 1);
-    float m_p, m_m;
-    double S_p, S_m, ea_p, ea_m;
-    bool fin_p, fin_m;
-    row_stats<LT, A_CT, MODE, EXACT_DIFF>(pi_t + (size_t)r * A, A, a, m_p, S_p, ea_p, fin_p);
-    row_stats<LT, A_CT, MODE, EXACT_DIFF>(mu_t + (size_t)r * A, A, a, m_m, S_m, ea_m, fin_m);
-    // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
-    const double ratio = (ea_p * S_m) / (ea_m * S_p);
-    ratio_s[r] = ratio;
-    lse_s[r] = m_p + logf((float)S_p);
-    acc_rho += fmin(P.rho_bar, ratio);
-    acc_clip += (ratio > P.rho_bar) ? 1.0 : 0.0;
-    if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
-    if (P.has_lp)
-      P.lp_out[row] = (float)(((double)Elem<LT>::get(pi_t + (size_t)r * A, a) - (double)m_p) - log(S_p));
-    if (P.has_lm)
-      P.lm_out[row] = (float)(((double)Elem<LT>::get(mu_t + (size_t)r * A, a) - (double)m_m) - log(S_m));
-    // data checks (host cannot see the data)
-    if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
-    if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
-    if (!isfinite(r_t[r])) record_bad(P.ws, row, VT_DATA_REWARD);
-    if (!isfinite(v_t[r])) record_bad(P.ws, row, VT_DATA_VALUE);
-    const float gm = g_t[r];
-    if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
-  }
-  __syncthreads();
-
-  // ---- a2, a7-a9: reverse V-trace recursion, warp per column ----------------------
-  if (warp < blen) {
-    const int bl = warp;
-    const long long b = b0 + bl;
-    const int kk = (tlen + 31) >> 5;  // steps per lane
-    const int s_beg = min(lane * kk, tlen), s_end = min(s_beg + kk, tlen);
-    // V(x) just after this chunk: next chunk's first value, or the bootstrap
-    const bool last_chunk = (kchunk == P.K - 1);
-    double V_after;
-    if (last_chunk) {
-      V_after = (double)__ldg(P.boot + b);
-      if (lane == 0 && !isfinite((float)V_after)) record_bad(P.ws, T * B + b, VT_DATA_VALUE);
-    } else {
-      V_after = (double)__ldg(P.val + (long long)(t0 + tlen) * B + b);
-    }
-    // local affine aggregate of this lane's segment: A_beg = D + G * A_end
-    double Gl = 1.0, Dl = 0.0;
-    for (int s = s_end - 1; s >= s_beg; --s) {
-      const int r = s * BC + bl;
-      const double ratio = ratio_s[r];
-      const double rho = fmin(P.rho_bar, ratio);
-      const double c = P.lambda * fmin(P.c_bar, ratio);
-      const double gam = (double)g_t[r];
-      const double Vt = (double)v_t[r];
-      const double Vn = (s + 1 < tlen) ? (double)v_t[r + BC] : V_after;
-      const double delta = rho * (reward_transform(r_t[r], P.reward_mode) + gam * Vn - Vt);
-      Dl = fma(gam * c, Dl, delta);
-      Gl = gam * c * Gl;
-    }
-    // inclusive suffix scan over lanes: lane l <- composition of segments l..31
-    double Gi = Gl, Di = Dl;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
-      if (lane + o < 32) {
-        Di = fma(Gi, Do, Di);
-        Gi = Gi * Go;
-      }
-    }
-    // exclusive (segments l+1..31)
-    double Ge = shfl_down_d(Gi, 1), De = shfl_down_d(Di, 1);
-    if (lane == 31) {
-      Ge = 1.0;
-      De = 0.0;
-    }
-    const double Gc = __shfl_sync(0xffffffffu, Gi, 0), Dc = __shfl_sync(0xffffffffu, Di, 0);
-    // carry A at the end of this chunk (A_T = 0: v_T = V(x_T), reading c2)
-    double carry = 0.0;
-    if (P.K > 1) {
-      ColRec* rec = P.recs + (size_t)u * BC + bl;
-      if (lane == 0) {
-        if (last_chunk) {
-          rec->incl = Dc;  // A at this chunk's start; carry is 0
-          st_release_u32(&rec->flag, (epoch << 2) | 2u);
-        } else {
-          rec->G = Gc;
-          rec->D = Dc;
-          st_release_u32(&rec->flag, (epoch << 2) | 1u);
-          // look back over later-time chunks of the same columns
-          double aG = 1.0, aD = 0.0;
-          int up = u - P.G;
-          while (true) {
-            const ColRec* pr = P.recs + (size_t)up * BC + bl;
-            unsigned int f = ld_acquire_u32(&pr->flag);
-            int spins = 0;
-            while ((f >> 2) != epoch || (f & 3u) == 0u) {
-              if (++spins > 8) __nanosleep(64);
-              f = ld_acquire_u32(&pr->flag);
-            }
-            if ((f & 3u) == 2u) {
-              carry = fma(aG, __ldcg(&pr->incl), aD);
-              break;
-            }
-            const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
-            aD = fma(aG, Dp, aD);
-            aG = aG * Gp;
-            up -= P.G;
-          }
-          rec->incl = fma(Gc, carry, Dc);
-          st_release_u32(&rec->flag, (epoch << 2) | 2u);
-        }
-      }
-      carry = __shfl_sync(0xffffffffu, carry, 0);
-    }
-    // second pass over the segment: v_t, q_t, pg_adv_t
-    double A_next = fma(Ge, carry, De);  // A at s_end
-    double V_next = (s_end < tlen) ? (double)v_t[s_end * BC + bl] : V_after;
-    for (int s = s_end - 1; s >= s_beg; --s) {
-      const int r = s * BC + bl;
-      const double ratio = ratio_s[r];
-      const double rho = fmin(P.rho_bar, ratio);
-      const double c = P.lambda * fmin(P.c_bar, ratio);
-      const double rho_pg = fmin(P.pg_rho_bar, ratio);
-      const double gam = (double)g_t[r];
-      const double Vt = (double)v_t[r];
-      const double rr = reward_transform(r_t[r], P.reward_mode);
-      const double delta = rho * (rr + gam * V_next - Vt);
-      const double A_t = fma(gam * c, A_next, delta);
-      const double v_next = V_next + A_next;  // v_{t+1}; v_T = V(x_T)
-      const double adv = rho_pg * (rr + gam * v_next - Vt);
-      vs_s[r] = (float)(Vt + A_t);
-      pg_s[r] = (float)adv;
-      A_next = A_t;
-      V_next = Vt;
-    }
-  }
-  __syncthreads();
-
-  // ---- a10-a11: gradient epilogue + row outputs -----------------------------------
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
-  for (int r = tid; r < nrow; r += NTHREADS) {
-    const int tl = r >> 3, bl = r & 7;
-    if (tl >= tlen || bl >= blen) continue;
-    const long long row = (long long)(t0 + tl) * B + b0 + bl;
-    const float vsr = vs_s[r], pgr = pg_s[r], Vt = v_t[r];
-    if (P.vs) P.vs[row] = vsr;
-    if (P.pg_adv) P.pg_adv[row] = pgr;
-    if constexpr (LOSS) {
-      const int a = min(max(a_t[r], 0), A - 1);
-      float H, lpa, sq;
-      row_epilogue<LT, A_CT>(pi_t + (size_t)r * A, A, a, lse_s[r], pgr, ce, H, lpa, sq);
-      const float dv = cv * (Vt - vsr);
-      P.dvalues[row] = dv;
-      const double res = (double)vsr - (double)Vt;
-      acc_pg += -(double)pgr * (double)lpa;
-      acc_v += 0.5 * res * res;
-      acc_H += (double)H;
-      acc_dz += (double)sq;
-      acc_dv += (double)dv * (double)dv;
-      if constexpr (!USE_TMA) {
-        LT* gdz = reinterpret_cast<LT*>(P.dlogits);
-        for (int j = 0; j < A; ++j) gdz[row * A + j] = pi_t[(size_t)r * A + j];
+
+  for (int it = 0;; ++it) {
+    const int st = it % NSTAGE;
+    const int u = s_unit[st];
+    if (u >= P.units) break;  // CTA-uniform
+    unsigned char* sb = smem + (size_t)st * L.stage;
+    LT* pi_t = reinterpret_cast<LT*>(sb + L.pi);
+    LT* mu_t = reinterpret_cast<LT*>(sb + L.mu);
+    int* a_t = reinterpret_cast<int*>(sb + L.a);
+    float* r_t = reinterpret_cast<float*>(sb + L.r);
+    float* g_t = reinterpret_cast<float*>(sb + L.g);
+    float* v_t = reinterpret_cast<float*>(sb + L.v);
+    const int kchunk = P.K - 1 - u / P.G;  // reverse time order of tickets
+    const int grp = u % P.G;
+    const int t0 = kchunk * Tc;
+    const int tlen = (int)min((long long)Tc, T - t0);
+    const long long b0 = (long long)grp * BC;
+    const int blen = (int)min((long long)BC, B - b0);
+
+    // ---- a1: the unit's tiles ------------------------------------------------------
+    if constexpr (USE_TMA) {
+      mbar_wait(&bar[st], (uint32_t)((it / NSTAGE) & 1));
+    } else {
+      const LT* gpi = reinterpret_cast<const LT*>(P.pi);
+      const LT* gmu = reinterpret_cast<const LT*>(P.mu);
+      const int rowlen = BC * A;
+      for (int i = tid; i < nrow * A; i += NTHREADS) {
+        const int tl = i / rowlen, rem = i - tl * rowlen, bl = rem / A, j = rem - bl * A;
+        LT zp = store_cvt<LT>(0.f), zm = store_cvt<LT>(0.f);
+        if (tl < tlen && bl < blen) {
+          const long long gi = (((long long)(t0 + tl)) * B + b0 + bl) * A + j;
+          zp = gpi[gi];
+          zm = gmu[gi];
+        }
+        pi_t[i] = zp;
+        mu_t[i] = zm;
+      }
+      for (int i = tid; i < nrow; i += NTHREADS) {
+        const int tl = i / BC, bl = i - tl * BC;
+        int av = 0;
+        float rv = 0.f, gv = 0.f, vv = 0.f;
+        if (tl < tlen && bl < blen) {
+          const long long gi = ((long long)(t0 + tl)) * B + b0 + bl;
+          av = P.actions[gi];
+          rv = P.rew[gi];
+          gv = P.disc[gi];
+          vv = P.val[gi];
+        }
+        a_t[i] = av;
+        r_t[i] = rv;
+        g_t[i] = gv;
+        v_t[i] = vv;
+      }
+      __syncthreads();
+    }
+
+    double acc_pg = 0, acc_v = 0, acc_H = 0, acc_dz = 0, acc_dv = 0, acc_rho = 0, acc_clip = 0;
+
+    // ---- a3-a5: per-row statistics of both policies -------------------------------
+    for (int r = tid; r < nrow; r += NTHREADS) {
+      const int tl = r >> 3, bl = r & 7;
+      if (tl >= tlen || bl >= blen) continue;
+      const long long row = (long long)(t0 + tl) * B + b0 + bl;
+      const int a_raw = a_t[r];
+      const int a = min(max(a_raw, 0), A - 1);
+      float m_p, m_m;
+      double S_p, S_m, ea_p, ea_m;
+      bool fin_p, fin_m;
+      row_stats<LT, A_CT, MODE, EXACT_DIFF>(pi_t + (size_t)r * A, A, a, m_p, S_p, ea_p, fin_p);
+      row_stats<LT, A_CT, MODE, EXACT_DIFF>(mu_t + (size_t)r * A, A, a, m_m, S_m, ea_m, fin_m);
+      // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
+      const double ratio = (ea_p * S_m) / (ea_m * S_p);
+      ratio_s[r] = ratio;
+      lse_s[r] = m_p + logf((float)S_p);
+      acc_rho += fmin(P.rho_bar, ratio);
+      acc_clip += (ratio > P.rho_bar) ? 1.0 : 0.0;
+      if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
+      if (P.has_lp)
+        P.lp_out[row] =
+            (float)(((double)Elem<LT>::get(pi_t + (size_t)r * A, a) - (double)m_p) - log(S_p));
+      if (P.has_lm)
+        P.lm_out[row] =
+            (float)(((double)Elem<LT>::get(mu_t + (size_t)r * A, a) - (double)m_m) - log(S_m));
+      if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
+      if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
+      if (!isfinite(r_t[r])) record_bad(P.ws, row, VT_DATA_REWARD);
+      if (!isfinite(v_t[r])) record_bad(P.ws, row, VT_DATA_VALUE);
+      const float gm = g_t[r];
+      if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
+    }
+    __syncthreads();
+
+    // ---- a2, a7-a9: reverse V-trace recursion, warp per column --------------------
+    if (warp < blen) {
+      const int bl = warp;
+      const long long b = b0 + bl;
+      const int kk = (tlen + 31) >> 5;  // steps per lane
+      const int s_beg = min(lane * kk, tlen), s_end = min(s_beg + kk, tlen);
+      const bool last_chunk = (kchunk == P.K - 1);
+      double V_after;  // V(x) just after this chunk: next chunk's first value or bootstrap
+      if (last_chunk) {
+        V_after = (double)__ldg(P.boot + b);
+        if (lane == 0 && !isfinite((float)V_after)) record_bad(P.ws, T * B + b, VT_DATA_VALUE);
+      } else {
+        V_after = (double)__ldg(P.val + (long long)(t0 + tlen) * B + b);
+      }
+      // local affine aggregate of this lane's segment: A_beg = D + G * A_end
+      double Gl = 1.0, Dl = 0.0;
+      for (int s = s_end - 1; s >= s_beg; --s) {
+        const int r = s * BC + bl;
+        const double ratio = ratio_s[r];
+        const double rho = fmin(P.rho_bar, ratio);
+        const double c = P.lambda * fmin(P.c_bar, ratio);
+        const double gam = (double)g_t[r];
+        const double Vt = (double)v_t[r];
+        const double Vn = (s + 1 < tlen) ? (double)v_t[r + BC] : V_after;
+        const double delta = rho * (reward_transform(r_t[r], P.reward_mode) + gam * Vn - Vt);
+        Dl = fma(gam * c, Dl, delta);
+        Gl = gam * c * Gl;
+      }
+      // inclusive suffix scan over lanes: lane l <- composition of segments l..31
+      double Gi = Gl, Di = Dl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
+        if (lane + o < 32) {
+          Di = fma(Gi, Do, Di);
+          Gi = Gi * Go;
+        }
+      }
+      double Ge = shfl_down_d(Gi, 1), De = shfl_down_d(Di, 1);  // exclusive: l+1..31
+      if (lane == 31) {
+        Ge = 1.0;
+        De = 0.0;
+      }
+      const double Gc = __shfl_sync(0xffffffffu, Gi, 0), Dc = __shfl_sync(0xffffffffu, Di, 0);
+      double carry = 0.0;  // A at the end of this chunk; A_T = 0 (v_T = V(x_T), reading c2)
+      if (P.K > 1) {
+        ColRec* rec = P.recs + (size_t)u * BC + bl;
+        if (lane == 0) {
+          if (last_chunk) {
+            rec->incl = Dc;
+            st_release_u32(&rec->flag, (epoch << 2) | 2u);
+          } else {
+            rec->G = Gc;
+            rec->D = Dc;
+            st_release_u32(&rec->flag, (epoch << 2) | 1u);
+            double aG = 1.0, aD = 0.0;  // composition of the later chunks seen so far
+            int up = u - P.G;
+            while (true) {
+              const ColRec* pr = P.recs + (size_t)up * BC + bl;
+              unsigned int f = ld_acquire_u32(&pr->flag);
+              int spins = 0;
+              while ((f >> 2) != epoch || (f & 3u) == 0u) {
+                if (++spins > 8) __nanosleep(64);
+                f = ld_acquire_u32(&pr->flag);
+              }
+              if ((f & 3u) == 2u) {
+                carry = fma(aG, __ldcg(&pr->incl), aD);
+                break;
+              }
+              const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
+              aD = fma(aG, Dp, aD);
+              aG = aG * Gp;
+              up -= P.G;
+            }
+            rec->incl = fma(Gc, carry, Dc);
+            st_release_u32(&rec->flag, (epoch << 2) | 2u);
+          }
+        }
+        carry = __shfl_sync(0xffffffffu, carry, 0);
+      }
+      // second pass over the segment: v_t, q_t, pg_adv_t
+      double A_next = fma(Ge, carry, De);  // A at s_end
+      double V_next = (s_end < tlen) ? (double)v_t[s_end * BC + bl] : V_after;
+      for (int s = s_end - 1; s >= s_beg; --s) {
+        const int r = s * BC + bl;
+        const double ratio = ratio_s[r];
+        const double rho = fmin(P.rho_bar, ratio);
+        const double c = P.lambda * fmin(P.c_bar, ratio);
+        const double rho_pg = fmin(P.pg_rho_bar, ratio);
+        const double gam = (double)g_t[r];
+        const double Vt = (double)v_t[r];
+        const double rr = reward_transform(r_t[r], P.reward_mode);
+        const double delta = rho * (rr + gam * V_next - Vt);
+        const double A_t = fma(gam * c, A_next, delta);
+        const double v_next = V_next + A_next;  // v_{t+1}; v_T = V(x_T)
+        const double adv = rho_pg * (rr + gam * v_next - Vt);
+        vs_s[r] = (float)(Vt + A_t);
+        pg_s[r] = (float)adv;
+        A_next = A_t;
+        V_next = Vt;
       }
     }
-  }
-  if constexpr (LOSS && USE_TMA) {
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tma_store_2d(&maps.dz, (int)(b0 * A), t0, pi_t);
-      tma_store_commit_and_wait();
+    if constexpr (LOSS && USE_TMA) {
+      // the previous unit's dlogits store must have read dz_t before we overwrite it
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
+    __syncthreads();
+
+    // ---- a6, a10, a11: gradient epilogue + row outputs ----------------------------
+    for (int r = tid; r < nrow; r += NTHREADS) {
+      const int tl = r >> 3, bl = r & 7;
+      if (tl >= tlen || bl >= blen) continue;
+      const long long row = (long long)(t0 + tl) * B + b0 + bl;
+      const float vsr = vs_s[r], pgr = pg_s[r], Vt = v_t[r];
+      if (P.vs) P.vs[row] = vsr;
+      if (P.pg_adv) P.pg_adv[row] = pgr;
+      if constexpr (LOSS) {
+        const int a = min(max(a_t[r], 0), A - 1);
+        float H, lpa, sq;
+        row_epilogue<LT, A_CT>(pi_t + (size_t)r * A, dz_t + (size_t)r * A, A, a, lse_s[r], pgr,
+                               ce, H, lpa, sq);
+        const float dv = cv * (Vt - vsr);
+        P.dvalues[row] = dv;
+        const double res = (double)vsr - (double)Vt;
+        acc_pg += -(double)pgr * (double)lpa;
+        acc_v += 0.5 * res * res;
+        acc_H += (double)H;
+        acc_dz += (double)sq;
+        acc_dv += (double)dv * (double)dv;
+      }
+    }
+    if constexpr (LOSS && USE_TMA) fence_proxy_async_smem();
+    __syncthreads();  // stage st fully consumed; dz_t complete
+    if (tid == 0) {
+      if constexpr (LOSS && USE_TMA) {
+        tma_store_2d(&maps.dz, (int)(b0 * A), t0, dz_t);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if constexpr (USE_TMA) fence_proxy_async_smem();  // generic reads before async refill
+      claim_and_load(st);
+    }
+    if constexpr (LOSS && !USE_TMA) {
+      LT* gdz = reinterpret_cast<LT*>(P.dlogits);
+      const int rowlen = BC * A;
+      for (int i = tid; i < nrow * A; i += NTHREADS) {
+        const int tl = i / rowlen, rem = i - tl * rowlen, bl = rem / A, j = rem - bl * A;
+        if (tl < tlen && bl < blen)
+          gdz[(((long long)(t0 + tl)) * B + b0 + bl) * A + j] = dz_t[i];
+      }
+    }
+
+    // ---- a12: this unit's partial sums (fixed order: rows -> warps -> unit) --------
+    if constexpr (LOSS) {
+      double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
+#pragma unroll
+      for (int i = 0; i < NPART; ++i) {
+        double x = part[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) s_red[warp][i] = x;
+      }
+      __syncthreads();
+      if (tid < NPART) {
+        double x = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWARPS; ++w) x += s_red[w][tid];
+        P.unit_partials[(size_t)u * NPART + tid] = x;
+      }
+    }
+    __syncthreads();  // s_unit[st] (claimed above) visible; s_red free
   }
 
-  // ---- a12: partial sums, fixed-order reduction by the last CTA -------------------
-  double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
-#pragma unroll
-  for (int i = 0; i < NPART; ++i) {
-    double x = part[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s_red[warp][i] = x;
-  }
-  __syncthreads();
-  if (tid < NPART) {
-    double x = 0.0;
-#pragma unroll
-    for (int w = 0; w < NWARPS; ++w) x += s_red[w][tid];
-    P.unit_partials[(size_t)u * NPART + tid] = x;
-  }
-  __syncthreads();
+  // ---- exit: the last CTA out reduces the unit partials and re-arms the workspace --
   if (tid == 0) {
+    if constexpr (LOSS && USE_TMA) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __threadfence();
-    const unsigned int prev = atomicAdd(&P.ws->done, 1u);
-    s_last = (prev == (unsigned int)(P.units - 1));
+    const unsigned int prev = atomicAdd(&P.ws->exited, 1u);
+    s_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
   if (s_last) {
     __threadfence();
     if (LOSS && P.partials) {
-      // thread (i, lane) sums units lane, lane+32, ... of partial i in order,
-      // then lane 0 adds the 32 lane sums in order: a fixed tree.
+      // warp i sums partial i: lane l takes units l, l+32, ... in order, then the
+      // 32 lane sums are added in lane order (a fixed tree: bitwise reproducible)
       if (warp < NPART) {
         double x = 0.0;
         for (int v = lane; v < P.units; v += 32)
@@ -520,7 +579,7 @@ __global__ void __launch_bounds__(NTHREADS)
     }
     if (tid == 0) {
       P.ws->ticket = 0u;
-      P.ws->done = 0u;
+      P.ws->exited = 0u;
       __threadfence();
       *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
     }
@@ -534,6 +593,8 @@ struct Plan {
   int Tc, K, G, units;
   size_t smem;
 };
+
+constexpr size_t kMaxSmem = 220 * 1024;
 
 static int tc_max_for(int A, int elem) {
   const long long row_bytes = 2LL * A * elem + 16;
@@ -556,17 +617,7 @@ static Plan make_plan(long long T, long long B, int A, int elem) {
   }
   p.G = (int)((B + BC - 1) / BC);
   p.units = p.K * p.G;
-  const size_t nrow = (size_t)p.Tc * BC;
-  auto a128 = [](size_t x) { return (x + 127) & ~size_t(127); };
-  size_t off = 0;
-  off = a128(off + nrow * A * elem);
-  off = a128(off + nrow * A * elem);
-  for (int i = 0; i < 4; ++i) off = a128(off + nrow * 4);
-  off = a128(off + nrow * 8);
-  off = a128(off + nrow * 4);
-  off = a128(off + nrow * 4);
-  off = a128(off + nrow * 4);
-  p.smem = off;
+  p.smem = make_layout(p.Tc * BC, A, elem).total;
   return p;
 }
 
@@ -636,12 +687,24 @@ static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& pl
   auto kern = vtrace_fused_kernel<LT, A_CT, LOSS, TMA, MODE>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
+  static int num_sms = 0;
   std::call_once(once, [&] {
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024);
+                                    kMaxSmem);
+    int dev = 0;
+    if (attr_err == cudaSuccess) attr_err = cudaGetDevice(&dev);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   });
   if (attr_err != cudaSuccess) return VT_ERR_CUDA;
-  kern<<<plan.units, NTHREADS, plan.smem, st>>>(P, maps);
+  // persistent grid: every resident CTA slot, never more CTAs than units
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, plan.smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return VT_ERR_CUDA;
+  const long long grid = std::min<long long>(plan.units, (long long)per_sm * num_sms);
+  kern<<<(unsigned)grid, NTHREADS, plan.smem, st>>>(P, maps);
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
@@ -742,7 +805,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   bool tma = (A * BC <= 256) && (B * A < (1LL << 31)) && (T < (1LL << 31)) && ((B * A * elem) % 16 == 0) && ((B * 4) % 16 == 0) &&
              aligned(mu, 16) && aligned(pi, 16) && aligned(actions, 16) && aligned(disc, 16) &&
              aligned(rew, 16) && aligned(val, 16) && (!loss || aligned(dlogits, 16)) &&
-             plan.Tc <= 256 && plan.smem <= 200 * 1024;
+             plan.Tc <= 256 && plan.smem <= kMaxSmem;
   if (tma) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -754,7 +817,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
           encode_2d(&maps.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc) &&
           (!loss || encode_2d(&maps.dz, dlogits, ldt, elem, B * A, T, BC * (int)A, plan.Tc));
   }
-  if (plan.smem > 200 * 1024) return VT_ERR_SHAPE;
+  if (plan.smem > kMaxSmem) return VT_ERR_SHAPE;
   if (dt == VT_BFLOAT16) {
     return loss ? dispatch<__nv_bfloat16, true>(P, maps, plan, tma, st)
                 : dispatch<__nv_bfloat16, false>(P, maps, plan, tma, st);

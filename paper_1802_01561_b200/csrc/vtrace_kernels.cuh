@@ -39,9 +39,9 @@ constexpr int NPART = 8;
 enum ExpMode { EXP_F64 = 0, EXP_MUFU = 1 };
 
 struct alignas(16) WsHeader {
-  unsigned int ticket;
-  unsigned int done;
-  unsigned int epoch;
+  unsigned int ticket;   // next work unit to hand out
+  unsigned int exited;   // CTAs that have left the unit loop
+  unsigned int epoch;    // call counter (tags the look-back flags)
   unsigned int pad0;
   unsigned long long status;  // (row << 8) | kind, atomicMin; ~0ull = clean
   unsigned long long pad1[5];

@@ -3,6 +3,9 @@ element by element, on the same seeded inputs.  Tolerances are the ones
 BASELINE.json's north_star states: fp32 outputs rtol 1e-5 / atol 1e-6; bf16
 gradient store rtol 2e-2 / atol 1e-6; partial sums rel 1e-5; integer and
 bit-level properties exact."""
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -33,11 +36,27 @@ def _np(t):
     return t.float().cpu().numpy().astype(np.float64) if t.dtype != torch.float64 else t.cpu().numpy()
 
 
+REPORT = os.environ.get("VTRACE_PARITY_REPORT")
+
+
+def _report(name, err, ref, rtol, atol):
+    """Appends the worst err/tol ratio of an output to $VTRACE_PARITY_REPORT."""
+    if not REPORT:
+        return
+    ratio = float(np.max(err / (atol + rtol * np.abs(ref)))) if err.size else 0.0
+    with open(REPORT, "a") as f:
+        f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0],
+                            "output": name, "max_err_over_tol": ratio,
+                            "max_abs_err": float(err.max()) if err.size else 0.0,
+                            "n": int(err.size)}) + "\n")
+
+
 def assert_close(name, got, ref, rtol, atol):
     got = np.asarray(got, np.float64)
     ref = np.asarray(ref, np.float64)
     assert got.shape == ref.shape, (name, got.shape, ref.shape)
     err = np.abs(got - ref)
+    _report(name, err, ref, rtol, atol)
     bad = err > atol + rtol * np.abs(ref)
     if bad.any():
         i = np.unravel_index(np.argmax(err / (atol + rtol * np.abs(ref))), ref.shape)
@@ -189,7 +208,7 @@ def test_partials_of_shards_add_up():
     for b0 in range(0, 1024, 256):
         sh = wl.column_slice(inp, b0, b0 + 256)
         tot += pkg.loss_and_grad(*[_dev(sh)[k] for k in NAMES], reward_mode=1)["partials"].cpu()
-    tot[3] = tot[0] + 0.5 * tot[1] - 0.01 * tot[2]
+    # every partial (the total loss included) is a sum over trajectories
     np.testing.assert_allclose(tot.numpy(), full.numpy(), rtol=1e-12)
 
 
