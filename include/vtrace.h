@@ -83,7 +83,7 @@ typedef enum {
   VT_DATA_DISCOUNT = 5  /* discount non-finite or outside [0, 1]           */
 } vt_data_error;
 
-#define VT_MAX_ACTIONS 2048
+#define VT_MAX_ACTIONS 1024
 
 typedef struct {
   float clip_rho_threshold;    /* rho_bar; +INFINITY = no truncation         */

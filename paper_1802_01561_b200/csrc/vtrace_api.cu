@@ -17,74 +17,10 @@
 namespace vtb200 {
 
 // ---------------------------------------------------------------------------
-// Per-row statistics of one logits row:
-//   m = max_j z_j, S = sum_j exp(z_j - m), ea = exp(z_a - m), finite flag.
-// m is only a shift for range (reading c14); S and ea are accurate to ~1e-9.
+// Row arithmetic.  Each thread owns one row
+// (t, b) of the unit for the whole unit: it keeps the target row in registers
+// from the statistics phase to the gradient epilogue.
 
-template <typename LT, int A_CT, int MODE, bool EXACT_DIFF>
-__device__ __forceinline__ void row_stats(const LT* zrow, int A, int a, float& m, double& S,
-                                          double& ea, bool& finite) {
-  float chk = 0.f;
-  if constexpr (A_CT > 0) {
-    float z[A_CT];
-    load_row<LT, A_CT>(zrow, z);
-    m = z[0];
-#pragma unroll
-    for (int j = 0; j < A_CT; ++j) {
-      m = fmaxf(m, z[j]);
-      chk = __fmaf_rn(z[j], 0.f, chk);  // NaN iff some z_j is inf/nan
-    }
-    if constexpr (MODE == EXP_F64) {
-      const double m64 = (double)m;
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < A_CT; ++j) acc += exp64_nonpos((double)z[j] - m64);
-      S = acc;
-    } else {
-      float s_hi = 1.f, s_lo = 0.f;  // s_hi starts at 1 >= every term: Fast2Sum is exact
-#pragma unroll
-      for (int j = 0; j < A_CT; ++j) {
-        float e = exp_mufu<EXACT_DIFF>(z[j], m);
-        float s = s_hi + e;
-        s_lo += (s_hi - s) + e;
-        s_hi = s;
-      }
-      S = (double)(s_hi - 1.f) + (double)s_lo;
-    }
-  } else {
-    m = Elem<LT>::get(zrow, 0);
-    for (int j = 0; j < A; ++j) {
-      float zj = Elem<LT>::get(zrow, j);
-      m = fmaxf(m, zj);
-      chk = __fmaf_rn(zj, 0.f, chk);
-    }
-    const double m64 = (double)m;
-    double acc = 0.0;
-    if constexpr (MODE == EXP_F64) {
-      for (int j = 0; j < A; ++j) acc += exp64_nonpos((double)Elem<LT>::get(zrow, j) - m64);
-      S = acc;
-    } else {
-      float s_hi = 1.f, s_lo = 0.f;
-      for (int j = 0; j < A; ++j) {
-        float e = exp_mufu<EXACT_DIFF>(Elem<LT>::get(zrow, j), m);
-        float s = s_hi + e;
-        s_lo += (s_hi - s) + e;
-        s_hi = s;
-      }
-      S = (double)(s_hi - 1.f) + (double)s_lo;
-    }
-  }
-  // the gathered term in fp64 in both modes (it enters the ratio undamped)
-  ea = exp64_nonpos((double)Elem<LT>::get(zrow, a) - (double)m);
-  finite = (chk == 0.f) && (m == m);
-}
-
-// Gradient epilogue of one row, fp32:
-//   logp_j = z_j - lse, pi_j = exp(logp_j), H = -sum pi_j logp_j,
-//   dz_j = pi_j (pg + c_e (logp_j + H))            for j != a
-//   dz_a = -pg sum_{j != a} pi_j + c_e pi_a (logp_a + H)
-// (pi_a - 1 is formed as -sum of the other pi_j: no cancellation).
-// Writes dz to dzrow; returns H, log pi(a), sum dz^2.
 template <typename T>
 __device__ __forceinline__ T store_cvt(float x);
 template <>
@@ -96,81 +32,116 @@ __device__ __forceinline__ __nv_bfloat16 store_cvt<__nv_bfloat16>(float x) {
   return __float2bfloat16_rn(x);
 }
 
+// A logits row held in registers (compile-time A) or read from smem (A_CT == 0).
 template <typename LT, int A_CT>
-__device__ __forceinline__ void row_epilogue(const LT* zrow, LT* dzrow, int A, int a, float lse,
-                                             float pg, float ce, float& H_out, float& lpa_out,
-                                             float& sq_out) {
-  const float L = 1.44269504088896341f;
-  if constexpr (A_CT > 0) {
-    float z[A_CT];
-    load_row<LT, A_CT>(zrow, z);
-    float lp[A_CT], p[A_CT];
-    float H = 0.f, rest = 0.f, lpa = 0.f, pa = 0.f;
+struct RowRegs {
+  static constexpr bool kPacked = (sizeof(LT) == 2) && (A_CT % 2 == 0) && (A_CT > 0);
+  static constexpr int kWords = kPacked ? A_CT / 2 : (A_CT > 0 ? A_CT : 1);
+  uint32_t w[kWords];
+  const LT* src;
+  __device__ __forceinline__ void load(const LT* row) {
+    src = row;
+    if constexpr (kPacked) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(row);
 #pragma unroll
-    for (int j = 0; j < A_CT; ++j) {
-      lp[j] = z[j] - lse;
-      p[j] = ex2_approx(lp[j] * L);
-      H = fmaf(-p[j], lp[j], H);
-      const bool isa = (j == a);
-      rest += isa ? 0.f : p[j];
-      lpa = isa ? lp[j] : lpa;
-      pa = isa ? p[j] : pa;
-    }
-    float sq = 0.f;
-    if constexpr (sizeof(LT) == 2 && (A_CT % 2) == 0) {
-      uint32_t* w = reinterpret_cast<uint32_t*>(dzrow);
+      for (int k = 0; k < kWords; ++k) w[k] = p[k];
+    } else if constexpr (A_CT > 0) {
+      if constexpr (sizeof(LT) == 4 && (A_CT % 2) == 0) {
+        const float2* p = reinterpret_cast<const float2*>(row);
 #pragma unroll
-      for (int k = 0; k < A_CT / 2; ++k) {
-        float d0 = p[2 * k] * fmaf(ce, lp[2 * k] + H, pg);
-        float d1 = p[2 * k + 1] * fmaf(ce, lp[2 * k + 1] + H, pg);
-        if (2 * k == a) d0 = fmaf(-pg, rest, ce * pa * (lpa + H));
-        if (2 * k + 1 == a) d1 = fmaf(-pg, rest, ce * pa * (lpa + H));
-        sq = fmaf(d0, d0, sq);
-        sq = fmaf(d1, d1, sq);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(d0, d1);
-        w[k] = *reinterpret_cast<uint32_t*>(&h2);
+        for (int k = 0; k < A_CT / 2; ++k) {
+          float2 x = p[k];
+          w[2 * k] = __float_as_uint(x.x);
+          w[2 * k + 1] = __float_as_uint(x.y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < A_CT; ++j) w[j] = __float_as_uint(Elem<LT>::get(row, j));
       }
+    }
+  }
+  __device__ __forceinline__ float get(int j) const {  // j compile-time in unrolled loops
+    if constexpr (kPacked) {
+      const uint32_t x = w[j >> 1];
+      return (j & 1) ? __uint_as_float(x & 0xffff0000u) : __uint_as_float(x << 16);
+    } else if constexpr (A_CT > 0) {
+      return __uint_as_float(w[j]);
     } else {
+      return Elem<LT>::get(src, j);
+    }
+  }
+};
+
+// Statistics of one logits row: m = max z, S = sum_j exp(z_j - m) (accurate to
+// ~1e-8 relative), ea = exp(z_a - m) in fp64, and sed = sum_j e_j (z_j - m)
+// (for the entropy, fp32).  MUFU mode: ex2.approx on the fp32 argument, whose
+// rounding residual (and, for fp32 logits, that of z - m) enters as a
+// first-order correction sum_j e_j * ln2 * residual_j; the e_j are added with
+// Fast2Sum (s_hi starts at 1 >= every term, so each step is exact).
+template <typename LT, int A_CT, int MODE>
+__device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int a, float& m,
+                                          double& S, double& ea, float& sed, bool& finite) {
+  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m is exact in fp32 for bf16 inputs
+  constexpr int NA = A_CT > 0 ? A_CT : 1;
+  const int nA = A_CT > 0 ? A_CT : A;
+  m = R.get(0);
 #pragma unroll
-      for (int j = 0; j < A_CT; ++j) {
-        float d = p[j] * fmaf(ce, lp[j] + H, pg);
-        if (j == a) d = fmaf(-pg, rest, ce * pa * (lpa + H));
-        sq = fmaf(d, d, sq);
-        dzrow[j] = store_cvt<LT>(d);
+  for (int j = 1; j < NA; ++j) m = fmaxf(m, R.get(j));
+  if constexpr (A_CT == 0)
+    for (int j = 1; j < nA; ++j) m = fmaxf(m, R.get(j));
+  float s_hi = 1.f, s_lo = 0.f, res = 0.f, sd = 0.f;
+  double S64 = 0.0;
+  float chk = 0.f;
+  auto term = [&](float z) {
+    const float d = z - m;
+    if constexpr (MODE == EXP_F64) {
+      const double e = exp64_nonpos((double)z - (double)m);
+      S64 += e;
+      sd = fmaf((float)e, d, sd);
+      chk = __fmaf_rn(z, 0.f, chk);
+    } else {
+      const float L = 1.44269502f;  // fp32(log2 e); log2 e - L = 1.925963e-8
+      const float y = d * L;
+      float y_lo = fmaf(d, L, -y);
+      if constexpr (!EXACT_DIFF) {
+        const float bb = d - z;  // TwoSum residual of the fp32 difference z - m
+        const float d_lo = (z - (d - bb)) + (-m - bb);
+        y_lo = fmaf(d_lo, L, y_lo);
       }
+      const float e = ex2_approx(y);
+      res = fmaf(e, y_lo, res);
+      sd = fmaf(e, d, sd);
+      const float s = s_hi + e;
+      s_lo += (s_hi - s) + e;
+      s_hi = s;
     }
-    H_out = H;
-    lpa_out = lpa;
-    sq_out = sq;
+  };
+  if constexpr (A_CT > 0) {
+#pragma unroll
+    for (int j = 0; j < A_CT; ++j) term(R.get(j));
   } else {
-    float H = 0.f, rest = 0.f;
-    for (int j = 0; j < A; ++j) {
-      float lpj = Elem<LT>::get(zrow, j) - lse;
-      float pj = ex2_approx(lpj * L);
-      H = fmaf(-pj, lpj, H);
-      rest += (j == a) ? 0.f : pj;
-    }
-    const float lpa = Elem<LT>::get(zrow, a) - lse;
-    const float pa = ex2_approx(lpa * L);
-    float sq = 0.f;
-    for (int j = 0; j < A; ++j) {
-      float lpj = Elem<LT>::get(zrow, j) - lse;
-      float pj = ex2_approx(lpj * L);
-      float d = pj * fmaf(ce, lpj + H, pg);
-      if (j == a) d = fmaf(-pg, rest, ce * pa * (lpa + H));
-      sq = fmaf(d, d, sq);
-      dzrow[j] = store_cvt<LT>(d);
-    }
-    H_out = H;
-    lpa_out = lpa;
-    sq_out = sq;
+    for (int j = 0; j < nA; ++j) term(R.get(j));
+  }
+  const float za = Elem<LT>::get(R.src, a);
+  ea = exp64_nonpos((double)za - (double)m);
+  sed = sd;
+  if constexpr (MODE == EXP_F64) {
+    S = S64;
+    finite = (chk == 0.f) && (m == m);
+  } else {
+    // sum_j e_j (1 + ln2 (y_lo_j + d_j * (log2e - L)))
+    const float corr = fmaf(sd, 1.925963e-08f * 0.693147182f, res * 0.693147182f);
+    S = (double)(s_hi - 1.f) + (double)(s_lo + corr);
+    // any inf/nan logit turns S into NaN: +inf -> m = inf -> d = nan; nan -> d = nan;
+    // -inf -> y_lo = fma(-inf, L, +inf) = nan
+    finite = isfinite(S) && isfinite(m);
   }
 }
 
 __device__ __forceinline__ double reward_transform(float r, int mode) {
+  if (mode == 1) return (double)fminf(1.f, fmaxf(-1.f, r));  // P:944 (exact in fp32)
   double x = (double)r;
-  if (mode == 1) return fmin(1.0, fmax(-1.0, x));
-  if (mode == 2) {                                  // P:819
+  if (mode == 2) {  // P:819
     double th = tanh(x);
     return 0.3 * fmin(th, 0.0) + 5.0 * fmax(th, 0.0);
   }
@@ -182,18 +153,16 @@ __device__ __forceinline__ void record_bad(WsHeader* ws, long long row, int kind
   atomicMin(&ws->status, key);
 }
 
-__device__ __forceinline__ size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
-
 // ---------------------------------------------------------------------------
 // Shared-memory layout of one CTA (host and device agree on it).
 //   NSTAGE input stages: z^pi, z^mu [Tc][8*A] (logits dtype), a, r, gamma, V [Tc][8]
-//   per-unit row statistics: ratio (f64), lse, vs, pg_adv (f32)
+//   per-unit row values: ratio (f64), vs, pg_adv, A = v - V (f32)
 //   one dlogits staging tile [Tc][8*A] (TMA-stored while the next unit runs)
 
 constexpr int NSTAGE = 2;
 
 struct Layout {
-  size_t pi, mu, a, r, g, v, stage, ratio, lse, vs, pg, dz, total;
+  size_t pi, mu, a, r, g, v, stage, ratio, vs, pg, adv, dz, total;
 };
 
 __host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
@@ -210,30 +179,30 @@ __host__ __device__ inline Layout make_layout(int nrow, int A, int elem) {
   L.stage = off;
   off = NSTAGE * L.stage;
   L.ratio = off; off = a128(off + (size_t)nrow * 8);
-  L.lse = off;   off = a128(off + (size_t)nrow * 4);
   L.vs = off;    off = a128(off + (size_t)nrow * 4);
   L.pg = off;    off = a128(off + (size_t)nrow * 4);
+  L.adv = off;   off = a128(off + (size_t)nrow * 4);
   L.dz = off;    off = a128(off + (size_t)nrow * A * elem);
   L.total = off;
   return L;
 }
 
 // ---------------------------------------------------------------------------
-// The fused kernel.  Persistent CTAs loop over work units handed out by an
-// atomic ticket (reverse time order); a 2-stage TMA ring prefetches the next
-// unit's tiles while the current unit is computed.  Template: logits type,
-// compile-time A (0 = runtime), LOSS (loss_and_grad) vs targets only, TMA
-// staging vs plain loads, exp mode.
+// The fused kernel.  A cooperative (co-resident) persistent grid; CTA c owns
+// units c, c + grid, c + 2 grid, ... (unit ids run in reverse time order, so a
+// unit only ever waits on units of earlier rounds or of the same round, all
+// resident).  A 2-stage TMA ring prefetches the CTA's next unit while the
+// current one is computed.  Each thread owns one row (Tc * 8 <= 256).
 
 template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE>
 __global__ void __launch_bounds__(NTHREADS)
     vtrace_fused_kernel(const Params P, const __grid_constant__ TmaMaps maps) {
-  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m exact in fp32 for bf16 inputs
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[NSTAGE];
-  __shared__ int s_unit[NSTAGE];
   __shared__ unsigned int s_epoch;
   __shared__ int s_last;
+  __shared__ double s_agg[BC][2];
+  __shared__ double s_incl[BC];
   __shared__ double s_red[NWARPS][NPART];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -243,15 +212,13 @@ __global__ void __launch_bounds__(NTHREADS)
   const long long T = P.T, B = P.B;
   const Layout L = make_layout(nrow, A, (int)sizeof(LT));
   double* ratio_s = reinterpret_cast<double*>(smem + L.ratio);
-  float* lse_s = reinterpret_cast<float*>(smem + L.lse);
   float* vs_s = reinterpret_cast<float*>(smem + L.vs);
   float* pg_s = reinterpret_cast<float*>(smem + L.pg);
+  float* adv_s = reinterpret_cast<float*>(smem + L.adv);
   LT* dz_t = reinterpret_cast<LT*>(smem + L.dz);
+  const int stride = (int)gridDim.x;
 
-  // thread 0: claim the next unit for stage `st` and start its TMA loads
-  auto claim_and_load = [&](int st) {
-    const int u = (int)atomicAdd(&P.ws->ticket, 1u);
-    s_unit[st] = u;
+  auto load_unit = [&](int u, int st) {  // thread 0 only
     if constexpr (USE_TMA) {
       if (u < P.units) {
         const int kc = P.K - 1 - u / P.G;
@@ -276,18 +243,21 @@ __global__ void __launch_bounds__(NTHREADS)
     if constexpr (USE_TMA) {
       for (int st = 0; st < NSTAGE; ++st) mbar_init(&bar[st], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int st = 0; st < NSTAGE; ++st) load_unit((int)blockIdx.x + st * stride, st);
     }
-    for (int st = 0; st < NSTAGE; ++st) claim_and_load(st);
   }
   __syncthreads();
   const unsigned int epoch = s_epoch & 0x3fffffffu;
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
 
-  for (int it = 0;; ++it) {
+  // per-thread partial sums over all rows this thread owns (fixed order)
+  float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
+        acc_clip = 0.f;
+
+  int it = 0;
+  for (int u = (int)blockIdx.x; u < P.units; u += stride, ++it) {
     const int st = it % NSTAGE;
-    const int u = s_unit[st];
-    if (u >= P.units) break;  // CTA-uniform
     unsigned char* sb = smem + (size_t)st * L.stage;
     LT* pi_t = reinterpret_cast<LT*>(sb + L.pi);
     LT* mu_t = reinterpret_cast<LT*>(sb + L.mu);
@@ -295,12 +265,13 @@ __global__ void __launch_bounds__(NTHREADS)
     float* r_t = reinterpret_cast<float*>(sb + L.r);
     float* g_t = reinterpret_cast<float*>(sb + L.g);
     float* v_t = reinterpret_cast<float*>(sb + L.v);
-    const int kchunk = P.K - 1 - u / P.G;  // reverse time order of tickets
+    const int kchunk = P.K - 1 - u / P.G;  // unit ids run in reverse time order
     const int grp = u % P.G;
     const int t0 = kchunk * Tc;
     const int tlen = (int)min((long long)Tc, T - t0);
     const long long b0 = (long long)grp * BC;
     const int blen = (int)min((long long)BC, B - b0);
+    const bool last_chunk = (kchunk == P.K - 1);
 
     // ---- a1: the unit's tiles ------------------------------------------------------
     if constexpr (USE_TMA) {
@@ -339,33 +310,39 @@ __global__ void __launch_bounds__(NTHREADS)
       __syncthreads();
     }
 
-    double acc_pg = 0, acc_v = 0, acc_H = 0, acc_dz = 0, acc_dv = 0, acc_rho = 0, acc_clip = 0;
-
-    // ---- a3-a5: per-row statistics of both policies -------------------------------
-    for (int r = tid; r < nrow; r += NTHREADS) {
-      const int tl = r >> 3, bl = r & 7;
-      if (tl >= tlen || bl >= blen) continue;
-      const long long row = (long long)(t0 + tl) * B + b0 + bl;
+    // ---- a3-a5: statistics of this thread's row, both policies -----------------------
+    const int r = tid;  // row r = t_local * 8 + b_local
+    const int tl = r >> 3, bl = r & 7;
+    const bool row_ok = (r < nrow) && (tl < tlen) && (bl < blen);
+    const long long row = (long long)(t0 + tl) * B + b0 + bl;
+    RowRegs<LT, A_CT> zp;
+    int a = 0;
+    float lse = 0.f, cshift = 0.f, rest = 0.f, pa = 0.f;
+    if (row_ok) {
       const int a_raw = a_t[r];
-      const int a = min(max(a_raw, 0), A - 1);
-      float m_p, m_m;
+      a = min(max(a_raw, 0), A - 1);
+      RowRegs<LT, A_CT> zm;
+      zp.load(pi_t + (size_t)r * A);
+      zm.load(mu_t + (size_t)r * A);
+      float m_p, m_m, sed_p, sed_m;
       double S_p, S_m, ea_p, ea_m;
       bool fin_p, fin_m;
-      row_stats<LT, A_CT, MODE, EXACT_DIFF>(pi_t + (size_t)r * A, A, a, m_p, S_p, ea_p, fin_p);
-      row_stats<LT, A_CT, MODE, EXACT_DIFF>(mu_t + (size_t)r * A, A, a, m_m, S_m, ea_m, fin_m);
+      row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, ea_p, sed_p, fin_p);
+      row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
       // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
       const double ratio = (ea_p * S_m) / (ea_m * S_p);
       ratio_s[r] = ratio;
-      lse_s[r] = m_p + logf((float)S_p);
-      acc_rho += fmin(P.rho_bar, ratio);
-      acc_clip += (ratio > P.rho_bar) ? 1.0 : 0.0;
+      const float Sf = (float)S_p;
+      const float inv_S = 1.f / Sf;
+      lse = m_p + __logf(Sf);              // log sum_j exp(z_j)
+      cshift = m_p + sed_p * inv_S;        // lse - H: log pi_j + H = z_j - cshift
+      rest = (float)((S_p - ea_p) / S_p);  // 1 - pi(a), without cancellation
+      pa = (float)(ea_p / S_p);
+      acc_rho += (float)fmin(P.rho_bar, ratio);
+      acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
       if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
-      if (P.has_lp)
-        P.lp_out[row] =
-            (float)(((double)Elem<LT>::get(pi_t + (size_t)r * A, a) - (double)m_p) - log(S_p));
-      if (P.has_lm)
-        P.lm_out[row] =
-            (float)(((double)Elem<LT>::get(mu_t + (size_t)r * A, a) - (double)m_m) - log(S_m));
+      if (P.has_lp) P.lp_out[row] = (float)log(ea_p / S_p);
+      if (P.has_lm) P.lm_out[row] = (float)log(ea_m / S_m);
       if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
       if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
       if (!isfinite(r_t[r])) record_bad(P.ws, row, VT_DATA_REWARD);
@@ -375,36 +352,34 @@ __global__ void __launch_bounds__(NTHREADS)
     }
     __syncthreads();
 
-    // ---- a2, a7-a9: reverse V-trace recursion, warp per column --------------------
-    if (warp < blen) {
-      const int bl = warp;
-      const long long b = b0 + bl;
-      const int kk = (tlen + 31) >> 5;  // steps per lane
-      const int s_beg = min(lane * kk, tlen), s_end = min(s_beg + kk, tlen);
-      const bool last_chunk = (kchunk == P.K - 1);
-      double V_after;  // V(x) just after this chunk: next chunk's first value or bootstrap
-      if (last_chunk) {
-        V_after = (double)__ldg(P.boot + b);
-        if (lane == 0 && !isfinite((float)V_after)) record_bad(P.ws, T * B + b, VT_DATA_VALUE);
+    // ---- a2, a7-a9: reverse V-trace recursion; warp = column, lane = step ------------
+    // Each step is the affine map A_t = delta_t + (gamma_t c_t) A_{t+1} on A = v - V
+    // (Remark 1); a suffix scan composes (G1,D1)o(G2,D2) = (G1 G2, D1 + G1 D2).
+    double Gi = 1.0, Di = 0.0, Vt = 0.0, Vn = 0.0, rr = 0.0, gam = 0.0, rho_pg = 0.0;
+    const bool col_ok = warp < blen;  // warp-uniform
+    const bool step_ok = col_ok && lane < tlen;
+    if (step_ok) {
+      const int q = lane * BC + warp;
+      const double ratio = ratio_s[q];
+      const double rho = fmin(P.rho_bar, ratio);
+      const double c = P.lambda * fmin(P.c_bar, ratio);
+      rho_pg = fmin(P.pg_rho_bar, ratio);
+      gam = (double)g_t[q];
+      Vt = (double)v_t[q];
+      if (lane + 1 < tlen) {
+        Vn = (double)v_t[q + BC];
+      } else if (last_chunk) {
+        const float bv = __ldg(P.boot + b0 + warp);
+        if (!isfinite(bv)) record_bad(P.ws, T * B + b0 + warp, VT_DATA_VALUE);
+        Vn = (double)bv;
       } else {
-        V_after = (double)__ldg(P.val + (long long)(t0 + tlen) * B + b);
+        Vn = (double)__ldg(P.val + (long long)(t0 + tlen) * B + b0 + warp);
       }
-      // local affine aggregate of this lane's segment: A_beg = D + G * A_end
-      double Gl = 1.0, Dl = 0.0;
-      for (int s = s_end - 1; s >= s_beg; --s) {
-        const int r = s * BC + bl;
-        const double ratio = ratio_s[r];
-        const double rho = fmin(P.rho_bar, ratio);
-        const double c = P.lambda * fmin(P.c_bar, ratio);
-        const double gam = (double)g_t[r];
-        const double Vt = (double)v_t[r];
-        const double Vn = (s + 1 < tlen) ? (double)v_t[r + BC] : V_after;
-        const double delta = rho * (reward_transform(r_t[r], P.reward_mode) + gam * Vn - Vt);
-        Dl = fma(gam * c, Dl, delta);
-        Gl = gam * c * Gl;
-      }
-      // inclusive suffix scan over lanes: lane l <- composition of segments l..31
-      double Gi = Gl, Di = Dl;
+      rr = reward_transform(r_t[q], P.reward_mode);
+      Di = rho * (rr + gam * Vn - Vt);  // delta_t V
+      Gi = gam * c;
+    }
+    if (col_ok) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
@@ -413,141 +388,180 @@ __global__ void __launch_bounds__(NTHREADS)
           Gi = Gi * Go;
         }
       }
-      double Ge = shfl_down_d(Gi, 1), De = shfl_down_d(Di, 1);  // exclusive: l+1..31
-      if (lane == 31) {
-        Ge = 1.0;
-        De = 0.0;
+    }
+    // carry = A at the end of this chunk (A_T = 0: v_T = V(x_T), reading c2), from
+    // the later-time chunks by decoupled look-back on per-unit flags
+    double carry = 0.0;
+    if (P.K > 1) {
+      if (col_ok && lane == 0) {
+        s_agg[warp][0] = Gi;
+        s_agg[warp][1] = Di;
       }
-      const double Gc = __shfl_sync(0xffffffffu, Gi, 0), Dc = __shfl_sync(0xffffffffu, Di, 0);
-      double carry = 0.0;  // A at the end of this chunk; A_T = 0 (v_T = V(x_T), reading c2)
-      if (P.K > 1) {
-        ColRec* rec = P.recs + (size_t)u * BC + bl;
-        if (lane == 0) {
+      __syncthreads();
+      unsigned int* flags = P.flags;
+      if (kchunk > 0 && warp == 0) {  // chunk 0 is never looked back at
+        if (lane < blen) {
+          ColRec* rec = P.recs + (size_t)u * BC + lane;
           if (last_chunk) {
-            rec->incl = Dc;
-            st_release_u32(&rec->flag, (epoch << 2) | 2u);
+            rec->incl = s_agg[lane][1];
           } else {
-            rec->G = Gc;
-            rec->D = Dc;
-            st_release_u32(&rec->flag, (epoch << 2) | 1u);
-            double aG = 1.0, aD = 0.0;  // composition of the later chunks seen so far
-            int up = u - P.G;
-            while (true) {
-              const ColRec* pr = P.recs + (size_t)up * BC + bl;
-              unsigned int f = ld_acquire_u32(&pr->flag);
-              int spins = 0;
-              while ((f >> 2) != epoch || (f & 3u) == 0u) {
-                if (++spins > 8) __nanosleep(64);
-                f = ld_acquire_u32(&pr->flag);
-              }
-              if ((f & 3u) == 2u) {
-                carry = fma(aG, __ldcg(&pr->incl), aD);
-                break;
-              }
-              const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
-              aD = fma(aG, Dp, aD);
-              aG = aG * Gp;
-              up -= P.G;
+            rec->G = s_agg[lane][0];
+            rec->D = s_agg[lane][1];
+          }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_u32(flags + u, (epoch << 2) | (last_chunk ? 2u : 1u));
+      }
+      if (!last_chunk && col_ok) {
+        if (lane == 0) {
+          double aG = 1.0, aD = 0.0;  // composition of the later chunks seen so far
+          int up = u - P.G;
+          while (true) {
+            unsigned int f = ld_acquire_u32(flags + up);
+            int spins = 0;
+            while ((f >> 2) != epoch || (f & 3u) == 0u) {
+              if (++spins > 4) __nanosleep(32);
+              f = ld_acquire_u32(flags + up);
             }
-            rec->incl = fma(Gc, carry, Dc);
-            st_release_u32(&rec->flag, (epoch << 2) | 2u);
+            const ColRec* pr = P.recs + (size_t)up * BC + warp;
+            if ((f & 3u) == 2u) {
+              carry = fma(aG, __ldcg(&pr->incl), aD);
+              break;
+            }
+            const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
+            aD = fma(aG, Dp, aD);
+            aG = aG * Gp;
+            up -= P.G;
           }
         }
         carry = __shfl_sync(0xffffffffu, carry, 0);
       }
-      // second pass over the segment: v_t, q_t, pg_adv_t
-      double A_next = fma(Ge, carry, De);  // A at s_end
-      double V_next = (s_end < tlen) ? (double)v_t[s_end * BC + bl] : V_after;
-      for (int s = s_end - 1; s >= s_beg; --s) {
-        const int r = s * BC + bl;
-        const double ratio = ratio_s[r];
-        const double rho = fmin(P.rho_bar, ratio);
-        const double c = P.lambda * fmin(P.c_bar, ratio);
-        const double rho_pg = fmin(P.pg_rho_bar, ratio);
-        const double gam = (double)g_t[r];
-        const double Vt = (double)v_t[r];
-        const double rr = reward_transform(r_t[r], P.reward_mode);
-        const double delta = rho * (rr + gam * V_next - Vt);
-        const double A_t = fma(gam * c, A_next, delta);
-        const double v_next = V_next + A_next;  // v_{t+1}; v_T = V(x_T)
-        const double adv = rho_pg * (rr + gam * v_next - Vt);
-        vs_s[r] = (float)(Vt + A_t);
-        pg_s[r] = (float)adv;
-        A_next = A_t;
-        V_next = Vt;
+    }
+    if (col_ok) {
+      const double A_t = fma(Gi, carry, Di);            // A_t = v_t - V(x_t)
+      const double A_n = shfl_down_d(A_t, 1);           // A_{t+1} (lane tlen: = carry)
+      if (step_ok) {
+        const double v_next = Vn + (lane + 1 < 32 ? A_n : carry);  // v_{t+1}
+        const double adv = rho_pg * (rr + gam * v_next - Vt);        // P:242, P:257
+        const int q = lane * BC + warp;
+        vs_s[q] = (float)(Vt + A_t);
+        pg_s[q] = (float)adv;
+        adv_s[q] = (float)A_t;
+      }
+      if (P.K > 1 && kchunk > 0 && !last_chunk && lane == 0) s_incl[warp] = A_t;
+    }
+    if (P.K > 1 && kchunk > 0 && !last_chunk) {
+      __syncthreads();
+      if (warp == 0) {
+        if (lane < blen) P.recs[(size_t)u * BC + lane].incl = s_incl[lane];
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_u32(P.flags + u, (epoch << 2) | 2u);
       }
     }
     if constexpr (LOSS && USE_TMA) {
-      // the previous unit's dlogits store must have read dz_t before we overwrite it
+      // the previous unit's dlogits store must have read dz_t before it is overwritten
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     __syncthreads();
 
-    // ---- a6, a10, a11: gradient epilogue + row outputs ----------------------------
-    for (int r = tid; r < nrow; r += NTHREADS) {
-      const int tl = r >> 3, bl = r & 7;
-      if (tl >= tlen || bl >= blen) continue;
-      const long long row = (long long)(t0 + tl) * B + b0 + bl;
-      const float vsr = vs_s[r], pgr = pg_s[r], Vt = v_t[r];
+    // ---- a6, a10, a11: gradient epilogue of this thread's row ----------------------
+    if (row_ok) {
+      const float vsr = vs_s[r], pgr = pg_s[r], Ar = adv_s[r];
       if (P.vs) P.vs[row] = vsr;
       if (P.pg_adv) P.pg_adv[row] = pgr;
       if constexpr (LOSS) {
-        const int a = min(max(a_t[r], 0), A - 1);
-        float H, lpa, sq;
-        row_epilogue<LT, A_CT>(pi_t + (size_t)r * A, dz_t + (size_t)r * A, A, a, lse_s[r], pgr,
-                               ce, H, lpa, sq);
-        const float dv = cv * (Vt - vsr);
+        const float L2E = 1.44269504088896341f;
+        const float lseL = lse * L2E;
+        LT* dzrow = dz_t + (size_t)r * A;
+        float sq = 0.f;
+        auto dz_of = [&](float z) {  // pi_j (pg + c_e (log pi_j + H))
+          const float p = ex2_approx(fmaf(z, L2E, -lseL));
+          return p * fmaf(ce, z - cshift, pgr);
+        };
+        if constexpr (RowRegs<LT, A_CT>::kPacked) {
+          uint32_t* w = reinterpret_cast<uint32_t*>(dzrow);
+#pragma unroll
+          for (int k = 0; k < A_CT / 2; ++k) {
+            const float d0 = dz_of(zp.get(2 * k)), d1 = dz_of(zp.get(2 * k + 1));
+            sq = fmaf(d0, d0, sq);
+            sq = fmaf(d1, d1, sq);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(d0, d1);
+            w[k] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+        } else if constexpr (A_CT > 0) {
+#pragma unroll
+          for (int j = 0; j < A_CT; ++j) {
+            const float d = dz_of(zp.get(j));
+            sq = fmaf(d, d, sq);
+            dzrow[j] = store_cvt<LT>(d);
+          }
+        } else {
+          for (int j = 0; j < A; ++j) {
+            const float d = dz_of(zp.get(j));
+            sq = fmaf(d, d, sq);
+            dzrow[j] = store_cvt<LT>(d);
+          }
+        }
+        // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
+        const float za = Elem<LT>::get(zp.src, a);
+        const float d_wrong = dz_of(za);
+        const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
+        dzrow[a] = store_cvt<LT>(d_a);
+        sq = fmaf(d_a, d_a, fmaf(-d_wrong, d_wrong, sq));
+        const float dv = -cv * Ar;  // c_v (V - v)
         P.dvalues[row] = dv;
-        const double res = (double)vsr - (double)Vt;
-        acc_pg += -(double)pgr * (double)lpa;
-        acc_v += 0.5 * res * res;
-        acc_H += (double)H;
-        acc_dz += (double)sq;
-        acc_dv += (double)dv * (double)dv;
+        acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)
+        acc_v = fmaf(0.5f * Ar, Ar, acc_v);
+        acc_H += lse - cshift;  // H = lse - (lse - H)
+        acc_dz += sq;
+        acc_dv = fmaf(dv, dv, acc_dv);
       }
     }
     if constexpr (LOSS && USE_TMA) fence_proxy_async_smem();
-    __syncthreads();  // stage st fully consumed; dz_t complete
+    __syncthreads();  // stage st consumed; dz_t complete
     if (tid == 0) {
       if constexpr (LOSS && USE_TMA) {
         tma_store_2d(&maps.dz, (int)(b0 * A), t0, dz_t);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      if constexpr (USE_TMA) fence_proxy_async_smem();  // generic reads before async refill
-      claim_and_load(st);
+      if constexpr (USE_TMA) {
+        fence_proxy_async_smem();  // generic reads of the stage before its async refill
+        load_unit(u + NSTAGE * stride, st);
+      }
     }
     if constexpr (LOSS && !USE_TMA) {
       LT* gdz = reinterpret_cast<LT*>(P.dlogits);
       const int rowlen = BC * A;
       for (int i = tid; i < nrow * A; i += NTHREADS) {
-        const int tl = i / rowlen, rem = i - tl * rowlen, bl = rem / A, j = rem - bl * A;
-        if (tl < tlen && bl < blen)
-          gdz[(((long long)(t0 + tl)) * B + b0 + bl) * A + j] = dz_t[i];
-      }
-    }
-
-    // ---- a12: this unit's partial sums (fixed order: rows -> warps -> unit) --------
-    if constexpr (LOSS) {
-      double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
-#pragma unroll
-      for (int i = 0; i < NPART; ++i) {
-        double x = part[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0) s_red[warp][i] = x;
+        const int tl2 = i / rowlen, rem = i - tl2 * rowlen, bl2 = rem / A, j = rem - bl2 * A;
+        if (tl2 < tlen && bl2 < blen)
+          gdz[(((long long)(t0 + tl2)) * B + b0 + bl2) * A + j] = dz_t[i];
       }
       __syncthreads();
-      if (tid < NPART) {
-        double x = 0.0;
-#pragma unroll
-        for (int w = 0; w < NWARPS; ++w) x += s_red[w][tid];
-        P.unit_partials[(size_t)u * NPART + tid] = x;
-      }
     }
-    __syncthreads();  // s_unit[st] (claimed above) visible; s_red free
   }
 
-  // ---- exit: the last CTA out reduces the unit partials and re-arms the workspace --
+  // ---- a12: CTA partials (fixed order), then the last CTA out reduces them ---------
+  {
+    const double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
+#pragma unroll
+    for (int i = 0; i < NPART; ++i) {
+      double x = part[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) s_red[warp][i] = x;
+    }
+    __syncthreads();
+    if (tid < NPART) {
+      double x = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWARPS; ++w) x += s_red[w][tid];
+      P.cta_partials[(size_t)blockIdx.x * NPART + tid] = x;
+    }
+  }
+  __syncthreads();
   if (tid == 0) {
     if constexpr (LOSS && USE_TMA) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __threadfence();
@@ -558,12 +572,10 @@ __global__ void __launch_bounds__(NTHREADS)
   if (s_last) {
     __threadfence();
     if (LOSS && P.partials) {
-      // warp i sums partial i: lane l takes units l, l+32, ... in order, then the
-      // 32 lane sums are added in lane order (a fixed tree: bitwise reproducible)
-      if (warp < NPART) {
+      if (warp < NPART) {  // warp i: partial i; lanes stride the CTAs, then lane order
         double x = 0.0;
-        for (int v = lane; v < P.units; v += 32)
-          x += __ldcg(P.unit_partials + (size_t)v * NPART + warp);
+        for (int v = lane; v < (int)gridDim.x; v += 32)
+          x += __ldcg(P.cta_partials + (size_t)v * NPART + warp);
         double tot = 0.0;
         for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, x, l);
         if (lane == 0) s_red[warp][0] = tot;
@@ -578,7 +590,6 @@ __global__ void __launch_bounds__(NTHREADS)
       }
     }
     if (tid == 0) {
-      P.ws->ticket = 0u;
       P.ws->exited = 0u;
       __threadfence();
       *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
@@ -595,13 +606,15 @@ struct Plan {
 };
 
 constexpr size_t kMaxSmem = 220 * 1024;
+constexpr int kMaxCtas = 4096;  // bound on the persistent grid (workspace sizing)
 
+// Tc (steps per unit) depends only on (T, A, dtype): at most 32 so that a
+// unit's Tc * 8 rows map one-to-one onto the 256 threads, and small enough for
+// two input stages plus the staging tile to fit in shared memory.
 static int tc_max_for(int A, int elem) {
-  const long long row_bytes = 2LL * A * elem + 16;
-  long long tc = 40960 / (BC * row_bytes);
-  if (tc > 64) tc = 64;
-  if (tc < 1) tc = 1;
-  return (int)tc;
+  for (int tc = 32; tc > 1; --tc)
+    if (make_layout(tc * BC, A, elem).total <= 100 * 1024) return tc;
+  return 1;
 }
 
 static Plan make_plan(long long T, long long B, int A, int elem) {
@@ -621,9 +634,20 @@ static Plan make_plan(long long T, long long B, int A, int elem) {
   return p;
 }
 
-static size_t ws_bytes_for(const Plan& p) {
-  return 256 + (size_t)p.units * BC * sizeof(ColRec) + (size_t)p.units * NPART * sizeof(double);
+struct WsLayout {
+  size_t flags, recs, cta, total;
+};
+
+static WsLayout ws_layout(const Plan& p) {
+  WsLayout w;
+  w.flags = 256;
+  w.recs = a128(w.flags + (size_t)p.units * 4);
+  w.cta = a128(w.recs + (size_t)p.units * BC * sizeof(ColRec));
+  w.total = w.cta + (size_t)kMaxCtas * NPART * sizeof(double);
+  return w;
 }
+
+static size_t ws_bytes_for(const Plan& p) { return ws_layout(p).total; }
 
 // ---- device / driver queries ---------------------------------------------------------
 static std::mutex g_mu;
@@ -675,8 +699,9 @@ static bool encode_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, 
 static int exp_mode() {
   static int mode = -1;
   if (mode < 0) {
+    // default: compensated MUFU exps; VTRACE_EXP_MODE=f64 selects fp64 exps (reference mode)
     const char* e = getenv("VTRACE_EXP_MODE");
-    mode = (e && (e[0] == 'm' || e[0] == 'M' || e[0] == '1')) ? EXP_MUFU : EXP_F64;
+    mode = (e && (e[0] == 'f' || e[0] == 'F' || e[0] == '0')) ? EXP_F64 : EXP_MUFU;
   }
   return mode;
 }
@@ -697,14 +722,27 @@ static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& pl
       attr_err = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   });
   if (attr_err != cudaSuccess) return VT_ERR_CUDA;
-  // persistent grid: every resident CTA slot, never more CTAs than units
+  // persistent, co-resident grid: every CTA slot of the device, never more CTAs
+  // than units (cooperative launch guarantees co-residency for the look-back)
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, plan.smem) !=
           cudaSuccess ||
       per_sm < 1)
     return VT_ERR_CUDA;
-  const long long grid = std::min<long long>(plan.units, (long long)per_sm * num_sms);
-  kern<<<(unsigned)grid, NTHREADS, plan.smem, st>>>(P, maps);
+  const long long grid =
+      std::min<long long>({(long long)plan.units, (long long)per_sm * num_sms, (long long)kMaxCtas});
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, P, maps) != cudaSuccess) return VT_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
@@ -795,9 +833,10 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   P.c_e = loss ? (double)w->entropy_cost : 0.0;
   unsigned char* wsb = static_cast<unsigned char*>(ws);
   P.ws = reinterpret_cast<WsHeader*>(wsb);
-  P.recs = reinterpret_cast<ColRec*>(wsb + 256);
-  P.unit_partials =
-      reinterpret_cast<double*>(wsb + 256 + (size_t)plan.units * BC * sizeof(ColRec));
+  const WsLayout wl = ws_layout(plan);
+  P.flags = reinterpret_cast<unsigned int*>(wsb + wl.flags);
+  P.recs = reinterpret_cast<ColRec*>(wsb + wl.recs);
+  P.cta_partials = reinterpret_cast<double*>(wsb + wl.cta);
 
   // TMA eligibility: 16-byte aligned bases and row pitches, box inner <= 256 elements
   TmaMaps maps;

@@ -1,11 +1,10 @@
 // vtrace_kernels.cuh -- fused V-trace + actor-critic loss + gradient kernel for sm_100a.
 //
-// One CTA processes one work unit = (column group of BC=8 trajectories) x
-// (time chunk of Tc steps).  Units are handed out by an atomic ticket in
-// REVERSE time order, so the unit holding the later chunk of a column group
-// always started earlier; the reverse V-trace recursion (Remark 1)
-// crosses chunk boundaries through a decoupled look-back on per-unit
-// affine aggregates (G, D):  A_start = D + G * A_end  with A = v - V.
+// A work unit = (column group of BC=8 trajectories) x (time chunk of Tc <= 32
+// steps); unit ids run in REVERSE time order.  A co-resident persistent grid
+// walks the units round-robin; the reverse V-trace recursion (Remark 1)
+// crosses chunk boundaries through a decoupled look-back on per-unit affine
+// aggregates (G, D):  A_start = D + G * A_end  with A = v - V.
 //
 // Phases inside a unit:
 //   a1  stage: TMA 2D tile loads of z^pi, z^mu [Tc][BC*A] and a, r, gamma, V [Tc][BC]
@@ -39,7 +38,7 @@ constexpr int NPART = 8;
 enum ExpMode { EXP_F64 = 0, EXP_MUFU = 1 };
 
 struct alignas(16) WsHeader {
-  unsigned int ticket;   // next work unit to hand out
+  unsigned int pad_t;
   unsigned int exited;   // CTAs that have left the unit loop
   unsigned int epoch;    // call counter (tags the look-back flags)
   unsigned int pad0;
@@ -47,13 +46,11 @@ struct alignas(16) WsHeader {
   unsigned long long pad1[5];
 };
 
-// Decoupled look-back record of one (unit, column): published by lane 0 of
-// the column's warp.  flag = (epoch << 2) | state; state 1 = aggregate (G, D)
-// of the chunk, state 2 = inclusive carry (A = v - V at the chunk's first step).
+// Decoupled look-back record of one (unit, column).  The unit's flag
+// (epoch << 2) | state says what is published: state 1 = the chunk's affine
+// aggregate (G, D), state 2 = the inclusive carry (A = v - V at its first step).
 struct alignas(16) ColRec {
-  unsigned int flag;
-  unsigned int pad;
-  double G, D, incl;
+  double G, D, incl, pad;
 };
 static_assert(sizeof(ColRec) == 32, "ColRec layout");
 
@@ -80,8 +77,9 @@ struct Params {
   double c_v, c_e;
   int reward_mode;
   WsHeader* ws;
+  unsigned int* flags;
   ColRec* recs;
-  double* unit_partials;
+  double* cta_partials;
 };
 
 struct TmaMaps {
