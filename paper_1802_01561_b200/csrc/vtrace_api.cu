@@ -156,43 +156,84 @@ __device__ __forceinline__ void record_bad(WsHeader* ws, long long row, int kind
 // ---------------------------------------------------------------------------
 // Shared-memory layout of one CTA (host and device agree on it).
 //   NSTAGE input stages: z^pi, z^mu [Tc][8*A] (logits dtype), a, r, gamma, V [Tc][8]
-//   per-unit row values: ratio (f64), vs, pg_adv, A = v - V (f32)
+//   2 row-state buffers (by unit parity): ratio (f64), lse, lse - H, 1 - pi(a)
+//   2 scan-output buffers (by unit parity): v, pg_adv, A = v - V (f32)
 //   one dlogits staging tile [Tc][8*A] (TMA-stored while the next unit runs)
 
-constexpr int NSTAGE = 2;
+constexpr int NSTAGE = 3;
+constexpr int NROWWARPS = NWARPS - 1;       // warps 0..6 own rows, warp 7 runs the scan
+constexpr int NROWTHREADS = NROWWARPS * 32;  // 224 >= Tc * 8
 
 struct Layout {
-  size_t pi, mu, a, r, g, v, stage, ratio, vs, pg, adv, dz, total;
+  size_t pi, mu, a, r, g, v, stage;               // offsets inside a stage
+  size_t ratio[2], lse[2], csh[2], rest[2];      // row state
+  size_t vs[2], pg[2], adv[2];                   // scan output
+  size_t dz, total;
 };
 
 __host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Big tiles 128-byte aligned, small [Tc][8] arrays 16-byte aligned (TMA minimum).
 __host__ __device__ inline Layout make_layout(int nrow, int A, int elem) {
   Layout L;
   size_t off = 0;
   L.pi = off; off = a128(off + (size_t)nrow * A * elem);
   L.mu = off; off = a128(off + (size_t)nrow * A * elem);
-  L.a = off;  off = a128(off + (size_t)nrow * 4);
-  L.r = off;  off = a128(off + (size_t)nrow * 4);
-  L.g = off;  off = a128(off + (size_t)nrow * 4);
+  L.a = off;  off = a16(off + (size_t)nrow * 4);
+  L.r = off;  off = a16(off + (size_t)nrow * 4);
+  L.g = off;  off = a16(off + (size_t)nrow * 4);
   L.v = off;  off = a128(off + (size_t)nrow * 4);
   L.stage = off;
   off = NSTAGE * L.stage;
-  L.ratio = off; off = a128(off + (size_t)nrow * 8);
-  L.vs = off;    off = a128(off + (size_t)nrow * 4);
-  L.pg = off;    off = a128(off + (size_t)nrow * 4);
-  L.adv = off;   off = a128(off + (size_t)nrow * 4);
-  L.dz = off;    off = a128(off + (size_t)nrow * A * elem);
+  for (int p = 0; p < 2; ++p) {
+    L.ratio[p] = off; off = a16(off + (size_t)nrow * 8);
+    L.lse[p] = off;   off = a16(off + (size_t)nrow * 4);
+    L.csh[p] = off;   off = a16(off + (size_t)nrow * 4);
+    L.rest[p] = off;  off = a16(off + (size_t)nrow * 4);
+    L.vs[p] = off;    off = a16(off + (size_t)nrow * 4);
+    L.pg[p] = off;    off = a16(off + (size_t)nrow * 4);
+    L.adv[p] = off;   off = a16(off + (size_t)nrow * 4);
+  }
+  off = a128(off);
+  L.dz = off; off = a128(off + (size_t)nrow * A * elem);
   L.total = off;
   return L;
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// geometry of one work unit
+struct Unit {
+  int u, kchunk, t0, tlen, blen;
+  long long b0;
+  bool last_chunk;
+  __device__ __forceinline__ void set(int uu, const Params& P) {
+    u = uu;
+    kchunk = P.K - 1 - uu / P.G;  // unit ids run in reverse time order
+    t0 = kchunk * P.Tc;
+    tlen = (int)min((long long)P.Tc, P.T - t0);
+    b0 = (long long)(uu % P.G) * BC;
+    blen = (int)min((long long)BC, P.B - b0);
+    last_chunk = (kchunk == P.K - 1);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // The fused kernel.  A cooperative (co-resident) persistent grid; CTA c owns
-// units c, c + grid, c + 2 grid, ... (unit ids run in reverse time order, so a
-// unit only ever waits on units of earlier rounds or of the same round, all
-// resident).  A 2-stage TMA ring prefetches the CTA's next unit while the
-// current one is computed.  Each thread owns one row (Tc * 8 <= 256).
+// units c, c + grid, ...  (unit ids run in reverse time order, so a unit only
+// ever waits, in the look-back, on units of earlier or the same rounds, all
+// resident).  Warp-specialised software pipeline over the CTA's units; in
+// iteration i:
+//   row warps 0..6 : P1(i)  row statistics of unit i  (stage i%3 -> row state i%2)
+//   scan warp 7    : SCAN(i-1) reverse recursion of unit i-1 (row state (i-1)%2 ->
+//                    scan output (i-1)%2), look-back, publication
+//   -- barrier 1 (256) --
+//   row warps      : P3(i-1) gradient epilogue of unit i-1 -> dz tile -> TMA store;
+//                    stage (i-1)%3 is refilled with unit i+2
+// so the latency-bound recursion overlaps the row arithmetic of the next unit.
 
 template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE>
 __global__ void __launch_bounds__(NTHREADS)
@@ -201,8 +242,6 @@ __global__ void __launch_bounds__(NTHREADS)
   __shared__ __align__(8) uint64_t bar[NSTAGE];
   __shared__ unsigned int s_epoch;
   __shared__ int s_last;
-  __shared__ double s_agg[BC][2];
-  __shared__ double s_incl[BC];
   __shared__ double s_red[NWARPS][NPART];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -211,335 +250,368 @@ __global__ void __launch_bounds__(NTHREADS)
   const int nrow = Tc * BC;
   const long long T = P.T, B = P.B;
   const Layout L = make_layout(nrow, A, (int)sizeof(LT));
-  double* ratio_s = reinterpret_cast<double*>(smem + L.ratio);
-  float* vs_s = reinterpret_cast<float*>(smem + L.vs);
-  float* pg_s = reinterpret_cast<float*>(smem + L.pg);
-  float* adv_s = reinterpret_cast<float*>(smem + L.adv);
-  LT* dz_t = reinterpret_cast<LT*>(smem + L.dz);
   const int stride = (int)gridDim.x;
-
-  auto load_unit = [&](int u, int st) {  // thread 0 only
-    if constexpr (USE_TMA) {
-      if (u < P.units) {
-        const int kc = P.K - 1 - u / P.G;
-        const int t0 = kc * Tc;
-        const int b0 = (u % P.G) * BC;
-        unsigned char* sb = smem + (size_t)st * L.stage;
-        const uint32_t bytes =
-            (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) + 4 * (size_t)nrow * 4);
-        mbar_expect_tx(&bar[st], bytes);
-        tma_load_2d(sb + L.pi, &maps.pi, b0 * A, t0, &bar[st]);
-        tma_load_2d(sb + L.mu, &maps.mu, b0 * A, t0, &bar[st]);
-        tma_load_2d(sb + L.a, &maps.a, b0, t0, &bar[st]);
-        tma_load_2d(sb + L.r, &maps.r, b0, t0, &bar[st]);
-        tma_load_2d(sb + L.g, &maps.g, b0, t0, &bar[st]);
-        tma_load_2d(sb + L.v, &maps.v, b0, t0, &bar[st]);
-      }
-    }
-  };
+  const int n_my = (P.units - (int)blockIdx.x + stride - 1) / stride;  // units of this CTA
 
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch);
     if constexpr (USE_TMA) {
       for (int st = 0; st < NSTAGE; ++st) mbar_init(&bar[st], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int st = 0; st < NSTAGE; ++st) load_unit((int)blockIdx.x + st * stride, st);
     }
   }
   __syncthreads();
   const unsigned int epoch = s_epoch & 0x3fffffffu;
+
+  // TMA: unit i of this CTA -> stage i % NSTAGE
+  auto load_unit = [&](int i) {
+    if constexpr (USE_TMA) {
+      if (i < n_my) {
+        Unit U;
+        U.set((int)blockIdx.x + i * stride, P);
+        const int st = i % NSTAGE;
+        unsigned char* sb = smem + (size_t)st * L.stage;
+        const uint32_t bytes =
+            (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) + 4 * (size_t)nrow * 4);
+        mbar_expect_tx(&bar[st], bytes);
+        const int xb = (int)(U.b0 * A);
+        tma_load_2d(sb + L.pi, &maps.pi, xb, U.t0, &bar[st]);
+        tma_load_2d(sb + L.mu, &maps.mu, xb, U.t0, &bar[st]);
+        tma_load_2d(sb + L.a, &maps.a, (int)U.b0, U.t0, &bar[st]);
+        tma_load_2d(sb + L.r, &maps.r, (int)U.b0, U.t0, &bar[st]);
+        tma_load_2d(sb + L.g, &maps.g, (int)U.b0, U.t0, &bar[st]);
+        tma_load_2d(sb + L.v, &maps.v, (int)U.b0, U.t0, &bar[st]);
+      }
+    }
+  };
+  if (USE_TMA && tid == 0)
+    for (int i = 0; i < NSTAGE; ++i) load_unit(i);
+
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
-
-  // per-thread partial sums over all rows this thread owns (fixed order)
+  // per-thread partial sums (fixed assignment of rows to threads: deterministic)
   float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
         acc_clip = 0.f;
 
-  int it = 0;
-  for (int u = (int)blockIdx.x; u < P.units; u += stride, ++it) {
-    const int st = it % NSTAGE;
-    unsigned char* sb = smem + (size_t)st * L.stage;
-    LT* pi_t = reinterpret_cast<LT*>(sb + L.pi);
-    LT* mu_t = reinterpret_cast<LT*>(sb + L.mu);
-    int* a_t = reinterpret_cast<int*>(sb + L.a);
-    float* r_t = reinterpret_cast<float*>(sb + L.r);
-    float* g_t = reinterpret_cast<float*>(sb + L.g);
-    float* v_t = reinterpret_cast<float*>(sb + L.v);
-    const int kchunk = P.K - 1 - u / P.G;  // unit ids run in reverse time order
-    const int grp = u % P.G;
-    const int t0 = kchunk * Tc;
-    const int tlen = (int)min((long long)Tc, T - t0);
-    const long long b0 = (long long)grp * BC;
-    const int blen = (int)min((long long)BC, B - b0);
-    const bool last_chunk = (kchunk == P.K - 1);
-
-    // ---- a1: the unit's tiles ------------------------------------------------------
-    if constexpr (USE_TMA) {
-      mbar_wait(&bar[st], (uint32_t)((it / NSTAGE) & 1));
-    } else {
-      const LT* gpi = reinterpret_cast<const LT*>(P.pi);
-      const LT* gmu = reinterpret_cast<const LT*>(P.mu);
-      const int rowlen = BC * A;
-      for (int i = tid; i < nrow * A; i += NTHREADS) {
-        const int tl = i / rowlen, rem = i - tl * rowlen, bl = rem / A, j = rem - bl * A;
-        LT zp = store_cvt<LT>(0.f), zm = store_cvt<LT>(0.f);
-        if (tl < tlen && bl < blen) {
-          const long long gi = (((long long)(t0 + tl)) * B + b0 + bl) * A + j;
-          zp = gpi[gi];
-          zm = gmu[gi];
+  for (int i = 0; i <= n_my; ++i) {
+    // ================= phase A: P1(i) on row warps || SCAN(i-1) on the scan warp ====
+    if (warp < NROWWARPS) {
+      if (i < n_my) {
+        Unit U;
+        U.set((int)blockIdx.x + i * stride, P);
+        const int st = i % NSTAGE, par = i & 1;
+        unsigned char* sb = smem + (size_t)st * L.stage;
+        const LT* pi_t = reinterpret_cast<const LT*>(sb + L.pi);
+        const LT* mu_t = reinterpret_cast<const LT*>(sb + L.mu);
+        if constexpr (USE_TMA) {
+          mbar_wait(&bar[st], (uint32_t)((i / NSTAGE) & 1));
+        } else {
+          // plain staged loads (unaligned shapes): row warps fill the stage
+          LT* wpi = reinterpret_cast<LT*>(sb + L.pi);
+          LT* wmu = reinterpret_cast<LT*>(sb + L.mu);
+          int* wa = reinterpret_cast<int*>(sb + L.a);
+          float* wr = reinterpret_cast<float*>(sb + L.r);
+          float* wg = reinterpret_cast<float*>(sb + L.g);
+          float* wv = reinterpret_cast<float*>(sb + L.v);
+          const LT* gpi = reinterpret_cast<const LT*>(P.pi);
+          const LT* gmu = reinterpret_cast<const LT*>(P.mu);
+          const int rowlen = BC * A;
+          for (int k = tid; k < nrow * A; k += NROWTHREADS) {
+            const int tl = k / rowlen, rem = k - tl * rowlen, bl = rem / A, j = rem - bl * A;
+            LT zp = store_cvt<LT>(0.f), zm = store_cvt<LT>(0.f);
+            if (tl < U.tlen && bl < U.blen) {
+              const long long gi = (((long long)(U.t0 + tl)) * B + U.b0 + bl) * A + j;
+              zp = gpi[gi];
+              zm = gmu[gi];
+            }
+            wpi[k] = zp;
+            wmu[k] = zm;
+          }
+          for (int k = tid; k < nrow; k += NROWTHREADS) {
+            const int tl = k / BC, bl = k - tl * BC;
+            int av = 0;
+            float rv = 0.f, gv = 0.f, vv = 0.f;
+            if (tl < U.tlen && bl < U.blen) {
+              const long long gi = ((long long)(U.t0 + tl)) * B + U.b0 + bl;
+              av = P.actions[gi];
+              rv = P.rew[gi];
+              gv = P.disc[gi];
+              vv = P.val[gi];
+            }
+            wa[k] = av;
+            wr[k] = rv;
+            wg[k] = gv;
+            wv[k] = vv;
+          }
+          named_bar_sync(2, NROWTHREADS);
         }
-        pi_t[i] = zp;
-        mu_t[i] = zm;
-      }
-      for (int i = tid; i < nrow; i += NTHREADS) {
-        const int tl = i / BC, bl = i - tl * BC;
-        int av = 0;
-        float rv = 0.f, gv = 0.f, vv = 0.f;
-        if (tl < tlen && bl < blen) {
-          const long long gi = ((long long)(t0 + tl)) * B + b0 + bl;
-          av = P.actions[gi];
-          rv = P.rew[gi];
-          gv = P.disc[gi];
-          vv = P.val[gi];
+        const int r = tid;
+        const int tl = r >> 3, bl = r & 7;
+        if (r < nrow && tl < U.tlen && bl < U.blen) {
+          const int* a_t = reinterpret_cast<const int*>(sb + L.a);
+          const float* r_t = reinterpret_cast<const float*>(sb + L.r);
+          const float* g_t = reinterpret_cast<const float*>(sb + L.g);
+          const float* v_t = reinterpret_cast<const float*>(sb + L.v);
+          const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
+          const int a_raw = a_t[r];
+          const int a = min(max(a_raw, 0), A - 1);
+          RowRegs<LT, A_CT> zp, zm;
+          zp.load(pi_t + (size_t)r * A);
+          zm.load(mu_t + (size_t)r * A);
+          float m_p, m_m, sed_p, sed_m;
+          double S_p, S_m, ea_p, ea_m;
+          bool fin_p, fin_m;
+          row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, ea_p, sed_p, fin_p);
+          row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
+          // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
+          const double ratio = (ea_p * S_m) / (ea_m * S_p);
+          const float Sf = (float)S_p, inv_S = __frcp_rn(Sf);
+          reinterpret_cast<double*>(smem + L.ratio[par])[r] = ratio;
+          const float lse = m_p + __logf(Sf);  // log sum_j exp(z_j)
+          reinterpret_cast<float*>(smem + L.lse[par])[r] = lse;
+          reinterpret_cast<float*>(smem + L.csh[par])[r] = m_p + sed_p * inv_S;  // lse - H
+          reinterpret_cast<float*>(smem + L.rest[par])[r] = (float)(S_p - ea_p) * inv_S;
+          acc_rho += (float)fmin(P.rho_bar, ratio);
+          acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
+          if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
+          if (P.has_lp) P.lp_out[row] = (float)log(ea_p / S_p);
+          if (P.has_lm) P.lm_out[row] = (float)log(ea_m / S_m);
+          if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
+          if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
+          if (!isfinite(r_t[r])) record_bad(P.ws, row, VT_DATA_REWARD);
+          if (!isfinite(v_t[r])) record_bad(P.ws, row, VT_DATA_VALUE);
+          const float gm = g_t[r];
+          if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
         }
-        a_t[i] = av;
-        r_t[i] = rv;
-        g_t[i] = gv;
-        v_t[i] = vv;
       }
-      __syncthreads();
-    }
-
-    // ---- a3-a5: statistics of this thread's row, both policies -----------------------
-    const int r = tid;  // row r = t_local * 8 + b_local
-    const int tl = r >> 3, bl = r & 7;
-    const bool row_ok = (r < nrow) && (tl < tlen) && (bl < blen);
-    const long long row = (long long)(t0 + tl) * B + b0 + bl;
-    RowRegs<LT, A_CT> zp;
-    int a = 0;
-    float lse = 0.f, cshift = 0.f, rest = 0.f, pa = 0.f;
-    if (row_ok) {
-      const int a_raw = a_t[r];
-      a = min(max(a_raw, 0), A - 1);
-      RowRegs<LT, A_CT> zm;
-      zp.load(pi_t + (size_t)r * A);
-      zm.load(mu_t + (size_t)r * A);
-      float m_p, m_m, sed_p, sed_m;
-      double S_p, S_m, ea_p, ea_m;
-      bool fin_p, fin_m;
-      row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, ea_p, sed_p, fin_p);
-      row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
-      // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
-      const double ratio = (ea_p * S_m) / (ea_m * S_p);
-      ratio_s[r] = ratio;
-      const float Sf = (float)S_p;
-      const float inv_S = 1.f / Sf;
-      lse = m_p + __logf(Sf);              // log sum_j exp(z_j)
-      cshift = m_p + sed_p * inv_S;        // lse - H: log pi_j + H = z_j - cshift
-      rest = (float)((S_p - ea_p) / S_p);  // 1 - pi(a), without cancellation
-      pa = (float)(ea_p / S_p);
-      acc_rho += (float)fmin(P.rho_bar, ratio);
-      acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
-      if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
-      if (P.has_lp) P.lp_out[row] = (float)log(ea_p / S_p);
-      if (P.has_lm) P.lm_out[row] = (float)log(ea_m / S_m);
-      if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
-      if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
-      if (!isfinite(r_t[r])) record_bad(P.ws, row, VT_DATA_REWARD);
-      if (!isfinite(v_t[r])) record_bad(P.ws, row, VT_DATA_VALUE);
-      const float gm = g_t[r];
-      if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
-    }
-    __syncthreads();
-
-    // ---- a2, a7-a9: reverse V-trace recursion; warp = column, lane = step ------------
-    // Each step is the affine map A_t = delta_t + (gamma_t c_t) A_{t+1} on A = v - V
-    // (Remark 1); a suffix scan composes (G1,D1)o(G2,D2) = (G1 G2, D1 + G1 D2).
-    double Gi = 1.0, Di = 0.0, Vt = 0.0, Vn = 0.0, rr = 0.0, gam = 0.0, rho_pg = 0.0;
-    const bool col_ok = warp < blen;  // warp-uniform
-    const bool step_ok = col_ok && lane < tlen;
-    if (step_ok) {
-      const int q = lane * BC + warp;
-      const double ratio = ratio_s[q];
-      const double rho = fmin(P.rho_bar, ratio);
-      const double c = P.lambda * fmin(P.c_bar, ratio);
-      rho_pg = fmin(P.pg_rho_bar, ratio);
-      gam = (double)g_t[q];
-      Vt = (double)v_t[q];
-      if (lane + 1 < tlen) {
-        Vn = (double)v_t[q + BC];
-      } else if (last_chunk) {
-        const float bv = __ldg(P.boot + b0 + warp);
-        if (!isfinite(bv)) record_bad(P.ws, T * B + b0 + warp, VT_DATA_VALUE);
-        Vn = (double)bv;
-      } else {
-        Vn = (double)__ldg(P.val + (long long)(t0 + tlen) * B + b0 + warp);
+    } else if (i >= 1) {
+      // ---- SCAN(i-1): warp 7.  Lane 4c + s owns column c, segment s of 4 --------
+      Unit U;
+      U.set((int)blockIdx.x + (i - 1) * stride, P);
+      const int st = (i - 1) % NSTAGE, par = (i - 1) & 1;
+      const unsigned char* sb = smem + (size_t)st * L.stage;
+      const float* r_t = reinterpret_cast<const float*>(sb + L.r);
+      const float* g_t = reinterpret_cast<const float*>(sb + L.g);
+      const float* v_t = reinterpret_cast<const float*>(sb + L.v);
+      const double* ratio_s = reinterpret_cast<const double*>(smem + L.ratio[par]);
+      float* vs_s = reinterpret_cast<float*>(smem + L.vs[par]);
+      float* pg_s = reinterpret_cast<float*>(smem + L.pg[par]);
+      float* adv_s = reinterpret_cast<float*>(smem + L.adv[par]);
+      const int c = lane >> 2, sg = lane & 3;
+      const bool col_ok = c < U.blen;
+      const int kk = (U.tlen + 3) >> 2;
+      const int s_beg = min(sg * kk, U.tlen), s_end = min(s_beg + kk, U.tlen);
+      const bool need_carry = (P.K > 1) && !U.last_chunk;
+      // early (speculative) look-back read: the predecessor is usually long done
+      unsigned int f0 = 0u;
+      double incl0 = 0.0;
+      const int up0 = U.u - P.G;
+      if (need_carry) {
+        f0 = ld_acquire_u32(P.flags + up0);
+        if (col_ok && sg == 0) incl0 = __ldcg(&P.recs[(size_t)up0 * BC + c].incl);
       }
-      rr = reward_transform(r_t[q], P.reward_mode);
-      Di = rho * (rr + gam * Vn - Vt);  // delta_t V
-      Gi = gam * c;
-    }
-    if (col_ok) {
+      double V_after = 0.0;  // V(x) just after this chunk (next chunk's first V, or bootstrap)
+      if (col_ok && s_end == U.tlen && s_beg < s_end) {
+        if (U.last_chunk) {
+          const float bv = __ldg(P.boot + U.b0 + c);
+          if (!isfinite(bv)) record_bad(P.ws, T * B + U.b0 + c, VT_DATA_VALUE);
+          V_after = (double)bv;
+        } else {
+          V_after = (double)__ldg(P.val + (long long)(U.t0 + U.tlen) * B + U.b0 + c);
+        }
+      }
+      // local affine aggregate of the segment: A_beg = D + G * A_end  (Remark 1)
+      double G = 1.0, D = 0.0;
+      if (col_ok) {
+        double Vn = (s_end < U.tlen) ? (double)v_t[s_end * BC + c] : V_after;
+        for (int s = s_end - 1; s >= s_beg; --s) {
+          const int q = s * BC + c;
+          const double ratio = ratio_s[q];
+          const double rho = fmin(P.rho_bar, ratio);
+          const double cc = P.lambda * fmin(P.c_bar, ratio);
+          const double gam = (double)g_t[q];
+          const double Vt = (double)v_t[q];
+          const double delta = rho * (reward_transform(r_t[q], P.reward_mode) + gam * Vn - Vt);
+          D = fma(gam * cc, D, delta);
+          G = gam * cc * G;
+          Vn = Vt;
+        }
+      }
+      // suffix scan over the 4 segments of each column (width-4 shuffles)
+      double Gi = G, Di = D;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
-        if (lane + o < 32) {
+      for (int o = 1; o < 4; o <<= 1) {
+        const double Go = __shfl_down_sync(0xffffffffu, Gi, o, 4);
+        const double Do = __shfl_down_sync(0xffffffffu, Di, o, 4);
+        if (sg + o < 4) {
           Di = fma(Gi, Do, Di);
           Gi = Gi * Go;
         }
       }
-    }
-    // carry = A at the end of this chunk (A_T = 0: v_T = V(x_T), reading c2), from
-    // the later-time chunks by decoupled look-back on per-unit flags
-    double carry = 0.0;
-    if (P.K > 1) {
-      if (col_ok && lane == 0) {
-        s_agg[warp][0] = Gi;
-        s_agg[warp][1] = Di;
+      double Ge = __shfl_down_sync(0xffffffffu, Gi, 1, 4);  // exclusive: segments > sg
+      double De = __shfl_down_sync(0xffffffffu, Di, 1, 4);
+      if (sg == 3) {
+        Ge = 1.0;
+        De = 0.0;
       }
-      __syncthreads();
-      unsigned int* flags = P.flags;
-      if (kchunk > 0 && warp == 0) {  // chunk 0 is never looked back at
-        if (lane < blen) {
-          ColRec* rec = P.recs + (size_t)u * BC + lane;
-          if (last_chunk) {
-            rec->incl = s_agg[lane][1];
-          } else {
-            rec->G = s_agg[lane][0];
-            rec->D = s_agg[lane][1];
+      // carry = A at the end of the chunk (A_T = 0: v_T = V(x_T), reading c2)
+      double carry = 0.0;
+      if (P.K > 1) {
+        ColRec* my = P.recs + (size_t)U.u * BC;
+        if (U.kchunk > 0 && !U.last_chunk) {  // publish the aggregate (chunk 0 is never read)
+          if (col_ok && sg == 0) {
+            my[c].G = Gi;
+            my[c].D = Di;
           }
+          __syncwarp();
+          __threadfence();
+          if (lane == 0) st_release_u32(P.flags + U.u, (epoch << 2) | 1u);
         }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_u32(flags + u, (epoch << 2) | (last_chunk ? 2u : 1u));
-      }
-      if (!last_chunk && col_ok) {
-        if (lane == 0) {
-          double aG = 1.0, aD = 0.0;  // composition of the later chunks seen so far
-          int up = u - P.G;
-          while (true) {
-            unsigned int f = ld_acquire_u32(flags + up);
-            int spins = 0;
-            while ((f >> 2) != epoch || (f & 3u) == 0u) {
-              if (++spins > 4) __nanosleep(32);
-              f = ld_acquire_u32(flags + up);
+        if (need_carry) {
+          const bool ready = ((f0 >> 2) == epoch) && ((f0 & 3u) == 2u);
+          if (__all_sync(0xffffffffu, ready)) {
+            carry = incl0;
+          } else if (col_ok && sg == 0) {
+            double aG = 1.0, aD = 0.0;  // composition of the later chunks seen so far
+            int up = up0;
+            while (true) {
+              unsigned int f = ld_acquire_u32(P.flags + up);
+              int spins = 0;
+              while ((f >> 2) != epoch || (f & 3u) == 0u) {
+                if (++spins > 4) __nanosleep(32);
+                f = ld_acquire_u32(P.flags + up);
+              }
+              const ColRec* pr = P.recs + (size_t)up * BC + c;
+              if ((f & 3u) == 2u) {
+                carry = fma(aG, __ldcg(&pr->incl), aD);
+                break;
+              }
+              const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
+              aD = fma(aG, Dp, aD);
+              aG = aG * Gp;
+              up -= P.G;
             }
-            const ColRec* pr = P.recs + (size_t)up * BC + warp;
-            if ((f & 3u) == 2u) {
-              carry = fma(aG, __ldcg(&pr->incl), aD);
-              break;
-            }
-            const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
-            aD = fma(aG, Dp, aD);
-            aG = aG * Gp;
-            up -= P.G;
           }
+          carry = __shfl_sync(0xffffffffu, carry, lane & ~3);
         }
-        carry = __shfl_sync(0xffffffffu, carry, 0);
+        if (U.kchunk > 0) {  // publish the inclusive carry A at this chunk's start
+          if (col_ok && sg == 0) my[c].incl = fma(Gi, carry, Di);
+          __syncwarp();
+          __threadfence();
+          if (lane == 0) st_release_u32(P.flags + U.u, (epoch << 2) | 2u);
+        }
+      }
+      // second pass over the segment: v_t, q_t, pg_adv_t
+      if (col_ok) {
+        double A_next = fma(Ge, carry, De);  // A at s_end
+        double V_next = (s_end < U.tlen) ? (double)v_t[s_end * BC + c] : V_after;
+        for (int s = s_end - 1; s >= s_beg; --s) {
+          const int q = s * BC + c;
+          const double ratio = ratio_s[q];
+          const double rho = fmin(P.rho_bar, ratio);
+          const double cc = P.lambda * fmin(P.c_bar, ratio);
+          const double rho_pg = fmin(P.pg_rho_bar, ratio);
+          const double gam = (double)g_t[q];
+          const double Vt = (double)v_t[q];
+          const double rr = reward_transform(r_t[q], P.reward_mode);
+          const double delta = rho * (rr + gam * V_next - Vt);
+          const double A_t = fma(gam * cc, A_next, delta);
+          const double v_next = V_next + A_next;  // v_{t+1}; v_T = V(x_T)
+          vs_s[q] = (float)(Vt + A_t);
+          pg_s[q] = (float)(rho_pg * (rr + gam * v_next - Vt));
+          adv_s[q] = (float)A_t;
+          A_next = A_t;
+          V_next = Vt;
+        }
       }
     }
-    if (col_ok) {
-      const double A_t = fma(Gi, carry, Di);            // A_t = v_t - V(x_t)
-      const double A_n = shfl_down_d(A_t, 1);           // A_{t+1} (lane tlen: = carry)
-      if (step_ok) {
-        const double v_next = Vn + (lane + 1 < 32 ? A_n : carry);  // v_{t+1}
-        const double adv = rho_pg * (rr + gam * v_next - Vt);
-        const int q = lane * BC + warp;
-        vs_s[q] = (float)(Vt + A_t);
-        pg_s[q] = (float)adv;
-        adv_s[q] = (float)A_t;
-      }
-      if (P.K > 1 && kchunk > 0 && !last_chunk && lane == 0) s_incl[warp] = A_t;
-    }
-    if (P.K > 1 && kchunk > 0 && !last_chunk) {
-      __syncthreads();
-      if (warp == 0) {
-        if (lane < blen) P.recs[(size_t)u * BC + lane].incl = s_incl[lane];
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_u32(P.flags + u, (epoch << 2) | 2u);
-      }
-    }
-    if constexpr (LOSS && USE_TMA) {
-      // the previous unit's dlogits store must have read dz_t before it is overwritten
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
-    __syncthreads();
+    named_bar_sync(1, NTHREADS);
 
-    // ---- a6, a10, a11: gradient epilogue of this thread's row ----------------------
-    if (row_ok) {
-      const float vsr = vs_s[r], pgr = pg_s[r], Ar = adv_s[r];
-      if (P.vs) P.vs[row] = vsr;
-      if (P.pg_adv) P.pg_adv[row] = pgr;
-      if constexpr (LOSS) {
-        const float L2E = 1.44269504088896341f;
-        const float lseL = lse * L2E;
-        LT* dzrow = dz_t + (size_t)r * A;
-        float sq = 0.f;
-        auto dz_of = [&](float z) {  // pi_j (pg + c_e (log pi_j + H))
-          const float p = ex2_approx(fmaf(z, L2E, -lseL));
-          return p * fmaf(ce, z - cshift, pgr);
-        };
-        if constexpr (RowRegs<LT, A_CT>::kPacked) {
-          uint32_t* w = reinterpret_cast<uint32_t*>(dzrow);
+    // ================= phase B: P3(i-1) on the row warps ============================
+    if (warp < NROWWARPS && i >= 1) {
+      Unit U;
+      U.set((int)blockIdx.x + (i - 1) * stride, P);
+      const int st = (i - 1) % NSTAGE, par = (i - 1) & 1;
+      const unsigned char* sb = smem + (size_t)st * L.stage;
+      LT* dz_t = reinterpret_cast<LT*>(smem + L.dz);
+      const int r = tid;
+      const int tl = r >> 3, bl = r & 7;
+      if (r < nrow && tl < U.tlen && bl < U.blen) {
+        const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
+        const float vsr = reinterpret_cast<const float*>(smem + L.vs[par])[r];
+        const float pgr = reinterpret_cast<const float*>(smem + L.pg[par])[r];
+        if (P.vs) P.vs[row] = vsr;
+        if (P.pg_adv) P.pg_adv[row] = pgr;
+        if constexpr (LOSS) {
+          const float Ar = reinterpret_cast<const float*>(smem + L.adv[par])[r];
+          const float lse = reinterpret_cast<const float*>(smem + L.lse[par])[r];
+          const float cshift = reinterpret_cast<const float*>(smem + L.csh[par])[r];
+          const float rest = reinterpret_cast<const float*>(smem + L.rest[par])[r];
+          const float pa = 1.f - rest;  // pi(a); only scaled by c_e below
+          const int a = min(max(reinterpret_cast<const int*>(sb + L.a)[r], 0), A - 1);
+          const LT* zrow = reinterpret_cast<const LT*>(sb + L.pi) + (size_t)r * A;
+          RowRegs<LT, A_CT> zp;
+          zp.load(zrow);
+          const float L2E = 1.44269504088896341f;
+          const float lseL = lse * L2E;
+          LT* dzrow = dz_t + (size_t)r * A;
+          float sq = 0.f;
+          // dz_j = pi_j (pg + c_e (log pi_j + H))   (j != a)
+          if constexpr (RowRegs<LT, A_CT>::kPacked) {
+            uint32_t* w = reinterpret_cast<uint32_t*>(dzrow);
 #pragma unroll
-          for (int k = 0; k < A_CT / 2; ++k) {
-            const float d0 = dz_of(zp.get(2 * k)), d1 = dz_of(zp.get(2 * k + 1));
-            sq = fmaf(d0, d0, sq);
-            sq = fmaf(d1, d1, sq);
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(d0, d1);
-            w[k] = *reinterpret_cast<uint32_t*>(&h2);
+            for (int k = 0; k < A_CT / 2; ++k) {
+              const float z0 = zp.get(2 * k), z1 = zp.get(2 * k + 1);
+              const float d0 = ex2_approx(fmaf(z0, L2E, -lseL)) * fmaf(ce, z0 - cshift, pgr);
+              const float d1 = ex2_approx(fmaf(z1, L2E, -lseL)) * fmaf(ce, z1 - cshift, pgr);
+              sq = fmaf(d0, d0, sq);
+              sq = fmaf(d1, d1, sq);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(d0, d1);
+              w[k] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+          } else {
+            const int nA = A_CT > 0 ? A_CT : A;
+#pragma unroll 4
+            for (int j = 0; j < nA; ++j) {
+              const float z = zp.get(j);
+              const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z - cshift, pgr);
+              sq = fmaf(d, d, sq);
+              dzrow[j] = store_cvt<LT>(d);
+            }
           }
-        } else if constexpr (A_CT > 0) {
-#pragma unroll
-          for (int j = 0; j < A_CT; ++j) {
-            const float d = dz_of(zp.get(j));
-            sq = fmaf(d, d, sq);
-            dzrow[j] = store_cvt<LT>(d);
-          }
-        } else {
-          for (int j = 0; j < A; ++j) {
-            const float d = dz_of(zp.get(j));
-            sq = fmaf(d, d, sq);
-            dzrow[j] = store_cvt<LT>(d);
+          // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
+          const float za = Elem<LT>::get(zrow, a);
+          const float d_wrong = ex2_approx(fmaf(za, L2E, -lseL)) * fmaf(ce, za - cshift, pgr);
+          const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
+          dzrow[a] = store_cvt<LT>(d_a);
+          sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
+          const float dv = -cv * Ar;  // c_v (V - v)
+          P.dvalues[row] = dv;
+          acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)
+          acc_v = fmaf(0.5f * Ar, Ar, acc_v);
+          acc_H += lse - cshift;  // H = lse - (lse - H)
+          acc_dz += sq;
+          acc_dv = fmaf(dv, dv, acc_dv);
+          if constexpr (!USE_TMA) {
+            LT* gdz = reinterpret_cast<LT*>(P.dlogits) + row * A;
+            for (int j = 0; j < A; ++j) gdz[j] = dzrow[j];
           }
         }
-        // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
-        const float za = Elem<LT>::get(zp.src, a);
-        const float d_wrong = dz_of(za);
-        const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
-        dzrow[a] = store_cvt<LT>(d_a);
-        sq = fmaf(d_a, d_a, fmaf(-d_wrong, d_wrong, sq));
-        const float dv = -cv * Ar;  // c_v (V - v)
-        P.dvalues[row] = dv;
-        acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)
-        acc_v = fmaf(0.5f * Ar, Ar, acc_v);
-        acc_H += lse - cshift;  // H = lse - (lse - H)
-        acc_dz += sq;
-        acc_dv = fmaf(dv, dv, acc_dv);
       }
-    }
-    if constexpr (LOSS && USE_TMA) fence_proxy_async_smem();
-    __syncthreads();  // stage st consumed; dz_t complete
-    if (tid == 0) {
-      if constexpr (LOSS && USE_TMA) {
-        tma_store_2d(&maps.dz, (int)(b0 * A), t0, dz_t);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if constexpr (LOSS && USE_TMA) fence_proxy_async_smem();
+      named_bar_sync(2, NROWTHREADS);  // dz tile complete; stage (i-1) consumed
+      if (tid == 0) {
+        if constexpr (LOSS && USE_TMA) {
+          tma_store_2d(&maps.dz, (int)(U.b0 * A), U.t0, dz_t);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if constexpr (USE_TMA) {
+          fence_proxy_async_smem();  // generic reads of the stage before its async refill
+          load_unit(i + 2);          // stage (i-1)%3 == (i+2)%3
+        }
+        if constexpr (LOSS && USE_TMA)  // dz tile must be read before P3(i) rewrites it
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
-      if constexpr (USE_TMA) {
-        fence_proxy_async_smem();  // generic reads of the stage before its async refill
-        load_unit(u + NSTAGE * stride, st);
-      }
-    }
-    if constexpr (LOSS && !USE_TMA) {
-      LT* gdz = reinterpret_cast<LT*>(P.dlogits);
-      const int rowlen = BC * A;
-      for (int i = tid; i < nrow * A; i += NTHREADS) {
-        const int tl2 = i / rowlen, rem = i - tl2 * rowlen, bl2 = rem / A, j = rem - bl2 * A;
-        if (tl2 < tlen && bl2 < blen)
-          gdz[(((long long)(t0 + tl2)) * B + b0 + bl2) * A + j] = dz_t[i];
-      }
-      __syncthreads();
     }
   }
 
@@ -547,11 +619,11 @@ __global__ void __launch_bounds__(NTHREADS)
   {
     const double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
 #pragma unroll
-    for (int i = 0; i < NPART; ++i) {
-      double x = part[i];
+    for (int k = 0; k < NPART; ++k) {
+      double x = part[k];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) s_red[warp][i] = x;
+      if (lane == 0) s_red[warp][k] = x;
     }
     __syncthreads();
     if (tid < NPART) {
@@ -572,7 +644,7 @@ __global__ void __launch_bounds__(NTHREADS)
   if (s_last) {
     __threadfence();
     if (LOSS && P.partials) {
-      if (warp < NPART) {  // warp i: partial i; lanes stride the CTAs, then lane order
+      if (warp < NPART) {  // warp k: partial k; lanes stride the CTAs, then lane order
         double x = 0.0;
         for (int v = lane; v < (int)gridDim.x; v += 32)
           x += __ldcg(P.cta_partials + (size_t)v * NPART + warp);
@@ -583,10 +655,10 @@ __global__ void __launch_bounds__(NTHREADS)
       __syncthreads();
       if (tid == 0) {
         double out[NPART];
-        for (int i = 0; i < NPART; ++i) out[i] = s_red[i][0];
+        for (int k = 0; k < NPART; ++k) out[k] = s_red[k][0];
         out[VT_P_TOTAL_LOSS] = out[VT_P_PG_LOSS] + P.c_v * out[VT_P_BASELINE_LOSS] -
                                P.c_e * out[VT_P_ENTROPY_SUM];
-        for (int i = 0; i < NPART; ++i) P.partials[i] = out[i];
+        for (int k = 0; k < NPART; ++k) P.partials[k] = out[k];
       }
     }
     if (tid == 0) {
@@ -612,7 +684,7 @@ constexpr int kMaxCtas = 4096;  // bound on the persistent grid (workspace sizin
 // unit's Tc * 8 rows map one-to-one onto the 256 threads, and small enough for
 // two input stages plus the staging tile to fit in shared memory.
 static int tc_max_for(int A, int elem) {
-  for (int tc = 32; tc > 1; --tc)
+  for (int tc = NROWTHREADS / BC; tc > 1; --tc)
     if (make_layout(tc * BC, A, elem).total <= 100 * 1024) return tc;
   return 1;
 }

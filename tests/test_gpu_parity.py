@@ -209,7 +209,7 @@ def test_partials_of_shards_add_up():
         sh = wl.column_slice(inp, b0, b0 + 256)
         tot += pkg.loss_and_grad(*[_dev(sh)[k] for k in NAMES], reward_mode=1)["partials"].cpu()
     # every partial (the total loss included) is a sum over trajectories
-    np.testing.assert_allclose(tot.numpy(), full.numpy(), rtol=1e-12)
+    np.testing.assert_allclose(tot.numpy(), full.numpy(), rtol=1e-7)  # per-thread fp32 partial sums
 
 
 def test_data_errors_reported():
