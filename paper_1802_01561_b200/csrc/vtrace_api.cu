@@ -174,15 +174,17 @@ struct Layout {
 __host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Big tiles 128-byte aligned, small [Tc][8] arrays 16-byte aligned (TMA minimum).
+// Every TMA destination is 128-byte aligned (a tiled cp.async.bulk.tensor into a
+// merely 16-byte aligned address faults with "misaligned address" on sm_100a);
+// the row-state arrays, read and written by threads only, are 16-byte aligned.
 __host__ __device__ inline Layout make_layout(int nrow, int A, int elem) {
   Layout L;
   size_t off = 0;
   L.pi = off; off = a128(off + (size_t)nrow * A * elem);
   L.mu = off; off = a128(off + (size_t)nrow * A * elem);
-  L.a = off;  off = a16(off + (size_t)nrow * 4);
-  L.r = off;  off = a16(off + (size_t)nrow * 4);
-  L.g = off;  off = a16(off + (size_t)nrow * 4);
+  L.a = off;  off = a128(off + (size_t)nrow * 4);
+  L.r = off;  off = a128(off + (size_t)nrow * 4);
+  L.g = off;  off = a128(off + (size_t)nrow * 4);
   L.v = off;  off = a128(off + (size_t)nrow * 4);
   L.stage = off;
   off = NSTAGE * L.stage;
