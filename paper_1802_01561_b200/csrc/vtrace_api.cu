@@ -209,17 +209,32 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 // geometry of one work unit
 struct Unit {
-  int u, kchunk, t0, tlen, blen;
+  int u, kchunk, grp, t0, tlen, blen;
   long long b0;
   bool last_chunk;
+  __device__ __forceinline__ void finish(const Params& P) {
+    t0 = kchunk * P.Tc;
+    tlen = (int)min((long long)P.Tc, P.T - t0);
+    b0 = (long long)grp * BC;
+    blen = (int)min((long long)BC, P.B - b0);
+    last_chunk = (kchunk == P.K - 1);
+  }
   __device__ __forceinline__ void set(int uu, const Params& P) {
     u = uu;
     kchunk = P.K - 1 - uu / P.G;  // unit ids run in reverse time order
-    t0 = kchunk * P.Tc;
-    tlen = (int)min((long long)P.Tc, P.T - t0);
-    b0 = (long long)(uu % P.G) * BC;
-    blen = (int)min((long long)BC, P.B - b0);
-    last_chunk = (kchunk == P.K - 1);
+    grp = uu % P.G;
+    finish(P);
+  }
+  // u += gridDim.x without a division: gridDim.x = stride_q * G + stride_r
+  __device__ __forceinline__ void advance(const Params& P, int stride) {
+    u += stride;
+    grp += P.stride_r;
+    kchunk -= P.stride_q;
+    if (grp >= P.G) {
+      grp -= P.G;
+      --kchunk;
+    }
+    finish(P);
   }
 };
 
@@ -295,12 +310,17 @@ __global__ void __launch_bounds__(NTHREADS)
   float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
         acc_clip = 0.f;
 
+  Unit Ucur, Uprev;  // units i and i-1 of this CTA
+  Ucur.set((int)blockIdx.x, P);
+  Uprev = Ucur;
+  unsigned long long* tim = P.timing ? P.timing + (size_t)blockIdx.x * P.timing_iters * 8 : nullptr;
   for (int i = 0; i <= n_my; ++i) {
+    if (tim && i < P.timing_iters && (tid == 0 || tid == NROWTHREADS))
+      tim[i * 8 + (tid == 0 ? 0 : 4)] = clock64();
     // ================= phase A: P1(i) on row warps || SCAN(i-1) on the scan warp ====
     if (warp < NROWWARPS) {
       if (i < n_my) {
-        Unit U;
-        U.set((int)blockIdx.x + i * stride, P);
+        const Unit& U = Ucur;
         const int st = i % NSTAGE, par = i & 1;
         unsigned char* sb = smem + (size_t)st * L.stage;
         const LT* pi_t = reinterpret_cast<const LT*>(sb + L.pi);
@@ -388,8 +408,7 @@ __global__ void __launch_bounds__(NTHREADS)
       }
     } else if (i >= 1) {
       // ---- SCAN(i-1): warp 7.  Lane 4c + s owns column c, segment s of 4 --------
-      Unit U;
-      U.set((int)blockIdx.x + (i - 1) * stride, P);
+      const Unit& U = Uprev;
       const int st = (i - 1) % NSTAGE, par = (i - 1) & 1;
       const unsigned char* sb = smem + (size_t)st * L.stage;
       const float* r_t = reinterpret_cast<const float*>(sb + L.r);
@@ -405,13 +424,13 @@ __global__ void __launch_bounds__(NTHREADS)
       const int s_beg = min(sg * kk, U.tlen), s_end = min(s_beg + kk, U.tlen);
       const bool need_carry = (P.K > 1) && !U.last_chunk;
       // early (speculative) look-back read: the predecessor is usually long done
-      unsigned int f0 = 0u;
+      const unsigned long long tagA = ((unsigned long long)epoch << 2) | 1ull;
+      const unsigned long long tagI = ((unsigned long long)epoch << 2) | 2ull;
+      unsigned long long t0tag = 0ull;
       double incl0 = 0.0;
       const int up0 = U.u - P.G;
-      if (need_carry) {
-        f0 = ld_acquire_u32(P.flags + up0);
-        if (col_ok && sg == 0) incl0 = __ldcg(&P.recs[(size_t)up0 * BC + c].incl);
-      }
+      if (need_carry && col_ok && sg == 0)
+        ld_tag16(P.recs + ((size_t)up0 * BC + c) * RECS_PER_COL + 2, incl0, t0tag);
       double V_after = 0.0;  // V(x) just after this chunk (next chunk's first V, or bootstrap)
       if (col_ok && s_end == U.tlen && s_beg < s_end) {
         if (U.last_chunk) {
@@ -459,49 +478,44 @@ __global__ void __launch_bounds__(NTHREADS)
       // carry = A at the end of the chunk (A_T = 0: v_T = V(x_T), reading c2)
       double carry = 0.0;
       if (P.K > 1) {
-        ColRec* my = P.recs + (size_t)U.u * BC;
-        if (U.kchunk > 0 && !U.last_chunk) {  // publish the aggregate (chunk 0 is never read)
-          if (col_ok && sg == 0) {
-            my[c].G = Gi;
-            my[c].D = Di;
-          }
-          __syncwarp();
-          __threadfence();
-          if (lane == 0) st_release_u32(P.flags + U.u, (epoch << 2) | 1u);
+        TagRec* my = P.recs + ((size_t)U.u * BC + c) * RECS_PER_COL;
+        // publish the aggregate (chunk 0 is never looked back at)
+        if (U.kchunk > 0 && !U.last_chunk && col_ok && sg == 0) {
+          st_tag16(my + 0, Gi, tagA);
+          st_tag16(my + 1, Di, tagA);
         }
-        if (need_carry) {
-          const bool ready = ((f0 >> 2) == epoch) && ((f0 & 3u) == 2u);
-          if (__all_sync(0xffffffffu, ready)) {
+        if (need_carry && col_ok && sg == 0) {
+          if (t0tag == tagI) {
             carry = incl0;
-          } else if (col_ok && sg == 0) {
+          } else {
             double aG = 1.0, aD = 0.0;  // composition of the later chunks seen so far
             int up = up0;
+            int spins = 0;
             while (true) {
-              unsigned int f = ld_acquire_u32(P.flags + up);
-              int spins = 0;
-              while ((f >> 2) != epoch || (f & 3u) == 0u) {
-                if (++spins > 4) __nanosleep(32);
-                f = ld_acquire_u32(P.flags + up);
-              }
-              const ColRec* pr = P.recs + (size_t)up * BC + c;
-              if ((f & 3u) == 2u) {
-                carry = fma(aG, __ldcg(&pr->incl), aD);
+              const TagRec* pr = P.recs + ((size_t)up * BC + c) * RECS_PER_COL;
+              double vi, vg, vd;
+              unsigned long long ti, tg, td;
+              ld_tag16(pr + 2, vi, ti);
+              if (ti == tagI) {
+                carry = fma(aG, vi, aD);
                 break;
               }
-              const double Gp = __ldcg(&pr->G), Dp = __ldcg(&pr->D);
-              aD = fma(aG, Dp, aD);
-              aG = aG * Gp;
-              up -= P.G;
+              ld_tag16(pr + 0, vg, tg);
+              ld_tag16(pr + 1, vd, td);
+              if (tg == tagA && td == tagA) {
+                aD = fma(aG, vd, aD);
+                aG = aG * vg;
+                up -= P.G;
+                spins = 0;
+              } else if (++spins > 4) {
+                __nanosleep(32);
+              }
             }
           }
-          carry = __shfl_sync(0xffffffffu, carry, lane & ~3);
         }
-        if (U.kchunk > 0) {  // publish the inclusive carry A at this chunk's start
-          if (col_ok && sg == 0) my[c].incl = fma(Gi, carry, Di);
-          __syncwarp();
-          __threadfence();
-          if (lane == 0) st_release_u32(P.flags + U.u, (epoch << 2) | 2u);
-        }
+        carry = __shfl_sync(0xffffffffu, carry, lane & ~3);
+        // publish the inclusive carry: A at this chunk's first step
+        if (U.kchunk > 0 && col_ok && sg == 0) st_tag16(my + 2, fma(Gi, carry, Di), tagI);
       }
       // second pass over the segment: v_t, q_t, pg_adv_t
       if (col_ok) {
@@ -527,12 +541,18 @@ __global__ void __launch_bounds__(NTHREADS)
         }
       }
     }
+    if constexpr (LOSS && USE_TMA) {
+      // the previous unit's dlogits store must have read the tile before P3 rewrites it
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    if (tim && i < P.timing_iters && (tid == 0 || tid == NROWTHREADS))
+      tim[i * 8 + (tid == 0 ? 1 : 5)] = clock64();
     named_bar_sync(1, NTHREADS);
+    if (tim && i < P.timing_iters && tid == 0) tim[i * 8 + 2] = clock64();
 
     // ================= phase B: P3(i-1) on the row warps ============================
     if (warp < NROWWARPS && i >= 1) {
-      Unit U;
-      U.set((int)blockIdx.x + (i - 1) * stride, P);
+      const Unit& U = Uprev;
       const int st = (i - 1) % NSTAGE, par = (i - 1) & 1;
       const unsigned char* sb = smem + (size_t)st * L.stage;
       LT* dz_t = reinterpret_cast<LT*>(smem + L.dz);
@@ -611,10 +631,11 @@ __global__ void __launch_bounds__(NTHREADS)
           fence_proxy_async_smem();  // generic reads of the stage before its async refill
           load_unit(i + 2);          // stage (i-1)%3 == (i+2)%3
         }
-        if constexpr (LOSS && USE_TMA)  // dz tile must be read before P3(i) rewrites it
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (tim && i < P.timing_iters) tim[i * 8 + 3] = clock64();
       }
     }
+    Uprev = Ucur;
+    Ucur.advance(P, stride);
   }
 
   // ---- a12: CTA partials (fixed order), then the last CTA out reduces them ---------
@@ -709,14 +730,13 @@ static Plan make_plan(long long T, long long B, int A, int elem) {
 }
 
 struct WsLayout {
-  size_t flags, recs, cta, total;
+  size_t recs, cta, total;
 };
 
 static WsLayout ws_layout(const Plan& p) {
   WsLayout w;
-  w.flags = 256;
-  w.recs = a128(w.flags + (size_t)p.units * 4);
-  w.cta = a128(w.recs + (size_t)p.units * BC * sizeof(ColRec));
+  w.recs = 256;
+  w.cta = a128(w.recs + (size_t)p.units * BC * RECS_PER_COL * sizeof(TagRec));
   w.total = w.cta + (size_t)kMaxCtas * NPART * sizeof(double);
   return w;
 }
@@ -727,6 +747,9 @@ static size_t ws_bytes_for(const Plan& p) { return ws_layout(p).total; }
 static std::mutex g_mu;
 static int g_dev_ok[64];  // 0 unknown, 1 ok, 2 bad
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+// debug hook (not part of the ABI): per-CTA phase timestamps of the next launches
+static unsigned long long* g_timing = nullptr;
+static int g_timing_iters = 0;
 
 static vt_status check_device() {
   int dev = 0;
@@ -805,6 +828,11 @@ static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& pl
     return VT_ERR_CUDA;
   const long long grid =
       std::min<long long>({(long long)plan.units, (long long)per_sm * num_sms, (long long)kMaxCtas});
+  Params Pl = P;
+  Pl.stride_q = (int)(grid / P.G);
+  Pl.stride_r = (int)(grid % P.G);
+  Pl.timing = g_timing;
+  Pl.timing_iters = g_timing_iters;
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)grid);
@@ -816,7 +844,7 @@ static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& pl
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, P, maps) != cudaSuccess) return VT_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, Pl, maps) != cudaSuccess) return VT_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
@@ -908,8 +936,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   unsigned char* wsb = static_cast<unsigned char*>(ws);
   P.ws = reinterpret_cast<WsHeader*>(wsb);
   const WsLayout wl = ws_layout(plan);
-  P.flags = reinterpret_cast<unsigned int*>(wsb + wl.flags);
-  P.recs = reinterpret_cast<ColRec*>(wsb + wl.recs);
+  P.recs = reinterpret_cast<TagRec*>(wsb + wl.recs);
   P.cta_partials = reinterpret_cast<double*>(wsb + wl.cta);
 
   // TMA eligibility: 16-byte aligned bases and row pitches, box inner <= 256 elements
@@ -1063,5 +1090,12 @@ const char* vtrace_status_string(vt_status s) {
 }
 
 int32_t vtrace_version(void) { return 100; }
+
+// Debug hook, not declared in include/vtrace.h: while set, every launch records
+// clock64() per CTA and iteration into buf[grid][iters][8] (device memory).
+void vtrace_debug_set_timing(void* buf, int32_t iters) {
+  g_timing = static_cast<unsigned long long*>(buf);
+  g_timing_iters = buf ? iters : 0;
+}
 
 }  // extern "C"

@@ -46,13 +46,17 @@ struct alignas(16) WsHeader {
   unsigned long long pad1[5];
 };
 
-// Decoupled look-back record of one (unit, column).  The unit's flag
-// (epoch << 2) | state says what is published: state 1 = the chunk's affine
-// aggregate (G, D), state 2 = the inclusive carry (A = v - V at its first step).
-struct alignas(16) ColRec {
-  double G, D, incl, pad;
+// Decoupled look-back record: a 16-byte (value, tag) pair written and read
+// with single 16-byte relaxed accesses, so no fence or flag is needed; tag =
+// (epoch << 2) | kind.  Per (unit, column) there are three: the chunk's affine
+// aggregate G and D (kind 1) and the inclusive carry A = v - V at the chunk's
+// first step (kind 2).
+struct alignas(16) TagRec {
+  double value;
+  unsigned long long tag;
 };
-static_assert(sizeof(ColRec) == 32, "ColRec layout");
+static_assert(sizeof(TagRec) == 16, "TagRec layout");
+constexpr int RECS_PER_COL = 3;  // G, D, incl
 
 struct Params {
   long long T, B;
@@ -77,9 +81,11 @@ struct Params {
   double c_v, c_e;
   int reward_mode;
   WsHeader* ws;
-  unsigned int* flags;
-  ColRec* recs;
+  TagRec* recs;          // [units][BC][RECS_PER_COL]
   double* cta_partials;
+  unsigned long long* timing;  // debug: per-CTA phase timestamps (NULL = off)
+  int timing_iters;
+  int stride_q, stride_r;  // gridDim.x = stride_q * G + stride_r
 };
 
 struct TmaMaps {
@@ -151,6 +157,19 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
 
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_tag16(TagRec* p, double v, unsigned long long tag) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p),
+               "l"((unsigned long long)__double_as_longlong(v)), "l"(tag)
+               : "memory");
+}
+
+__device__ __forceinline__ void ld_tag16(const TagRec* p, double& v, unsigned long long& tag) {
+  unsigned long long a, b;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  v = __longlong_as_double((long long)a);
+  tag = b;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+T=${TAG:-t1}
+for cfg in large stress; do timeout 300 python tools/phase_timing.py $cfg > gpurun_out/${T}_timing_$cfg.txt 2>&1; done
+timeout 600 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/${T}_gpu.txt 2>&1; echo "rc=$?" >> gpurun_out/${T}_gpu.txt
+for cfg in large stress; do timeout 300 python bench.py --config $cfg --steps 2000 --warmup 10 --no-cpu-baseline --no-e2e > gpurun_out/${T}_bench_$cfg.txt 2>&1; done
