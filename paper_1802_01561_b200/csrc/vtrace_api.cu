@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(NTHREADS)
         Ge = 1.0;
         De = 0.0;
       }
+      if (tim && i < P.timing_iters && lane == 0) tim[i * 8 + 7] = clock64();
       // carry = A at the end of the chunk (A_T = 0: v_T = V(x_T), reading c2)
       double carry = 0.0;
       if (P.K > 1) {
@@ -607,6 +608,7 @@ __global__ void __launch_bounds__(NTHREADS)
           const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
           dzrow[a] = store_cvt<LT>(d_a);
           sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
+          if (tim && i < P.timing_iters && tid == 0) tim[i * 8 + 6] = clock64();
           const float dv = -cv * Ar;  // c_v (V - v)
           P.dvalues[row] = dv;
           acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)

@@ -36,10 +36,12 @@ for c in range(GRID):
         if not used[c, i]:
             continue
         r = t[c, i]
-        rows.append(dict(p1=r[1] - r[0], scan=r[5] - r[4], wait_row=r[2] - r[1],
+        rows.append(dict(p1=r[1] - r[0], scan=r[5] - r[4], scan_local=r[7] - r[4],
+                         scan_rest=r[5] - r[7], p3_rows=r[6] - r[2], p3_tail=r[3] - r[6],
+                         wait_row=r[2] - r[1],
                          wait_scan=r[2] - r[5], p3=r[3] - r[2],
                          iter=(t[c, i + 1, 0] - r[0]) if i + 1 < ITERS and used[c, i + 1] else 0))
-keys = ["p1", "scan", "wait_row", "p3", "iter"]
+keys = ["p1", "scan", "scan_local", "scan_rest", "wait_row", "p3", "p3_rows", "p3_tail", "iter"]
 print(name, "CTAs used", int(used[:, 0].sum()), "iterations/CTA", int(used.sum(1).max()))
 for k in keys:
     v = np.array([r[k] for r in rows if r[k] > 0])
