@@ -155,20 +155,22 @@ __device__ __forceinline__ void record_bad(WsHeader* ws, long long row, int kind
 
 // ---------------------------------------------------------------------------
 // Shared-memory layout of one CTA (host and device agree on it).
-//   NSTAGE input stages: z^pi, z^mu [Tc][8*A] (logits dtype), a, r, gamma, V [Tc][8]
-//   2 row-state buffers (by unit parity): ratio (f64), lse, lse - H, 1 - pi(a)
-//   2 scan-output buffers (by unit parity): v, pg_adv, A = v - V (f32)
-//   one dlogits staging tile [Tc][8*A] (TMA-stored while the next unit runs)
+//   NSTAGE input stages: z^pi, z^mu [Tc][8*A] (logits dtype); a, r, gamma [Tc][8];
+//     V [Tc+1][8] (one row past the chunk); bootstrap [8].  The gradient is written
+//     in place over the z^pi tile and TMA-stored from there.
+//   2 row-state buffers (by unit parity): ratio pi/mu and TD error r + gamma V' - V
+//     (f64), lse, lse - H, 1 - pi(a) (f32); A = v - V (f64, Tc+1 rows: the last is
+//     the carry from the later chunks)
 
 constexpr int NSTAGE = 3;
 constexpr int NROWWARPS = NWARPS - 1;       // warps 0..6 own rows, warp 7 runs the scan
 constexpr int NROWTHREADS = NROWWARPS * 32;  // 224 >= Tc * 8
+constexpr int KSEG = (NROWTHREADS / BC + 3) / 4;  // steps per scan lane (Tc <= 28)
 
 struct Layout {
-  size_t pi, mu, a, r, g, v, stage;               // offsets inside a stage
-  size_t ratio[2], lse[2], csh[2], rest[2];      // row state
-  size_t vs[2], pg[2], adv[2];                   // scan output
-  size_t dz, total;
+  size_t pi, mu, a, r, g, v, boot, stage;          // offsets inside a stage
+  size_t ratio[2], td[2], adv[2], lse[2], csh[2], rest[2];  // row state
+  size_t total;
 };
 
 __host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
@@ -180,26 +182,24 @@ __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15);
 __host__ __device__ inline Layout make_layout(int nrow, int A, int elem) {
   Layout L;
   size_t off = 0;
-  L.pi = off; off = a128(off + (size_t)nrow * A * elem);
-  L.mu = off; off = a128(off + (size_t)nrow * A * elem);
-  L.a = off;  off = a128(off + (size_t)nrow * 4);
-  L.r = off;  off = a128(off + (size_t)nrow * 4);
-  L.g = off;  off = a128(off + (size_t)nrow * 4);
-  L.v = off;  off = a128(off + (size_t)nrow * 4);
+  L.pi = off;   off = a128(off + (size_t)nrow * A * elem);
+  L.mu = off;   off = a128(off + (size_t)nrow * A * elem);
+  L.a = off;    off = a128(off + (size_t)nrow * 4);
+  L.r = off;    off = a128(off + (size_t)nrow * 4);
+  L.g = off;    off = a128(off + (size_t)nrow * 4);
+  L.v = off;    off = a128(off + (size_t)(nrow + BC) * 4);
+  L.boot = off; off = a128(off + (size_t)BC * 4);
   L.stage = off;
   off = NSTAGE * L.stage;
   for (int p = 0; p < 2; ++p) {
     L.ratio[p] = off; off = a16(off + (size_t)nrow * 8);
+    L.td[p] = off;    off = a16(off + (size_t)nrow * 8);
+    L.adv[p] = off;   off = a16(off + (size_t)(nrow + BC) * 8);
     L.lse[p] = off;   off = a16(off + (size_t)nrow * 4);
     L.csh[p] = off;   off = a16(off + (size_t)nrow * 4);
     L.rest[p] = off;  off = a16(off + (size_t)nrow * 4);
-    L.vs[p] = off;    off = a16(off + (size_t)nrow * 4);
-    L.pg[p] = off;    off = a16(off + (size_t)nrow * 4);
-    L.adv[p] = off;   off = a16(off + (size_t)nrow * 4);
   }
-  off = a128(off);
-  L.dz = off; off = a128(off + (size_t)nrow * A * elem);
-  L.total = off;
+  L.total = a128(off);
   return L;
 }
 
@@ -244,16 +244,18 @@ struct Unit {
 // ever waits, in the look-back, on units of earlier or the same rounds, all
 // resident).  Warp-specialised software pipeline over the CTA's units; in
 // iteration i:
-//   row warps 0..6 : P1(i)  row statistics of unit i  (stage i%3 -> row state i%2)
-//   scan warp 7    : SCAN(i-1) reverse recursion of unit i-1 (row state (i-1)%2 ->
-//                    scan output (i-1)%2), look-back, publication
-//   -- barrier 1 (256) --
-//   row warps      : P3(i-1) gradient epilogue of unit i-1 -> dz tile -> TMA store;
-//                    stage (i-1)%3 is refilled with unit i+2
+//   row warps 0..6 : P1(i)   row statistics + TD errors of unit i
+//   scan warp 7    : SCAN(i-1) the reverse recursion of unit i-1 (affine maps on
+//                    A = v - V), look-back, publication
+//   thread 0       : waits for the TMA store of unit i-2's gradient, reloads that
+//                    stage with unit i+1
+//   -- barrier 1 (256 threads) --
+//   row warps      : P3(i-1) v, pg_adv, dL/dV and dL/dz of unit i-1, dz written in
+//                    place over z^pi, then one TMA store
 // so the latency-bound recursion overlaps the row arithmetic of the next unit.
 
 template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE>
-__global__ void __launch_bounds__(NTHREADS)
+__global__ void __launch_bounds__(NTHREADS, 3)
     vtrace_fused_kernel(const Params P, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[NSTAGE];
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(NTHREADS)
   __syncthreads();
   const unsigned int epoch = s_epoch & 0x3fffffffu;
 
-  // TMA: unit i of this CTA -> stage i % NSTAGE
+  // TMA: unit i of this CTA -> stage i % NSTAGE (thread 0 only)
   auto load_unit = [&](int i) {
     if constexpr (USE_TMA) {
       if (i < n_my) {
@@ -288,8 +290,8 @@ __global__ void __launch_bounds__(NTHREADS)
         U.set((int)blockIdx.x + i * stride, P);
         const int st = i % NSTAGE;
         unsigned char* sb = smem + (size_t)st * L.stage;
-        const uint32_t bytes =
-            (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) + 4 * (size_t)nrow * 4);
+        const uint32_t bytes = (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) +
+                                          3 * (size_t)nrow * 4 + (size_t)(nrow + BC) * 4 + BC * 4);
         mbar_expect_tx(&bar[st], bytes);
         const int xb = (int)(U.b0 * A);
         tma_load_2d(sb + L.pi, &maps.pi, xb, U.t0, &bar[st]);
@@ -298,11 +300,11 @@ __global__ void __launch_bounds__(NTHREADS)
         tma_load_2d(sb + L.r, &maps.r, (int)U.b0, U.t0, &bar[st]);
         tma_load_2d(sb + L.g, &maps.g, (int)U.b0, U.t0, &bar[st]);
         tma_load_2d(sb + L.v, &maps.v, (int)U.b0, U.t0, &bar[st]);
+        tma_load_1d(sb + L.boot, &maps.boot, (int)U.b0, &bar[st]);
       }
     }
   };
-  if (USE_TMA && tid == 0)
-    for (int i = 0; i < NSTAGE; ++i) load_unit(i);
+  if (USE_TMA && tid == 0) load_unit(0);
 
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
@@ -313,7 +315,8 @@ __global__ void __launch_bounds__(NTHREADS)
   Unit Ucur, Uprev;  // units i and i-1 of this CTA
   Ucur.set((int)blockIdx.x, P);
   Uprev = Ucur;
-  unsigned long long* tim = P.timing ? P.timing + (size_t)blockIdx.x * P.timing_iters * 8 : nullptr;
+  unsigned long long* tim =
+      P.timing ? P.timing + (size_t)blockIdx.x * P.timing_iters * 8 : nullptr;
   for (int i = 0; i <= n_my; ++i) {
     if (tim && i < P.timing_iters && (tid == 0 || tid == NROWTHREADS))
       tim[i * 8 + (tid == 0 ? 0 : 4)] = clock64();
@@ -328,13 +331,14 @@ __global__ void __launch_bounds__(NTHREADS)
         if constexpr (USE_TMA) {
           mbar_wait(&bar[st], (uint32_t)((i / NSTAGE) & 1));
         } else {
-          // plain staged loads (unaligned shapes): row warps fill the stage
+          // plain staged loads (unaligned shapes): the row warps fill the stage
           LT* wpi = reinterpret_cast<LT*>(sb + L.pi);
           LT* wmu = reinterpret_cast<LT*>(sb + L.mu);
           int* wa = reinterpret_cast<int*>(sb + L.a);
           float* wr = reinterpret_cast<float*>(sb + L.r);
           float* wg = reinterpret_cast<float*>(sb + L.g);
           float* wv = reinterpret_cast<float*>(sb + L.v);
+          float* wb = reinterpret_cast<float*>(sb + L.boot);
           const LT* gpi = reinterpret_cast<const LT*>(P.pi);
           const LT* gmu = reinterpret_cast<const LT*>(P.mu);
           const int rowlen = BC * A;
@@ -349,22 +353,20 @@ __global__ void __launch_bounds__(NTHREADS)
             wpi[k] = zp;
             wmu[k] = zm;
           }
-          for (int k = tid; k < nrow; k += NROWTHREADS) {
+          for (int k = tid; k < nrow + BC; k += NROWTHREADS) {
             const int tl = k / BC, bl = k - tl * BC;
-            int av = 0;
-            float rv = 0.f, gv = 0.f, vv = 0.f;
-            if (tl < U.tlen && bl < U.blen) {
-              const long long gi = ((long long)(U.t0 + tl)) * B + U.b0 + bl;
-              av = P.actions[gi];
-              rv = P.rew[gi];
-              gv = P.disc[gi];
-              vv = P.val[gi];
+            const long long t = (long long)U.t0 + tl;
+            const bool ok = bl < U.blen && t < T && tl <= Tc;
+            const long long gi = t * B + U.b0 + bl;
+            if (k < nrow) {
+              const bool okr = ok && tl < U.tlen;
+              wa[k] = okr ? P.actions[gi] : 0;
+              wr[k] = okr ? P.rew[gi] : 0.f;
+              wg[k] = okr ? P.disc[gi] : 0.f;
             }
-            wa[k] = av;
-            wr[k] = rv;
-            wg[k] = gv;
-            wv[k] = vv;
+            wv[k] = ok ? P.val[gi] : 0.f;
           }
+          if (tid < BC) wb[tid] = tid < U.blen ? P.boot[U.b0 + tid] : 0.f;
           named_bar_sync(2, NROWTHREADS);
         }
         const int r = tid;
@@ -387,8 +389,19 @@ __global__ void __launch_bounds__(NTHREADS)
           row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
           // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
           const double ratio = (ea_p * S_m) / (ea_m * S_p);
+          // TD error r_t + gamma_t V(x_{t+1}) - V(x_t), V(x_T) = bootstrap
+          const float rt = r_t[r], gm = g_t[r], Vt = v_t[r];
+          float Vn;
+          if (tl + 1 < U.tlen || !U.last_chunk) {
+            Vn = v_t[r + BC];  // the V tile has Tc + 1 rows
+          } else {
+            Vn = reinterpret_cast<const float*>(sb + L.boot)[bl];
+            if (!isfinite(Vn)) record_bad(P.ws, T * B + U.b0 + bl, VT_DATA_VALUE);
+          }
+          const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
           const float Sf = (float)S_p, inv_S = __frcp_rn(Sf);
           reinterpret_cast<double*>(smem + L.ratio[par])[r] = ratio;
+          reinterpret_cast<double*>(smem + L.td[par])[r] = td;
           const float lse = m_p + __logf(Sf);  // log sum_j exp(z_j)
           reinterpret_cast<float*>(smem + L.lse[par])[r] = lse;
           reinterpret_cast<float*>(smem + L.csh[par])[r] = m_p + sed_p * inv_S;  // lse - H
@@ -400,10 +413,17 @@ __global__ void __launch_bounds__(NTHREADS)
           if (P.has_lm) P.lm_out[row] = (float)log(ea_m / S_m);
           if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
           if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
-          if (!isfinite(r_t[r])) record_bad(P.ws, row, VT_DATA_REWARD);
-          if (!isfinite(v_t[r])) record_bad(P.ws, row, VT_DATA_VALUE);
-          const float gm = g_t[r];
+          if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
+          if (!isfinite(Vt)) record_bad(P.ws, row, VT_DATA_VALUE);
           if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
+        }
+      }
+      if (tid == 0) {
+        // the gradient store of unit i-2 must have read its stage before the refill
+        if constexpr (LOSS && USE_TMA) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if constexpr (USE_TMA) {
+          fence_proxy_async_smem();  // generic reads of the stage before its async refill
+          load_unit(i + 1);          // stage (i+1)%3 == (i-2)%3
         }
       }
     } else if (i >= 1) {
@@ -411,16 +431,13 @@ __global__ void __launch_bounds__(NTHREADS)
       const Unit& U = Uprev;
       const int st = (i - 1) % NSTAGE, par = (i - 1) & 1;
       const unsigned char* sb = smem + (size_t)st * L.stage;
-      const float* r_t = reinterpret_cast<const float*>(sb + L.r);
       const float* g_t = reinterpret_cast<const float*>(sb + L.g);
-      const float* v_t = reinterpret_cast<const float*>(sb + L.v);
       const double* ratio_s = reinterpret_cast<const double*>(smem + L.ratio[par]);
-      float* vs_s = reinterpret_cast<float*>(smem + L.vs[par]);
-      float* pg_s = reinterpret_cast<float*>(smem + L.pg[par]);
-      float* adv_s = reinterpret_cast<float*>(smem + L.adv[par]);
+      const double* td_s = reinterpret_cast<const double*>(smem + L.td[par]);
+      double* adv_s = reinterpret_cast<double*>(smem + L.adv[par]);
       const int c = lane >> 2, sg = lane & 3;
       const bool col_ok = c < U.blen;
-      const int kk = (U.tlen + 3) >> 2;
+      const int kk = (U.tlen + 3) >> 2;  // <= KSEG
       const int s_beg = min(sg * kk, U.tlen), s_end = min(s_beg + kk, U.tlen);
       const bool need_carry = (P.K > 1) && !U.last_chunk;
       // early (speculative) look-back read: the predecessor is usually long done
@@ -431,31 +448,19 @@ __global__ void __launch_bounds__(NTHREADS)
       const int up0 = U.u - P.G;
       if (need_carry && col_ok && sg == 0)
         ld_tag16(P.recs + ((size_t)up0 * BC + c) * RECS_PER_COL + 2, incl0, t0tag);
-      double V_after = 0.0;  // V(x) just after this chunk (next chunk's first V, or bootstrap)
-      if (col_ok && s_end == U.tlen && s_beg < s_end) {
-        if (U.last_chunk) {
-          const float bv = __ldg(P.boot + U.b0 + c);
-          if (!isfinite(bv)) record_bad(P.ws, T * B + U.b0 + c, VT_DATA_VALUE);
-          V_after = (double)bv;
-        } else {
-          V_after = (double)__ldg(P.val + (long long)(U.t0 + U.tlen) * B + U.b0 + c);
-        }
-      }
-      // local affine aggregate of the segment: A_beg = D + G * A_end  (Remark 1)
-      double G = 1.0, D = 0.0;
-      if (col_ok) {
-        double Vn = (s_end < U.tlen) ? (double)v_t[s_end * BC + c] : V_after;
-        for (int s = s_end - 1; s >= s_beg; --s) {
-          const int q = s * BC + c;
+      // per step: delta_t = rho_t td_t and g_t = gamma_t c_t (Remark 2 P:225);
+      // delta_t is parked in adv_s (overwritten by A_t in the second pass)
+      double G = 1.0, D = 0.0;  // local affine aggregate: A_beg = D + G * A_end
+#pragma unroll
+      for (int k = KSEG - 1; k >= 0; --k) {
+        if (col_ok && s_beg + k < s_end) {
+          const int q = (s_beg + k) * BC + c;
           const double ratio = ratio_s[q];
-          const double rho = fmin(P.rho_bar, ratio);
-          const double cc = P.lambda * fmin(P.c_bar, ratio);
-          const double gam = (double)g_t[q];
-          const double Vt = (double)v_t[q];
-          const double delta = rho * (reward_transform(r_t[q], P.reward_mode) + gam * Vn - Vt);
-          D = fma(gam * cc, D, delta);
-          G = gam * cc * G;
-          Vn = Vt;
+          const double dl = fmin(P.rho_bar, ratio) * td_s[q];
+          const double gc = (double)g_t[q] * (P.lambda * fmin(P.c_bar, ratio));
+          adv_s[q] = dl;
+          D = fma(gc, D, dl);
+          G = gc * G;
         }
       }
       // suffix scan over the 4 segments of each column (width-4 shuffles)
@@ -518,33 +523,18 @@ __global__ void __launch_bounds__(NTHREADS)
         // publish the inclusive carry: A at this chunk's first step
         if (U.kchunk > 0 && col_ok && sg == 0) st_tag16(my + 2, fma(Gi, carry, Di), tagI);
       }
-      // second pass over the segment: v_t, q_t, pg_adv_t
-      if (col_ok) {
-        double A_next = fma(Ge, carry, De);  // A at s_end
-        double V_next = (s_end < U.tlen) ? (double)v_t[s_end * BC + c] : V_after;
-        for (int s = s_end - 1; s >= s_beg; --s) {
-          const int q = s * BC + c;
-          const double ratio = ratio_s[q];
-          const double rho = fmin(P.rho_bar, ratio);
-          const double cc = P.lambda * fmin(P.c_bar, ratio);
-          const double rho_pg = fmin(P.pg_rho_bar, ratio);
-          const double gam = (double)g_t[q];
-          const double Vt = (double)v_t[q];
-          const double rr = reward_transform(r_t[q], P.reward_mode);
-          const double delta = rho * (rr + gam * V_next - Vt);
-          const double A_t = fma(gam * cc, A_next, delta);
-          const double v_next = V_next + A_next;  // v_{t+1}; v_T = V(x_T)
-          vs_s[q] = (float)(Vt + A_t);
-          pg_s[q] = (float)(rho_pg * (rr + gam * v_next - Vt));
-          adv_s[q] = (float)A_t;
-          A_next = A_t;
-          V_next = Vt;
+      // second pass: A_t = delta_t + g_t A_{t+1}  (Remark 1)
+      double A_next = fma(Ge, carry, De);  // A at s_end
+      if (col_ok && sg == 0) adv_s[U.tlen * BC + c] = carry;  // A just after the chunk
+#pragma unroll
+      for (int k = KSEG - 1; k >= 0; --k) {
+        if (col_ok && s_beg + k < s_end) {
+          const int q = (s_beg + k) * BC + c;
+          const double gc = (double)g_t[q] * (P.lambda * fmin(P.c_bar, ratio_s[q]));
+          A_next = fma(gc, A_next, adv_s[q]);
+          adv_s[q] = A_next;
         }
       }
-    }
-    if constexpr (LOSS && USE_TMA) {
-      // the previous unit's dlogits store must have read the tile before P3 rewrites it
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     if (tim && i < P.timing_iters && (tid == 0 || tid == NROWTHREADS))
       tim[i * 8 + (tid == 0 ? 1 : 5)] = clock64();
@@ -555,33 +545,40 @@ __global__ void __launch_bounds__(NTHREADS)
     if (warp < NROWWARPS && i >= 1) {
       const Unit& U = Uprev;
       const int st = (i - 1) % NSTAGE, par = (i - 1) & 1;
-      const unsigned char* sb = smem + (size_t)st * L.stage;
-      LT* dz_t = reinterpret_cast<LT*>(smem + L.dz);
+      unsigned char* sb = smem + (size_t)st * L.stage;
       const int r = tid;
       const int tl = r >> 3, bl = r & 7;
       if (r < nrow && tl < U.tlen && bl < U.blen) {
         const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
-        const float vsr = reinterpret_cast<const float*>(smem + L.vs[par])[r];
-        const float pgr = reinterpret_cast<const float*>(smem + L.pg[par])[r];
+        const double* adv_s = reinterpret_cast<const double*>(smem + L.adv[par]);
+        const double A_t = adv_s[r], A_n = adv_s[r + BC];  // A_t and A_{t+1}
+        const double ratio = reinterpret_cast<const double*>(smem + L.ratio[par])[r];
+        const double td = reinterpret_cast<const double*>(smem + L.td[par])[r];
+        const float gm = reinterpret_cast<const float*>(sb + L.g)[r];
+        const float Vt = reinterpret_cast<const float*>(sb + L.v)[r];
+        // v_t = V(x_t) + A_t;  pg_adv_t = rho_pg (r_t + gamma_t v_{t+1} - V(x_t))
+        //                              = rho_pg (td_t + gamma_t A_{t+1})
+        const float vsr = (float)((double)Vt + A_t);
+        const float pgr = (float)(fmin(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
         if (P.vs) P.vs[row] = vsr;
         if (P.pg_adv) P.pg_adv[row] = pgr;
         if constexpr (LOSS) {
-          const float Ar = reinterpret_cast<const float*>(smem + L.adv[par])[r];
+          const float Ar = (float)A_t;
           const float lse = reinterpret_cast<const float*>(smem + L.lse[par])[r];
           const float cshift = reinterpret_cast<const float*>(smem + L.csh[par])[r];
           const float rest = reinterpret_cast<const float*>(smem + L.rest[par])[r];
           const float pa = 1.f - rest;  // pi(a); only scaled by c_e below
           const int a = min(max(reinterpret_cast<const int*>(sb + L.a)[r], 0), A - 1);
-          const LT* zrow = reinterpret_cast<const LT*>(sb + L.pi) + (size_t)r * A;
+          LT* zrow = reinterpret_cast<LT*>(sb + L.pi) + (size_t)r * A;  // dz overwrites z
           RowRegs<LT, A_CT> zp;
           zp.load(zrow);
+          const float za = Elem<LT>::get(zrow, a);
           const float L2E = 1.44269504088896341f;
           const float lseL = lse * L2E;
-          LT* dzrow = dz_t + (size_t)r * A;
           float sq = 0.f;
           // dz_j = pi_j (pg + c_e (log pi_j + H))   (j != a)
           if constexpr (RowRegs<LT, A_CT>::kPacked) {
-            uint32_t* w = reinterpret_cast<uint32_t*>(dzrow);
+            uint32_t* w = reinterpret_cast<uint32_t*>(zrow);
 #pragma unroll
             for (int k = 0; k < A_CT / 2; ++k) {
               const float z0 = zp.get(2 * k), z1 = zp.get(2 * k + 1);
@@ -592,21 +589,26 @@ __global__ void __launch_bounds__(NTHREADS)
               __nv_bfloat162 h2 = __floats2bfloat162_rn(d0, d1);
               w[k] = *reinterpret_cast<uint32_t*>(&h2);
             }
-          } else {
-            const int nA = A_CT > 0 ? A_CT : A;
-#pragma unroll 4
-            for (int j = 0; j < nA; ++j) {
+          } else if constexpr (A_CT > 0) {
+#pragma unroll
+            for (int j = 0; j < A_CT; ++j) {
               const float z = zp.get(j);
               const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z - cshift, pgr);
               sq = fmaf(d, d, sq);
-              dzrow[j] = store_cvt<LT>(d);
+              zrow[j] = store_cvt<LT>(d);
+            }
+          } else {
+            for (int j = 0; j < A; ++j) {
+              const float z = zp.get(j);
+              const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z - cshift, pgr);
+              sq = fmaf(d, d, sq);
+              zrow[j] = store_cvt<LT>(d);
             }
           }
           // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
-          const float za = Elem<LT>::get(zrow, a);
           const float d_wrong = ex2_approx(fmaf(za, L2E, -lseL)) * fmaf(ce, za - cshift, pgr);
           const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
-          dzrow[a] = store_cvt<LT>(d_a);
+          zrow[a] = store_cvt<LT>(d_a);
           sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
           if (tim && i < P.timing_iters && tid == 0) tim[i * 8 + 6] = clock64();
           const float dv = -cv * Ar;  // c_v (V - v)
@@ -618,23 +620,19 @@ __global__ void __launch_bounds__(NTHREADS)
           acc_dv = fmaf(dv, dv, acc_dv);
           if constexpr (!USE_TMA) {
             LT* gdz = reinterpret_cast<LT*>(P.dlogits) + row * A;
-            for (int j = 0; j < A; ++j) gdz[j] = dzrow[j];
+            for (int j = 0; j < A; ++j) gdz[j] = zrow[j];
           }
         }
       }
-      if constexpr (LOSS && USE_TMA) fence_proxy_async_smem();
-      named_bar_sync(2, NROWTHREADS);  // dz tile complete; stage (i-1) consumed
-      if (tid == 0) {
-        if constexpr (LOSS && USE_TMA) {
-          tma_store_2d(&maps.dz, (int)(U.b0 * A), U.t0, dz_t);
+      if constexpr (LOSS && USE_TMA) {
+        fence_proxy_async_smem();
+        named_bar_sync(2, NROWTHREADS);  // the gradient tile is complete
+        if (tid == 0) {
+          tma_store_2d(&maps.dz, (int)(U.b0 * A), U.t0, sb + L.pi);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if constexpr (USE_TMA) {
-          fence_proxy_async_smem();  // generic reads of the stage before its async refill
-          load_unit(i + 2);          // stage (i-1)%3 == (i+2)%3
-        }
-        if (tim && i < P.timing_iters) tim[i * 8 + 3] = clock64();
       }
+      if (tim && i < P.timing_iters && tid == 0) tim[i * 8 + 3] = clock64();
     }
     Uprev = Ucur;
     Ucur.advance(P, stride);
@@ -795,6 +793,19 @@ static bool encode_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, 
   return r == CUDA_SUCCESS;
 }
 
+static bool encode_1d(CUtensorMap* m, const void* base, long long n, int box) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t bx[1] = {(cuuint32_t)box};
+  cuuint32_t estr[1] = {1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(base), dims, strides,
+                   bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 static int exp_mode() {
   static int mode = -1;
   if (mode < 0) {
@@ -946,8 +957,9 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   std::memset(&maps, 0, sizeof(maps));
   bool tma = (A * BC <= 256) && (B * A < (1LL << 31)) && (T < (1LL << 31)) && ((B * A * elem) % 16 == 0) && ((B * 4) % 16 == 0) &&
              aligned(mu, 16) && aligned(pi, 16) && aligned(actions, 16) && aligned(disc, 16) &&
-             aligned(rew, 16) && aligned(val, 16) && (!loss || aligned(dlogits, 16)) &&
-             plan.Tc <= 256 && plan.smem <= kMaxSmem;
+             aligned(rew, 16) && aligned(val, 16) && aligned(boot, 16) &&
+             (!loss || aligned(dlogits, 16)) &&
+             plan.Tc + 1 <= 256 && plan.smem <= kMaxSmem;
   if (tma) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -956,7 +968,8 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
           encode_2d(&maps.a, actions, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, B, T, BC, plan.Tc) &&
           encode_2d(&maps.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc) &&
           encode_2d(&maps.g, disc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc) &&
-          encode_2d(&maps.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc) &&
+          encode_2d(&maps.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc + 1) &&
+          encode_1d(&maps.boot, boot, B, BC) &&
           (!loss || encode_2d(&maps.dz, dlogits, ldt, elem, B * A, T, BC * (int)A, plan.Tc));
   }
   if (plan.smem > kMaxSmem) return VT_ERR_SHAPE;
