@@ -26,7 +26,8 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
-        cmd = [NVCC, *FLAGS, "-o", SO + ".tmp", *SOURCES]
+        extra = ["-DVTRACE_TIMING"] if os.environ.get("VTRACE_TIMING") else []
+        cmd = [NVCC, *FLAGS, *extra, "-o", SO + ".tmp", *SOURCES]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)

@@ -32,40 +32,42 @@ __device__ __forceinline__ __nv_bfloat16 store_cvt<__nv_bfloat16>(float x) {
   return __float2bfloat16_rn(x);
 }
 
-// A logits row held in registers (compile-time A) or read from smem (A_CT == 0).
+// A logits row held in registers as fp32 (compile-time A, unpacked once) or
+// read from shared memory (A_CT == 0).
 template <typename LT, int A_CT>
 struct RowRegs {
   static constexpr bool kPacked = (sizeof(LT) == 2) && (A_CT % 2 == 0) && (A_CT > 0);
-  static constexpr int kWords = kPacked ? A_CT / 2 : (A_CT > 0 ? A_CT : 1);
-  uint32_t w[kWords];
+  static constexpr int kN = A_CT > 0 ? A_CT : 1;
+  float z[kN];
   const LT* src;
   __device__ __forceinline__ void load(const LT* row) {
     src = row;
     if constexpr (kPacked) {
       const uint32_t* p = reinterpret_cast<const uint32_t*>(row);
 #pragma unroll
-      for (int k = 0; k < kWords; ++k) w[k] = p[k];
+      for (int k = 0; k < A_CT / 2; ++k) {
+        const uint32_t x = p[k];
+        z[2 * k] = __uint_as_float(x << 16);
+        z[2 * k + 1] = __uint_as_float(x & 0xffff0000u);
+      }
     } else if constexpr (A_CT > 0) {
       if constexpr (sizeof(LT) == 4 && (A_CT % 2) == 0) {
         const float2* p = reinterpret_cast<const float2*>(row);
 #pragma unroll
         for (int k = 0; k < A_CT / 2; ++k) {
-          float2 x = p[k];
-          w[2 * k] = __float_as_uint(x.x);
-          w[2 * k + 1] = __float_as_uint(x.y);
+          const float2 x = p[k];
+          z[2 * k] = x.x;
+          z[2 * k + 1] = x.y;
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < A_CT; ++j) w[j] = __float_as_uint(Elem<LT>::get(row, j));
+        for (int j = 0; j < A_CT; ++j) z[j] = Elem<LT>::get(row, j);
       }
     }
   }
   __device__ __forceinline__ float get(int j) const {  // j compile-time in unrolled loops
-    if constexpr (kPacked) {
-      const uint32_t x = w[j >> 1];
-      return (j & 1) ? __uint_as_float(x & 0xffff0000u) : __uint_as_float(x << 16);
-    } else if constexpr (A_CT > 0) {
-      return __uint_as_float(w[j]);
+    if constexpr (A_CT > 0) {
+      return z[j];
     } else {
       return Elem<LT>::get(src, j);
     }
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(NTHREADS, 3)
   const int Tc = P.Tc;
   const int nrow = Tc * BC;
   const long long T = P.T, B = P.B;
-  const Layout L = make_layout(nrow, A, (int)sizeof(LT));
+  const KLayout& L = P.L;
   const int stride = (int)gridDim.x;
   const int n_my = (P.units - (int)blockIdx.x + stride - 1) / stride;  // units of this CTA
 
@@ -315,8 +317,12 @@ __global__ void __launch_bounds__(NTHREADS, 3)
   Unit Ucur, Uprev;  // units i and i-1 of this CTA
   Ucur.set((int)blockIdx.x, P);
   Uprev = Ucur;
+#ifdef VTRACE_TIMING
   unsigned long long* tim =
       P.timing ? P.timing + (size_t)blockIdx.x * P.timing_iters * 8 : nullptr;
+#else
+  constexpr unsigned long long* tim = nullptr;  // phase timing compiled out
+#endif
   for (int i = 0; i <= n_my; ++i) {
     if (tim && i < P.timing_iters && (tid == 0 || tid == NROWTHREADS))
       tim[i * 8 + (tid == 0 ? 0 : 4)] = clock64();
@@ -379,14 +385,19 @@ __global__ void __launch_bounds__(NTHREADS, 3)
           const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
           const int a_raw = a_t[r];
           const int a = min(max(a_raw, 0), A - 1);
-          RowRegs<LT, A_CT> zp, zm;
-          zp.load(pi_t + (size_t)r * A);
-          zm.load(mu_t + (size_t)r * A);
           float m_p, m_m, sed_p, sed_m;
           double S_p, S_m, ea_p, ea_m;
           bool fin_p, fin_m;
-          row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, ea_p, sed_p, fin_p);
-          row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
+          {
+            RowRegs<LT, A_CT> zp;
+            zp.load(pi_t + (size_t)r * A);
+            row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, ea_p, sed_p, fin_p);
+          }
+          {
+            RowRegs<LT, A_CT> zm;
+            zm.load(mu_t + (size_t)r * A);
+            row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
+          }
           // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
           const double ratio = (ea_p * S_m) / (ea_m * S_p);
           // TD error r_t + gamma_t V(x_{t+1}) - V(x_t), V(x_T) = bootstrap
@@ -947,6 +958,18 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   P.c_v = loss ? (double)w->baseline_cost : 0.0;
   P.c_e = loss ? (double)w->entropy_cost : 0.0;
   unsigned char* wsb = static_cast<unsigned char*>(ws);
+  {
+    const Layout Lh = make_layout(plan.Tc * BC, (int)A, elem);
+    KLayout& K = P.L;
+    K.pi = (unsigned)Lh.pi; K.mu = (unsigned)Lh.mu; K.a = (unsigned)Lh.a; K.r = (unsigned)Lh.r;
+    K.g = (unsigned)Lh.g; K.v = (unsigned)Lh.v; K.boot = (unsigned)Lh.boot;
+    K.stage = (unsigned)Lh.stage;
+    for (int q = 0; q < 2; ++q) {
+      K.ratio[q] = (unsigned)Lh.ratio[q]; K.td[q] = (unsigned)Lh.td[q];
+      K.adv[q] = (unsigned)Lh.adv[q]; K.lse[q] = (unsigned)Lh.lse[q];
+      K.csh[q] = (unsigned)Lh.csh[q]; K.rest[q] = (unsigned)Lh.rest[q];
+    }
+  }
   P.ws = reinterpret_cast<WsHeader*>(wsb);
   const WsLayout wl = ws_layout(plan);
   P.recs = reinterpret_cast<TagRec*>(wsb + wl.recs);

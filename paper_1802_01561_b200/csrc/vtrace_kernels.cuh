@@ -58,6 +58,13 @@ struct alignas(16) TagRec {
 static_assert(sizeof(TagRec) == 16, "TagRec layout");
 constexpr int RECS_PER_COL = 3;  // G, D, incl
 
+// Shared-memory offsets of one CTA (computed on the host, read from the
+// kernel's parameter space so they never occupy registers).
+struct KLayout {
+  unsigned int pi, mu, a, r, g, v, boot, stage;
+  unsigned int ratio[2], td[2], adv[2], lse[2], csh[2], rest[2];
+};
+
 struct Params {
   long long T, B;
   int A, Tc, K, G, units;
@@ -86,6 +93,7 @@ struct Params {
   unsigned long long* timing;  // debug: per-CTA phase timestamps (NULL = off)
   int timing_iters;
   int stride_q, stride_r;  // gridDim.x = stride_q * G + stride_r
+  KLayout L;
 };
 
 struct TmaMaps {
