@@ -75,14 +75,16 @@ struct RowRegs {
 };
 
 // Statistics of one logits row: m = max z, S = sum_j exp(z_j - m) (accurate to
-// ~1e-8 relative), ea = exp(z_a - m) in fp64, and sed = sum_j e_j (z_j - m)
-// (for the entropy, fp32).  MUFU mode: ex2.approx on the fp32 argument, whose
+// ~1e-8 relative), xa = z_a - m (exact, fp64), ea_f = exp(z_a - m) (fp32; it is
+// exactly 1 when a is the argmax), and sed = sum_j e_j (z_j - m) (for the
+// entropy, fp32).  MUFU mode: ex2.approx on the fp32 argument, whose
 // rounding residual (and, for fp32 logits, that of z - m) enters as a
 // first-order correction sum_j e_j * ln2 * residual_j; the e_j are added with
 // Fast2Sum (s_hi starts at 1 >= every term, so each step is exact).
 template <typename LT, int A_CT, int MODE>
 __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int a, float& m,
-                                          double& S, double& ea, float& sed, bool& finite) {
+                                          double& S, double& xa, float& ea_f, float& sed,
+                                          bool& finite) {
   constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m is exact in fp32 for bf16 inputs
   constexpr int NA = A_CT > 0 ? A_CT : 1;
   const int nA = A_CT > 0 ? A_CT : A;
@@ -97,7 +99,7 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   auto term = [&](float z) {
     const float d = z - m;
     if constexpr (MODE == EXP_F64) {
-      const double e = exp64_nonpos((double)z - (double)m);
+      const double e = exp64((double)z - (double)m);
       S64 += e;
       sd = fmaf((float)e, d, sd);
       chk = __fmaf_rn(z, 0.f, chk);
@@ -125,7 +127,8 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
     for (int j = 0; j < nA; ++j) term(R.get(j));
   }
   const float za = Elem<LT>::get(R.src, a);
-  ea = exp64_nonpos((double)za - (double)m);
+  xa = (double)za - (double)m;  // z_a - m, exact
+  ea_f = ex2_approx((za - m) * 1.44269504088896341f);  // exp(z_a - m), fp32 (exactly 1 at the max)
   sed = sd;
   if constexpr (MODE == EXP_F64) {
     S = S64;
@@ -165,9 +168,9 @@ __device__ __forceinline__ void record_bad(WsHeader* ws, long long row, int kind
 //     the carry from the later chunks)
 
 constexpr int NSTAGE = 3;
-constexpr int NROWWARPS = NWARPS - 1;       // warps 0..6 own rows, warp 7 runs the scan
-constexpr int NROWTHREADS = NROWWARPS * 32;  // 224 >= Tc * 8
-constexpr int KSEG = (NROWTHREADS / BC + 3) / 4;  // steps per scan lane (Tc <= 28)
+constexpr int NROWWARPS = NWARPS - 1;       // warps 0..4 own rows, warp 5 runs the scan
+constexpr int NROWTHREADS = NROWWARPS * 32;  // 160 >= Tc * 8
+constexpr int KSEG = (NROWTHREADS / BC + 3) / 4;  // steps per scan lane (Tc <= 20)
 
 struct Layout {
   size_t pi, mu, a, r, g, v, boot, stage;          // offsets inside a stage
@@ -209,16 +212,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// geometry of one work unit
+// geometry of one work unit (T, B < 2^31: 32-bit arithmetic)
 struct Unit {
-  int u, kchunk, grp, t0, tlen, blen;
-  long long b0;
+  int u, kchunk, grp, t0, tlen, b0, blen;
   bool last_chunk;
   __device__ __forceinline__ void finish(const Params& P) {
     t0 = kchunk * P.Tc;
-    tlen = (int)min((long long)P.Tc, P.T - t0);
-    b0 = (long long)grp * BC;
-    blen = (int)min((long long)BC, P.B - b0);
+    tlen = min(P.Tc, P.T32 - t0);
+    b0 = grp * BC;
+    blen = min(BC, P.B32 - b0);
     last_chunk = (kchunk == P.K - 1);
   }
   __device__ __forceinline__ void set(int uu, const Params& P) {
@@ -257,13 +259,14 @@ struct Unit {
 // so the latency-bound recursion overlaps the row arithmetic of the next unit.
 
 template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE>
-__global__ void __launch_bounds__(NTHREADS, 3)
+__global__ void __launch_bounds__(NTHREADS, 4)
     vtrace_fused_kernel(const Params P, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[NSTAGE];
   __shared__ unsigned int s_epoch;
   __shared__ int s_last;
   __shared__ double s_red[NWARPS][NPART];
+  __shared__ double s_fin[NPART];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int A = (A_CT > 0) ? A_CT : P.A;
@@ -385,21 +388,21 @@ __global__ void __launch_bounds__(NTHREADS, 3)
           const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
           const int a_raw = a_t[r];
           const int a = min(max(a_raw, 0), A - 1);
-          float m_p, m_m, sed_p, sed_m;
-          double S_p, S_m, ea_p, ea_m;
+          float m_p, m_m, sed_p, sed_m, ea_p, ea_m;
+          double S_p, S_m, xa_p, xa_m;
           bool fin_p, fin_m;
           {
             RowRegs<LT, A_CT> zp;
             zp.load(pi_t + (size_t)r * A);
-            row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, ea_p, sed_p, fin_p);
+            row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, xa_p, ea_p, sed_p, fin_p);
           }
           {
             RowRegs<LT, A_CT> zm;
             zm.load(mu_t + (size_t)r * A);
-            row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, ea_m, sed_m, fin_m);
+            row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, xa_m, ea_m, sed_m, fin_m);
           }
-          // pi(a)/mu(a) = (ea_p / S_p) / (ea_m / S_m)
-          const double ratio = (ea_p * S_m) / (ea_m * S_p);
+          // pi(a)/mu(a) = exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) S_mu / S_pi
+          const double ratio = exp64(xa_p - xa_m) * (S_m / S_p);
           // TD error r_t + gamma_t V(x_{t+1}) - V(x_t), V(x_T) = bootstrap
           const float rt = r_t[r], gm = g_t[r], Vt = v_t[r];
           float Vn;
@@ -416,12 +419,12 @@ __global__ void __launch_bounds__(NTHREADS, 3)
           const float lse = m_p + __logf(Sf);  // log sum_j exp(z_j)
           reinterpret_cast<float*>(smem + L.lse[par])[r] = lse;
           reinterpret_cast<float*>(smem + L.csh[par])[r] = m_p + sed_p * inv_S;  // lse - H
-          reinterpret_cast<float*>(smem + L.rest[par])[r] = (float)(S_p - ea_p) * inv_S;
+          reinterpret_cast<float*>(smem + L.rest[par])[r] = (float)(S_p - (double)ea_p) * inv_S;
           acc_rho += (float)fmin(P.rho_bar, ratio);
           acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
           if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
-          if (P.has_lp) P.lp_out[row] = (float)log(ea_p / S_p);
-          if (P.has_lm) P.lm_out[row] = (float)log(ea_m / S_m);
+          if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
+          if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
           if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
           if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
           if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
@@ -678,18 +681,18 @@ __global__ void __launch_bounds__(NTHREADS, 3)
   if (s_last) {
     __threadfence();
     if (LOSS && P.partials) {
-      if (warp < NPART) {  // warp k: partial k; lanes stride the CTAs, then lane order
-        double x = 0.0;
+      for (int k = warp; k < NPART; k += NWARPS) {  // warp w: partials w, w + NWARPS
+        double x = 0.0;  // lanes stride the CTAs, then lane order: a fixed tree
         for (int v = lane; v < (int)gridDim.x; v += 32)
-          x += __ldcg(P.cta_partials + (size_t)v * NPART + warp);
+          x += __ldcg(P.cta_partials + (size_t)v * NPART + k);
         double tot = 0.0;
         for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, x, l);
-        if (lane == 0) s_red[warp][0] = tot;
+        if (lane == 0) s_fin[k] = tot;
       }
       __syncthreads();
       if (tid == 0) {
         double out[NPART];
-        for (int k = 0; k < NPART; ++k) out[k] = s_red[k][0];
+        for (int k = 0; k < NPART; ++k) out[k] = s_fin[k];
         out[VT_P_TOTAL_LOSS] = out[VT_P_PG_LOSS] + P.c_v * out[VT_P_BASELINE_LOSS] -
                                P.c_e * out[VT_P_ENTROPY_SUM];
         for (int k = 0; k < NPART; ++k) P.partials[k] = out[k];
@@ -943,7 +946,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
 
   Params P;
   std::memset(&P, 0, sizeof(P));
-  P.T = T; P.B = B; P.A = (int)A; P.Tc = plan.Tc; P.K = plan.K; P.G = plan.G;
+  P.T = T; P.B = B; P.A = (int)A; P.T32 = (int)T; P.B32 = (int)B; P.Tc = plan.Tc; P.K = plan.K; P.G = plan.G;
   P.units = plan.units;
   P.has_lr = lr != nullptr; P.has_lp = lp != nullptr; P.has_lm = lm != nullptr;
   P.mu = mu; P.pi = pi; P.actions = actions; P.disc = disc; P.rew = rew; P.val = val;

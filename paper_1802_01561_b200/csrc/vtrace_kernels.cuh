@@ -31,7 +31,7 @@
 namespace vtb200 {
 
 constexpr int BC = 8;          // trajectories (columns) per unit
-constexpr int NWARPS = 8;      // one warp per column in the scan phase
+constexpr int NWARPS = 6;      // 5 row warps + 1 scan warp
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int NPART = 8;
 
@@ -67,6 +67,7 @@ struct KLayout {
 
 struct Params {
   long long T, B;
+  int T32, B32;
   int A, Tc, K, G, units;
   int has_lr, has_lp, has_lm;
   const void* mu;
@@ -243,15 +244,15 @@ __device__ __forceinline__ void load_row(const LT* row, float (&z)[A_CT]) {
   }
 }
 
-// fp64 exp for x <= 0 (clamped at -700).  Cody-Waite reduction
+// fp64 exp, argument clamped to [-700, 700].  Cody-Waite reduction
 // x = n ln2 + r, |r| <= ln2/2, then a degree-6 polynomial fitted to exp on
 // that interval (max relative error 1.9e-9; the path needs ~1e-8).
-__device__ __forceinline__ double exp64_nonpos(double x) {
+__device__ __forceinline__ double exp64(double x) {
   const double LOG2E = 1.4426950408889634;
   const double LN2_HI = 6.93147180369123816490e-01;
   const double LN2_LO = 1.90821492927058770002e-10;
   const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
-  x = fmax(x, -700.0);
+  x = fmin(fmax(x, -700.0), 700.0);
   double t = fma(x, LOG2E, MAGIC);
   double n = t - MAGIC;
   int ni = __double2loint(t);
@@ -264,7 +265,7 @@ __device__ __forceinline__ double exp64_nonpos(double x) {
   p = fma(p, r, 4.99999914930370937e-01);
   p = fma(p, r, 1.00000003612590005e+00);
   p = fma(p, r, 1.00000000059202110e+00);
-  // scale by 2^n: add n to the exponent field (p in [0.7, 1.5], n >= -1010)
+  // scale by 2^n: add n to the exponent field (p in [0.7, 1.5], |n| <= 1010)
   int hi = __double2hiint(p) + (ni << 20);
   return __hiloint2double(hi, __double2loint(p));
 }
