@@ -246,7 +246,8 @@ __device__ __forceinline__ void load_row(const LT* row, float (&z)[A_CT]) {
 
 // fp64 exp, argument clamped to [-700, 700].  Cody-Waite reduction
 // x = n ln2 + r, |r| <= ln2/2, then a degree-6 polynomial fitted to exp on
-// that interval (max relative error 1.9e-9; the path needs ~1e-8).
+// that interval as 1 + r q(r) (max relative error 2.2e-9; the path needs ~1e-8,
+// DESIGN.md; exp(0) = 1 exactly).
 __device__ __forceinline__ double exp64(double x) {
   const double LOG2E = 1.4426950408889634;
   const double LN2_HI = 6.93147180369123816490e-01;
@@ -258,13 +259,14 @@ __device__ __forceinline__ double exp64(double x) {
   int ni = __double2loint(t);
   double r = fma(-n, LN2_HI, x);
   r = fma(-n, LN2_LO, r);
-  double p = 1.38294205944386960e-03;
-  p = fma(p, r, 8.37477152027917178e-03);
-  p = fma(p, r, 4.16683580330002093e-02);
-  p = fma(p, r, 1.66664208321203350e-01);
-  p = fma(p, r, 4.99999914930370937e-01);
-  p = fma(p, r, 1.00000003612590005e+00);
-  p = fma(p, r, 1.00000000059202110e+00);
+  // p(r) = 1 + r q(r): exact at r = 0, so exp(0) == 1 bitwise (on-policy ratio)
+  double q = 1.38592910771707131e-03;
+  q = fma(q, r, 8.37476397493414765e-03);
+  q = fma(q, r, 4.16677243209218270e-02);
+  q = fma(q, r, 1.66664209451321627e-01);
+  q = fma(q, r, 4.99999953509942752e-01);
+  q = fma(q, r, 1.00000003609212618e+00);
+  const double p = fma(q, r, 1.0);
   // scale by 2^n: add n to the exponent field (p in [0.7, 1.5], |n| <= 1010)
   int hi = __double2hiint(p) + (ni << 20);
   return __hiloint2double(hi, __double2loint(p));
