@@ -277,6 +277,13 @@ __global__ void __launch_bounds__(NTHREADS, 4)
   const int stride = (int)gridDim.x;
   const int n_my = (P.units - (int)blockIdx.x + stride - 1) / stride;  // units of this CTA
 
+#ifdef VTRACE_TIMING
+  if (P.timing && tid == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.timing[(size_t)blockIdx.x * P.timing_iters * 8 + (P.timing_iters - 1) * 8 + 0] = g;
+  }
+#endif
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch);
     if constexpr (USE_TMA) {
@@ -339,6 +346,13 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         const LT* mu_t = reinterpret_cast<const LT*>(sb + L.mu);
         if constexpr (USE_TMA) {
           mbar_wait(&bar[st], (uint32_t)((i / NSTAGE) & 1));
+#ifdef VTRACE_TIMING
+          if (P.timing && tid == 0 && i == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            P.timing[(size_t)blockIdx.x * P.timing_iters * 8 + (P.timing_iters - 1) * 8 + 3] = g;
+          }
+#endif
         } else {
           // plain staged loads (unaligned shapes): the row warps fill the stage
           LT* wpi = reinterpret_cast<LT*>(sb + L.pi);
@@ -652,6 +666,13 @@ __global__ void __launch_bounds__(NTHREADS, 4)
     Ucur.advance(P, stride);
   }
 
+#ifdef VTRACE_TIMING
+  if (P.timing && tid == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    P.timing[(size_t)blockIdx.x * P.timing_iters * 8 + (P.timing_iters - 1) * 8 + 1] = g;
+  }
+#endif
   // ---- a12: CTA partials (fixed order), then the last CTA out reduces them ---------
   {
     const double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
@@ -698,6 +719,13 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         for (int k = 0; k < NPART; ++k) P.partials[k] = out[k];
       }
     }
+#ifdef VTRACE_TIMING
+    if (P.timing && tid == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      P.timing[(size_t)blockIdx.x * P.timing_iters * 8 + (P.timing_iters - 1) * 8 + 2] = g;
+    }
+#endif
     if (tid == 0) {
       P.ws->exited = 0u;
       __threadfence();

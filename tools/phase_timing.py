@@ -29,10 +29,10 @@ pkg.loss_and_grad(*args, workspace=ws, reward_mode=inp["reward_mode"])
 torch.cuda.synchronize()
 lib.vtrace_debug_set_timing(None, 0)
 t = buf.view(GRID, ITERS, 8).cpu().numpy().astype(np.int64)
-used = t[:, :, 0] != 0
+used = t[:, :ITERS - 1, 0] != 0
 rows = []
 for c in range(GRID):
-    for i in range(ITERS):
+    for i in range(ITERS - 1):
         if not used[c, i]:
             continue
         r = t[c, i]
@@ -40,7 +40,14 @@ for c in range(GRID):
                          scan_rest=r[5] - r[7], p3_rows=r[6] - r[2], p3_tail=r[3] - r[6],
                          wait_row=r[2] - r[1],
                          wait_scan=r[2] - r[5], p3=r[3] - r[2],
-                         iter=(t[c, i + 1, 0] - r[0]) if i + 1 < ITERS and used[c, i + 1] else 0))
+                         iter=(t[c, i + 1, 0] - r[0]) if i + 1 < ITERS - 1 and used[c, i + 1] else 0))
+g = t[:, ITERS - 1, :4]
+ok = g[:, 0] > 0
+if ok.any():
+    g0 = g[ok, 0].min()
+    print("globaltimer (ns from first CTA start): start med %.0f max %.0f | first data med %.0f max %.0f | loop end med %.0f max %.0f | last CTA done %.0f" % (
+        np.median(g[ok, 0] - g0), (g[ok, 0] - g0).max(), np.median(g[ok, 3] - g0), (g[ok, 3] - g0).max(),
+        np.median(g[ok, 1] - g0), (g[ok, 1] - g0).max(), (g[ok, 2].max() - g0) if (g[ok, 2] > 0).any() else -1))
 keys = ["p1", "scan", "scan_local", "scan_rest", "wait_row", "p3", "p3_rows", "p3_tail", "iter"]
 print(name, "CTAs used", int(used[:, 0].sum()), "iterations/CTA", int(used.sum(1).max()))
 for k in keys:
