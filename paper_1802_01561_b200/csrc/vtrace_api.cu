@@ -106,14 +106,16 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
     } else {
       const float L = 1.44269502f;  // fp32(log2 e); log2 e - L = 1.925963e-8
       const float y = d * L;
-      float y_lo = fmaf(d, L, -y);
+      const float e = ex2_approx(y);
+#ifndef VTRACE_NO_ARG_CORRECTION
+      float y_lo = fmaf(d, L, -y);  // exact residual of the rounded product d L
       if constexpr (!EXACT_DIFF) {
         const float bb = d - z;  // TwoSum residual of the fp32 difference z - m
         const float d_lo = (z - (d - bb)) + (-m - bb);
         y_lo = fmaf(d_lo, L, y_lo);
       }
-      const float e = ex2_approx(y);
       res = fmaf(e, y_lo, res);
+#endif
       sd = fmaf(e, d, sd);
       const float s = s_hi + e;
       s_lo += (s_hi - s) + e;
@@ -603,6 +605,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           const float za = Elem<LT>::get(zrow, a);
           const float L2E = 1.44269504088896341f;
           const float lseL = lse * L2E;
+          const float alpha = fmaf(-ce, cshift, pgr);  // pg + c_e (z_j - cshift) = alpha + c_e z_j
           float sq = 0.f;
           // dz_j = pi_j (pg + c_e (log pi_j + H))   (j != a)
           if constexpr (RowRegs<LT, A_CT>::kPacked) {
@@ -610,8 +613,8 @@ __global__ void __launch_bounds__(NTHREADS, 4)
 #pragma unroll
             for (int k = 0; k < A_CT / 2; ++k) {
               const float z0 = zp.get(2 * k), z1 = zp.get(2 * k + 1);
-              const float d0 = ex2_approx(fmaf(z0, L2E, -lseL)) * fmaf(ce, z0 - cshift, pgr);
-              const float d1 = ex2_approx(fmaf(z1, L2E, -lseL)) * fmaf(ce, z1 - cshift, pgr);
+              const float d0 = ex2_approx(fmaf(z0, L2E, -lseL)) * fmaf(ce, z0, alpha);
+              const float d1 = ex2_approx(fmaf(z1, L2E, -lseL)) * fmaf(ce, z1, alpha);
               sq = fmaf(d0, d0, sq);
               sq = fmaf(d1, d1, sq);
               __nv_bfloat162 h2 = __floats2bfloat162_rn(d0, d1);
@@ -621,20 +624,20 @@ __global__ void __launch_bounds__(NTHREADS, 4)
 #pragma unroll
             for (int j = 0; j < A_CT; ++j) {
               const float z = zp.get(j);
-              const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z - cshift, pgr);
+              const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z, alpha);
               sq = fmaf(d, d, sq);
               zrow[j] = store_cvt<LT>(d);
             }
           } else {
             for (int j = 0; j < A; ++j) {
               const float z = zp.get(j);
-              const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z - cshift, pgr);
+              const float d = ex2_approx(fmaf(z, L2E, -lseL)) * fmaf(ce, z, alpha);
               sq = fmaf(d, d, sq);
               zrow[j] = store_cvt<LT>(d);
             }
           }
           // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
-          const float d_wrong = ex2_approx(fmaf(za, L2E, -lseL)) * fmaf(ce, za - cshift, pgr);
+          const float d_wrong = ex2_approx(fmaf(za, L2E, -lseL)) * fmaf(ce, za, alpha);
           const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
           zrow[a] = store_cvt<LT>(d_a);
           sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
@@ -703,9 +706,19 @@ __global__ void __launch_bounds__(NTHREADS, 4)
     __threadfence();
     if (LOSS && P.partials) {
       for (int k = warp; k < NPART; k += NWARPS) {  // warp w: partials w, w + NWARPS
-        double x = 0.0;  // lanes stride the CTAs, then lane order: a fixed tree
-        for (int v = lane; v < (int)gridDim.x; v += 32)
-          x += __ldcg(P.cta_partials + (size_t)v * NPART + k);
+        // lanes stride the CTAs (8 independent loads in flight per lane), then the
+        // 32 lane sums are added in lane order: a fixed tree, bitwise reproducible
+        double x = 0.0;
+        for (int v0 = 0; v0 < (int)gridDim.x; v0 += 32 * 8) {
+          double buf[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int v = v0 + q * 32 + lane;
+            buf[q] = v < (int)gridDim.x ? __ldcg(P.cta_partials + (size_t)v * NPART + k) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x += buf[q];
+        }
         double tot = 0.0;
         for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, x, l);
         if (lane == 0) s_fin[k] = tot;
