@@ -27,8 +27,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
         extra = ["-DVTRACE_TIMING"] if os.environ.get("VTRACE_TIMING") else []
-        if os.environ.get("VTRACE_NO_ARG_CORRECTION"):  # precision experiment only
-            extra.append("-DVTRACE_NO_ARG_CORRECTION")
+        if os.environ.get("VTRACE_ARG_CORRECTION"):  # precision experiment only
+            extra.append("-DVTRACE_ARG_CORRECTION")
         cmd = [NVCC, *FLAGS, *extra, "-o", SO + ".tmp", *SOURCES]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

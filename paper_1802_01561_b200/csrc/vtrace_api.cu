@@ -107,7 +107,7 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
       const float L = 1.44269502f;  // fp32(log2 e); log2 e - L = 1.925963e-8
       const float y = d * L;
       const float e = ex2_approx(y);
-#ifndef VTRACE_NO_ARG_CORRECTION
+#ifdef VTRACE_ARG_CORRECTION
       float y_lo = fmaf(d, L, -y);  // exact residual of the rounded product d L
       if constexpr (!EXACT_DIFF) {
         const float bb = d - z;  // TwoSum residual of the fp32 difference z - m
@@ -136,12 +136,14 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
     S = S64;
     finite = (chk == 0.f) && (m == m);
   } else {
-    // sum_j e_j (1 + ln2 (y_lo_j + d_j * (log2e - L)))
+    // sum_j e_j (1 + ln2 (y_lo_j + d_j (log2e - L))): the fp32(log2 e) error is a
+    // systematic first-order term; the product rounding y_lo is random, within
+    // MUFU's own error, and only corrected with -DVTRACE_ARG_CORRECTION
     const float corr = fmaf(sd, 1.925963e-08f * 0.693147182f, res * 0.693147182f);
     S = (double)(s_hi - 1.f) + (double)(s_lo + corr);
-    // any inf/nan logit turns S into NaN: +inf -> m = inf -> d = nan; nan -> d = nan;
-    // -inf -> y_lo = fma(-inf, L, +inf) = nan
-    finite = isfinite(S) && isfinite(m);
+    // any inf/nan logit makes S or sd NaN: +inf -> m = inf -> d = nan; nan -> d = nan;
+    // -inf -> e = 0, sd += 0 * (-inf) = nan
+    finite = isfinite(S) && isfinite(sd) && isfinite(m);
   }
 }
 
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
 
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
+  const float rho_bar_f = (float)P.rho_bar;
   // per-thread partial sums (fixed assignment of rows to threads: deterministic)
   float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
         acc_clip = 0.f;
@@ -401,7 +404,6 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           const float* r_t = reinterpret_cast<const float*>(sb + L.r);
           const float* g_t = reinterpret_cast<const float*>(sb + L.g);
           const float* v_t = reinterpret_cast<const float*>(sb + L.v);
-          const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
           const int a_raw = a_t[r];
           const int a = min(max(a_raw, 0), A - 1);
           float m_p, m_m, sed_p, sed_m, ea_p, ea_m;
@@ -421,31 +423,40 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           const double ratio = exp64(xa_p - xa_m) * (S_m / S_p);
           // TD error r_t + gamma_t V(x_{t+1}) - V(x_t), V(x_T) = bootstrap
           const float rt = r_t[r], gm = g_t[r], Vt = v_t[r];
-          float Vn;
-          if (tl + 1 < U.tlen || !U.last_chunk) {
-            Vn = v_t[r + BC];  // the V tile has Tc + 1 rows
-          } else {
-            Vn = reinterpret_cast<const float*>(sb + L.boot)[bl];
-            if (!isfinite(Vn)) record_bad(P.ws, T * B + U.b0 + bl, VT_DATA_VALUE);
-          }
-          const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
-          const float Sf = (float)S_p, inv_S = __frcp_rn(Sf);
+          const float Vn = (tl + 1 < U.tlen || !U.last_chunk)
+                               ? v_t[r + BC]  // the V tile has Tc + 1 rows
+                               : reinterpret_cast<const float*>(sb + L.boot)[bl];
+          const double td =
+              reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
+          const float Sf = (float)S_p;
+          const float inv_S = rcp_approx(Sf);
           reinterpret_cast<double*>(smem + L.ratio[par])[r] = ratio;
           reinterpret_cast<double*>(smem + L.td[par])[r] = td;
           const float lse = m_p + __logf(Sf);  // log sum_j exp(z_j)
           reinterpret_cast<float*>(smem + L.lse[par])[r] = lse;
-          reinterpret_cast<float*>(smem + L.csh[par])[r] = m_p + sed_p * inv_S;  // lse - H
+          reinterpret_cast<float*>(smem + L.csh[par])[r] = fmaf(sed_p, inv_S, m_p);  // lse - H
           reinterpret_cast<float*>(smem + L.rest[par])[r] = (float)(S_p - (double)ea_p) * inv_S;
-          acc_rho += (float)fmin(P.rho_bar, ratio);
+          acc_rho += fminf(rho_bar_f, (float)ratio);
           acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
-          if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
-          if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
-          if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
-          if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
-          if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
-          if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
-          if (!isfinite(Vt)) record_bad(P.ws, row, VT_DATA_VALUE);
-          if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
+          if constexpr (!LOSS) {
+            const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
+            if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
+            if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
+            if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
+          }
+          // data checks (the host cannot see the data), one branch when clean
+          const bool bad = (a_raw != a) || !(fin_p && fin_m) || !isfinite(rt) ||
+                           !isfinite(Vt) || !isfinite(Vn) || !(gm >= 0.f && gm <= 1.f);
+          if (bad) {
+            const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
+            if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
+            if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
+            if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
+            if (!isfinite(Vt)) record_bad(P.ws, row, VT_DATA_VALUE);
+            if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
+            if (!isfinite(Vn) && U.last_chunk && tl + 1 == U.tlen)
+              record_bad(P.ws, T * B + U.b0 + bl, VT_DATA_VALUE);  // the bootstrap
+          }
         }
       }
       if (tid == 0) {
