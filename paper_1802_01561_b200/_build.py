@@ -10,6 +10,7 @@ ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libvtrace.so")
 SOURCES = [os.path.join(HERE, "csrc", "vtrace_api.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", "vtrace_kernels.cuh"),
+                  os.path.join(HERE, "csrc", "vtrace_ct.cuh"),
                   os.path.join(ROOT, "include", "vtrace.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

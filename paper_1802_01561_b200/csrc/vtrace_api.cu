@@ -85,7 +85,7 @@ template <typename LT, int A_CT, int MODE>
 __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int a, float& m,
                                           double& S, double& xa, float& ea_f, float& sed,
                                           bool& finite) {
-  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m is exact in fp32 for bf16 inputs
+  [[maybe_unused]] constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m exact in fp32 (bf16)
   constexpr int NA = A_CT > 0 ? A_CT : 1;
   const int nA = A_CT > 0 ? A_CT : A;
   m = R.get(0);
@@ -758,6 +758,10 @@ __global__ void __launch_bounds__(NTHREADS, 4)
   }
 }
 
+#include "vtrace_ct.cuh"
+
+#include "vtrace_ct.cuh"
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -796,14 +800,19 @@ static Plan make_plan(long long T, long long B, int A, int elem) {
 }
 
 struct WsLayout {
-  size_t recs, cta, total;
+  size_t recs, cta, ct_task, ct_group, ct_count, total;
 };
 
 static WsLayout ws_layout(const Plan& p) {
   WsLayout w;
   w.recs = 256;
   w.cta = a128(w.recs + (size_t)p.units * BC * RECS_PER_COL * sizeof(TagRec));
-  w.total = w.cta + (size_t)kMaxCtas * NPART * sizeof(double);
+  w.ct_task = a128(w.cta + (size_t)kMaxCtas * NPART * sizeof(double));
+  const size_t tasks = (size_t)(p.G * BC + CT_COLS - 1) / CT_COLS;  // >= ceil(B / 4)
+  const size_t groups = (tasks + CT_GROUP - 1) / CT_GROUP;
+  w.ct_group = a128(w.ct_task + tasks * NPART * sizeof(double));
+  w.ct_count = a128(w.ct_group + groups * NPART * sizeof(double));
+  w.total = a128(w.ct_count + (groups + 1) * sizeof(unsigned int));
   return w;
 }
 
@@ -950,6 +959,47 @@ static vt_status dispatch(const Params& P, const TmaMaps& maps, const Plan& plan
 
 static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
+// ---- column-task kernel launch -------------------------------------------------------
+constexpr long long kCtMinTasks = 1024;  // >= ~7 warps per SM
+
+static bool ct_enabled() {  // VTRACE_KERNEL=lookback forces the look-back kernel (tests)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VTRACE_KERNEL");
+    v = (e && e[0] == 'l') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename LT, int A_CT, bool LOSS, int MODE>
+static vt_status ct_launch_one(const Params& P, const CtParams& C, const TmaMaps& maps,
+                               cudaStream_t st) {
+  auto kern = vtrace_ct_kernel<LT, A_CT, LOSS, MODE>;
+  const size_t smem = (size_t)CT_WARPS * C.warp_bytes;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  });
+  if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
+  const unsigned grid = (unsigned)((C.tasks + CT_WARPS - 1) / CT_WARPS);
+  kern<<<grid, CT_WARPS * 32, smem, st>>>(P, C, maps);
+  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+}
+
+template <typename LT, bool LOSS>
+static vt_status ct_dispatch(const Params& P, const CtParams& C, const TmaMaps& maps,
+                             cudaStream_t st) {
+  if (exp_mode() == EXP_MUFU) {
+    if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_MUFU>(P, C, maps, st);
+    if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_MUFU>(P, C, maps, st);
+    return ct_launch_one<LT, 0, LOSS, EXP_MUFU>(P, C, maps, st);
+  }
+  if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_F64>(P, C, maps, st);
+  if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_F64>(P, C, maps, st);
+  return ct_launch_one<LT, 0, LOSS, EXP_F64>(P, C, maps, st);
+}
+
 static vt_status check_params(const vt_vtrace_params* p) {
   if (!p) return VT_ERR_INVALID_ARG;
   const float rb = p->clip_rho_threshold, cb = p->clip_c_threshold,
@@ -1051,6 +1101,46 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
           (!loss || encode_2d(&maps.dz, dlogits, ldt, elem, B * A, T, BC * (int)A, plan.Tc));
   }
   if (plan.smem > kMaxSmem) return VT_ERR_SHAPE;
+
+  // column-task kernel: wide batches (enough 4-trajectory tasks to fill the GPU)
+  const long long tasks = (B + CT_COLS - 1) / CT_COLS;
+  const bool ct = tma && ct_enabled() && tasks >= kCtMinTasks && (A * elem) % 4 == 0 &&
+                  CT_COLS * A <= 256 && (B % CT_COLS) == 0;
+  if (ct) {
+    const CUtensorMapDataType ldt =
+        dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    TmaMaps cm;
+    std::memset(&cm, 0, sizeof(cm));
+    const bool ok =
+        encode_2d(&cm.mu, mu, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
+        encode_2d(&cm.pi, pi, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
+        encode_2d(&cm.a, actions, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, B, T, CT_COLS, CT_STEPS) &&
+        encode_2d(&cm.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, CT_COLS, CT_STEPS) &&
+        encode_2d(&cm.g, disc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, CT_COLS, CT_STEPS) &&
+        encode_2d(&cm.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, CT_COLS, CT_STEPS + 1) &&
+        encode_1d(&cm.boot, boot, B, CT_COLS) &&
+        (!loss || encode_2d(&cm.dz, dlogits, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS));
+    if (ok) {
+      const CtLayout cl = make_ct_layout((int)A, elem);
+      CtParams C;
+      std::memset(&C, 0, sizeof(C));
+      C.pi = (unsigned)cl.pi; C.mu = (unsigned)cl.mu; C.a = (unsigned)cl.a; C.r = (unsigned)cl.r;
+      C.g = (unsigned)cl.g; C.v = (unsigned)cl.v; C.stage = (unsigned)cl.stage;
+      C.boot = (unsigned)cl.boot; C.warp_bytes = (unsigned)cl.warp_bytes;
+      C.tasks = (int)tasks;
+      C.groups = (int)((tasks + CT_GROUP - 1) / CT_GROUP);
+      C.K = (int)((T + CT_STEPS - 1) / CT_STEPS);
+      const WsLayout wl2 = ws_layout(plan);
+      C.task_partials = reinterpret_cast<double*>(wsb + wl2.ct_task);
+      C.group_partials = reinterpret_cast<double*>(wsb + wl2.ct_group);
+      C.group_count = reinterpret_cast<unsigned int*>(wsb + wl2.ct_count);
+      C.top_count = C.group_count + C.groups;
+      if (dt == VT_BFLOAT16)
+        return loss ? ct_dispatch<__nv_bfloat16, true>(P, C, cm, st)
+                    : ct_dispatch<__nv_bfloat16, false>(P, C, cm, st);
+      return loss ? ct_dispatch<float, true>(P, C, cm, st) : ct_dispatch<float, false>(P, C, cm, st);
+    }
+  }
   if (dt == VT_BFLOAT16) {
     return loss ? dispatch<__nv_bfloat16, true>(P, maps, plan, tma, st)
                 : dispatch<__nv_bfloat16, false>(P, maps, plan, tma, st);

@@ -276,3 +276,22 @@ def test_graph_capture_replay():
         torch.cuda.synchronize()
         for k in ref:
             assert torch.equal(out[k], ref[k]), k
+
+
+@pytest.mark.parametrize("T,B,A,dtype", [(100, 4096, 18, 1), (1, 4096, 18, 1), (7, 4104, 9, 0),
+                                          (129, 4096, 18, 0), (20, 4096, 6, 1), (33, 4096, 40, 0)])
+def test_parity_column_task_kernel(T, B, A, dtype):
+    """Wide batches take the column-task kernel (one warp per 4 trajectories)."""
+    inp = wl.make_inputs("large", seed=T + B + A, T=T, B=B, A=A, dtype=dtype)
+    lg, fl, ref_l, ref_f = run_both(inp)
+    check_all(inp, lg, fl, ref_l, ref_f)
+
+
+def test_column_task_shard_equals_slice_bitwise():
+    inp = wl.make_inputs("large", seed=31, B=8192, T=60)
+    full = pkg.loss_and_grad(*[_dev(inp)[k] for k in NAMES], reward_mode=1)
+    for b0, b1 in [(0, 4096), (4096, 8192)]:
+        sh = wl.column_slice(inp, b0, b1)
+        o = pkg.loss_and_grad(*[_dev(sh)[k] for k in NAMES], reward_mode=1)
+        for k in ("grad_target_logits", "grad_values", "vs", "pg_advantages"):
+            assert torch.equal(o[k], full[k][:, b0:b1]), (k, b0, b1)
