@@ -11,5 +11,5 @@ for cfg in large stress dmlab atari; do
 done
 CMD="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 300 $CMD > ${P}_plain.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:vtrace_fused -s 6 -c 1 -o ${P}_prof $CMD > ${P}_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:vtrace_ -s 6 -c 1 -o ${P}_prof $CMD > ${P}_ncu.log 2>&1
 echo "ncu rc=$?" >> ${P}_ncu.log
