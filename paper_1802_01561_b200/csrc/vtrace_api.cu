@@ -77,10 +77,7 @@ struct RowRegs {
 // Statistics of one logits row: m = max z, S = sum_j exp(z_j - m) (accurate to
 // ~1e-8 relative), xa = z_a - m (exact, fp64), ea_f = exp(z_a - m) (fp32; it is
 // exactly 1 when a is the argmax), and sed = sum_j e_j (z_j - m) (for the
-// entropy, fp32).  MUFU mode: ex2.approx on the fp32 argument, whose
-// rounding residual (and, for fp32 logits, that of z - m) enters as a
-// first-order correction sum_j e_j * ln2 * residual_j; the e_j are added with
-// Fast2Sum (s_hi starts at 1 >= every term, so each step is exact).
+// entropy, fp32).
 template <typename LT, int A_CT, int MODE>
 __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int a, float& m,
                                           double& S, double& xa, float& ea_f, float& sed,
@@ -93,33 +90,24 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   for (int j = 1; j < NA; ++j) m = fmaxf(m, R.get(j));
   if constexpr (A_CT == 0)
     for (int j = 1; j < nA; ++j) m = fmaxf(m, R.get(j));
-  float s_hi = 1.f, s_lo = 0.f, res = 0.f, sd = 0.f;
   double S64 = 0.0;
-  float chk = 0.f;
+  float sz = 0.f, chk = 0.f;
+  // MUFU mode: e_j = 2^{fma(z_j, L, -fl(m L))} (one rounding of the exponent),
+  // summed exactly in fp64 (fp32 -> fp64 conversion + DADD run on pipes the
+  // fp32-bound kernel leaves idle); the exact residual of fl(m L) is applied once.
+  const float L = 1.44269502f;  // fp32(log2 e); log2 e - L = 1.925963e-8
+  const float mL = m * L;
+  const float mL_err = fmaf(m, L, -mL);  // m L - fl(m L), exact
   auto term = [&](float z) {
-    const float d = z - m;
     if constexpr (MODE == EXP_F64) {
       const double e = exp64((double)z - (double)m);
       S64 += e;
-      sd = fmaf((float)e, d, sd);
+      sz = fmaf((float)e, z - m, sz);
       chk = __fmaf_rn(z, 0.f, chk);
     } else {
-      const float L = 1.44269502f;  // fp32(log2 e); log2 e - L = 1.925963e-8
-      const float y = d * L;
-      const float e = ex2_approx(y);
-#ifdef VTRACE_ARG_CORRECTION
-      float y_lo = fmaf(d, L, -y);  // exact residual of the rounded product d L
-      if constexpr (!EXACT_DIFF) {
-        const float bb = d - z;  // TwoSum residual of the fp32 difference z - m
-        const float d_lo = (z - (d - bb)) + (-m - bb);
-        y_lo = fmaf(d_lo, L, y_lo);
-      }
-      res = fmaf(e, y_lo, res);
-#endif
-      sd = fmaf(e, d, sd);
-      const float s = s_hi + e;
-      s_lo += (s_hi - s) + e;
-      s_hi = s;
+      const float e = ex2_approx(fmaf(z, L, -mL));
+      S64 += (double)e;
+      sz = fmaf(e, z, sz);  // sum_j e_j z_j (entropy; NaN if some z is inf/nan)
     }
   };
   if constexpr (A_CT > 0) {
@@ -131,19 +119,21 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   const float za = Elem<LT>::get(R.src, a);
   xa = (double)za - (double)m;  // z_a - m, exact
   ea_f = ex2_approx((za - m) * 1.44269504088896341f);  // exp(z_a - m), fp32 (exactly 1 at the max)
-  sed = sd;
   if constexpr (MODE == EXP_F64) {
     S = S64;
+    sed = sz;
     finite = (chk == 0.f) && (m == m);
   } else {
-    // sum_j e_j (1 + ln2 (y_lo_j + d_j (log2e - L))): the fp32(log2 e) error is a
-    // systematic first-order term; the product rounding y_lo is random, within
-    // MUFU's own error, and only corrected with -DVTRACE_ARG_CORRECTION
-    const float corr = fmaf(sd, 1.925963e-08f * 0.693147182f, res * 0.693147182f);
-    S = (double)(s_hi - 1.f) + (double)(s_lo + corr);
-    // any inf/nan logit makes S or sd NaN: +inf -> m = inf -> d = nan; nan -> d = nan;
-    // -inf -> e = 0, sd += 0 * (-inf) = nan
-    finite = isfinite(S) && isfinite(sd) && isfinite(m);
+    // sed = sum_j e_j (z_j - m); the computed e_j carry the common factor
+    // 2^{mL_err} and the per-term factor 2^{-(z_j - m)(log2 e - L)}: first order
+    const float Sf = (float)S64;
+    sed = fmaf(-m, Sf, sz);
+    const double corr = (double)fmaf(sed, 1.925963e-08f * 0.693147182f, 0.f) -
+                        (double)(mL_err * 0.693147182f) * S64;
+    S = S64 + corr;
+    // any inf/nan logit makes S or sed NaN: +inf -> m = inf -> exponent nan;
+    // nan -> exponent nan; -inf -> e = 0 and 0 * (-inf) = nan in sz
+    finite = isfinite(S) && isfinite(sed) && isfinite(m);
   }
 }
 

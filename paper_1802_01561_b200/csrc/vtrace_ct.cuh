@@ -103,12 +103,13 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
         acc_clip = 0.f;
   double carry = 0.0;  // A = v - V just after the current chunk, for column c (A_T = 0)
 
+  int st = 0;                 // it % CT_NSTAGE
+  uint32_t phase = 0;         // (it / CT_NSTAGE) & 1
   for (int it = 0; it < K; ++it) {
-    const int st = it % CT_NSTAGE;
     const int t0 = (K - 1 - it) * CT_STEPS;
     const int tlen = min(CT_STEPS, T - t0);
     unsigned char* sb = base + (size_t)st * C.stage;
-    mbar_wait(&wb[st], (uint32_t)((it / CT_NSTAGE) & 1));
+    mbar_wait(&wb[st], phase);
     const bool row_ok = (tl < tlen) && (c < blen);
     const int r = lane;
     LT* zrow = reinterpret_cast<LT*>(sb + C.pi) + (size_t)r * A;
@@ -263,6 +264,10 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       load_iter(it + 2);
     }
     __syncwarp();
+    if (++st == CT_NSTAGE) {
+      st = 0;
+      phase ^= 1u;
+    }
   }
   if constexpr (LOSS) {
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
