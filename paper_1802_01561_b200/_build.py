@@ -28,8 +28,9 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
         extra = ["-DVTRACE_TIMING"] if os.environ.get("VTRACE_TIMING") else []
-        if os.environ.get("VTRACE_ARG_CORRECTION"):  # precision experiment only
-            extra.append("-DVTRACE_ARG_CORRECTION")
+        for flag in ("VTRACE_SUM_F64",):  # A/B experiments only
+            if os.environ.get(flag):
+                extra.append("-D" + flag)
         cmd = [NVCC, *FLAGS, *extra, "-o", SO + ".tmp", *SOURCES]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -82,7 +82,7 @@ template <typename LT, int A_CT, int MODE>
 __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int a, float& m,
                                           double& S, double& xa, float& ea_f, float& sed,
                                           bool& finite) {
-  [[maybe_unused]] constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // z - m exact in fp32 (bf16)
+  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // bf16: 8-bit significands
   constexpr int NA = A_CT > 0 ? A_CT : 1;
   const int nA = A_CT > 0 ? A_CT : A;
   m = R.get(0);
@@ -90,50 +90,67 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   for (int j = 1; j < NA; ++j) m = fmaxf(m, R.get(j));
   if constexpr (A_CT == 0)
     for (int j = 1; j < nA; ++j) m = fmaxf(m, R.get(j));
-  double S64 = 0.0;
-  float sz = 0.f, chk = 0.f;
-  // MUFU mode: e_j = 2^{fma(z_j, L, -fl(m L))} (one rounding of the exponent),
-  // summed exactly in fp64 (fp32 -> fp64 conversion + DADD run on pipes the
-  // fp32-bound kernel leaves idle); the exact residual of fl(m L) is applied once.
-  const float L = 1.44269502f;  // fp32(log2 e); log2 e - L = 1.925963e-8
-  const float mL = m * L;
-  const float mL_err = fmaf(m, L, -mL);  // m L - fl(m L), exact
-  auto term = [&](float z) {
+  // MUFU mode: e_j = 2^{y_j} with one rounding of the exponent y_j = (z_j - m) L'.
+  //  bf16 logits: y_j = fma(z_j, L16, -m L16) with a 16-bit log2 e, so z L16 and
+  //    m L16 are exact and the max term is exactly 2^0 = 1;
+  //  fp32 logits: y_j = fl(z_j - m) * L32 (the max term again exactly 1).
+  // The truncation of log2 e is a first-order factor 2^{(z_j - m)(log2 e - L')},
+  // applied once per row through sed = sum_j e_j (z_j - m).  The e_j are summed
+  // exactly: Fast2Sum in fp32 (s_hi starts at 1 >= every term), or, with
+  // -DVTRACE_SUM_F64, fp32 -> fp64 conversions and two fp64 accumulators.
+  constexpr float L16 = 1.44268798828125f;          // log2 e to 16 bits
+  constexpr float L32 = 1.44269502f;                // fp32(log2 e)
+  constexpr float CORR16 = 4.8884952e-06f;          // ln2 (log2 e - L16)
+  constexpr float CORR32 = 1.3349930e-08f;          // ln2 (log2 e - L32)
+  const float mL = m * L16;                         // exact for bf16 m
+  double S64a = 0.0, S64b = 0.0;
+  float s_hi = 1.f, s_lo = 0.f, sd = 0.f, chk = 0.f;
+  auto term = [&](float z, int j) {
     if constexpr (MODE == EXP_F64) {
       const double e = exp64((double)z - (double)m);
-      S64 += e;
-      sz = fmaf((float)e, z - m, sz);
+      S64a += e;
+      sd = fmaf((float)e, z - m, sd);
       chk = __fmaf_rn(z, 0.f, chk);
     } else {
-      const float e = ex2_approx(fmaf(z, L, -mL));
-      S64 += (double)e;
-      sz = fmaf(e, z, sz);  // sum_j e_j z_j (entropy; NaN if some z is inf/nan)
+      float e, d;
+      if constexpr (EXACT_DIFF) {
+        e = ex2_approx(fmaf(z, L16, -mL));
+        d = z - m;
+      } else {
+        d = z - m;
+        e = ex2_approx(d * L32);
+      }
+      sd = fmaf(e, d, sd);  // NaN if some z is inf/nan (0 * inf for -inf)
+#ifdef VTRACE_SUM_F64
+      if (j & 1) S64b += (double)e; else S64a += (double)e;
+#else
+      const float sum = s_hi + e;
+      s_lo += (s_hi - sum) + e;
+      s_hi = sum;
+#endif
     }
   };
   if constexpr (A_CT > 0) {
 #pragma unroll
-    for (int j = 0; j < A_CT; ++j) term(R.get(j));
+    for (int j = 0; j < A_CT; ++j) term(R.get(j), j);
   } else {
-    for (int j = 0; j < nA; ++j) term(R.get(j));
+    for (int j = 0; j < nA; ++j) term(R.get(j), j);
   }
   const float za = Elem<LT>::get(R.src, a);
   xa = (double)za - (double)m;  // z_a - m, exact
   ea_f = ex2_approx((za - m) * 1.44269504088896341f);  // exp(z_a - m), fp32 (exactly 1 at the max)
+  sed = sd;
   if constexpr (MODE == EXP_F64) {
-    S = S64;
-    sed = sz;
+    S = S64a;
     finite = (chk == 0.f) && (m == m);
   } else {
-    // sed = sum_j e_j (z_j - m); the computed e_j carry the common factor
-    // 2^{mL_err} and the per-term factor 2^{-(z_j - m)(log2 e - L)}: first order
-    const float Sf = (float)S64;
-    sed = fmaf(-m, Sf, sz);
-    const double corr = (double)fmaf(sed, 1.925963e-08f * 0.693147182f, 0.f) -
-                        (double)(mL_err * 0.693147182f) * S64;
-    S = S64 + corr;
-    // any inf/nan logit makes S or sed NaN: +inf -> m = inf -> exponent nan;
-    // nan -> exponent nan; -inf -> e = 0 and 0 * (-inf) = nan in sz
-    finite = isfinite(S) && isfinite(sed) && isfinite(m);
+#ifdef VTRACE_SUM_F64
+    const double S0 = S64a + S64b;
+#else
+    const double S0 = (double)(s_hi - 1.f) + (double)s_lo;
+#endif
+    S = S0 + (double)(sd * (EXACT_DIFF ? CORR16 : CORR32));
+    finite = isfinite(S) && isfinite(sd) && isfinite(m);
   }
 }
 
