@@ -103,7 +103,8 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   constexpr float CORR16 = 4.8884952e-06f;          // ln2 (log2 e - L16)
   constexpr float CORR32 = 1.3349930e-08f;          // ln2 (log2 e - L32)
   const float mL = m * L16;                         // exact for bf16 m
-  double S64a = 0.0, S64b = 0.0;
+  double S64a = 0.0;
+  [[maybe_unused]] double S64b = 0.0;
   float s_hi = 1.f, s_lo = 0.f, sd = 0.f, chk = 0.f;
   auto term = [&](float z, int j) {
     if constexpr (MODE == EXP_F64) {
@@ -504,8 +505,8 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         if (col_ok && s_beg + k < s_end) {
           const int q = (s_beg + k) * BC + c;
           const double ratio = ratio_s[q];
-          const double dl = fmin(P.rho_bar, ratio) * td_s[q];
-          const double gc = (double)g_t[q] * (P.lambda * fmin(P.c_bar, ratio));
+          const double dl = dmin_t(P.rho_bar, ratio) * td_s[q];
+          const double gc = (double)g_t[q] * (P.lambda * dmin_t(P.c_bar, ratio));
           adv_s[q] = dl;
           D = fma(gc, D, dl);
           G = gc * G;
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
       for (int k = KSEG - 1; k >= 0; --k) {
         if (col_ok && s_beg + k < s_end) {
           const int q = (s_beg + k) * BC + c;
-          const double gc = (double)g_t[q] * (P.lambda * fmin(P.c_bar, ratio_s[q]));
+          const double gc = (double)g_t[q] * (P.lambda * dmin_t(P.c_bar, ratio_s[q]));
           A_next = fma(gc, A_next, adv_s[q]);
           adv_s[q] = A_next;
         }
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         // v_t = V(x_t) + A_t;  pg_adv_t = rho_pg (r_t + gamma_t v_{t+1} - V(x_t))
         //                              = rho_pg (td_t + gamma_t A_{t+1})
         const float vsr = (float)((double)Vt + A_t);
-        const float pgr = (float)(fmin(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
+        const float pgr = (float)(dmin_t(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
         if (P.vs) P.vs[row] = vsr;
         if (P.pg_adv) P.pg_adv[row] = pgr;
         if constexpr (LOSS) {

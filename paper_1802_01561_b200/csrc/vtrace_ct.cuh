@@ -115,11 +115,13 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
     LT* zrow = reinterpret_cast<LT*>(sb + C.pi) + (size_t)r * A;
 
     // ---- a3-a7: statistics of this lane's row ----------------------------------
+    // Every lane computes its row; rows past the end of the unroll (the last
+    // chunk only; TMA zero-filled) are masked out of the scan and the outputs.
     RowRegs<LT, A_CT> zp;
-    float lse = 0.f, cshift = 0.f, rest = 0.f, Vt = 0.f, gm = 0.f;
-    double ratio = 1.0, td = 0.0, dl = 0.0, gc = 1.0;
-    int a = 0;
-    if (row_ok) {
+    float lse, cshift, rest, Vt, gm;
+    double ratio, td, dl, gc;
+    int a;
+    {
       const int a_raw = reinterpret_cast<const int*>(sb + C.a)[r];
       a = min(max(a_raw, 0), A - 1);
       float m_p, m_m, sed_p, sed_m, ea_p, ea_m;
@@ -143,23 +145,29 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
                            ? reinterpret_cast<const float*>(sb + C.v)[r + CT_COLS]
                            : reinterpret_cast<const float*>(base + C.boot)[c];
       td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
-      dl = fmin(P.rho_bar, ratio) * td;                         // delta_t V
-      gc = (double)gm * (P.lambda * fmin(P.c_bar, ratio));      // gamma_t c_t
+      dl = dmin_t(P.rho_bar, ratio) * td;                         // delta_t V
+      gc = (double)gm * (P.lambda * dmin_t(P.c_bar, ratio));      // gamma_t c_t
       const float Sf = (float)S_p;
       const float inv_S = rcp_approx(Sf);
       lse = m_p + __logf(Sf);
       cshift = fmaf(sed_p, inv_S, m_p);  // lse - H
       rest = (float)(S_p - (double)ea_p) * inv_S;
-      acc_rho += fminf(rho_bar_f, (float)ratio);
-      acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
+      if (row_ok) {
+        acc_rho += fminf(rho_bar_f, (float)ratio);
+        acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
+      }
       const long long row = (long long)(t0 + tl) * B + b0 + c;
-      if constexpr (!LOSS) {
+      if (!LOSS && row_ok) {
         if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
         if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
         if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
       }
-      const bool bad = (a_raw != a) || !(fin_p && fin_m) || !isfinite(rt) || !isfinite(Vt) ||
-                       !isfinite(Vn) || !(gm >= 0.f && gm <= 1.f);
+      const bool bad = row_ok && ((a_raw != a) || !(fin_p && fin_m) || !isfinite(rt) ||
+                                  !isfinite(Vt) || !isfinite(Vn) || !(gm >= 0.f && gm <= 1.f));
+      if (!row_ok) {
+        dl = 0.0;  // identity map for steps past the end of the unroll
+        gc = 1.0;
+      }
       if (bad) {
         if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
         if (!(fin_p && fin_m)) record_bad(P.ws, row, VT_DATA_LOGITS);
@@ -178,10 +186,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
 #pragma unroll
     for (int o = CT_COLS; o < 32; o <<= 1) {
       const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
-      if (lane + o < 32) {
-        Di = fma(Gi, Do, Di);
-        Gi = Gi * Go;
-      }
+      const bool in = lane + o < 32;  // beyond the chunk: identity map
+      Di = fma(Gi, in ? Do : 0.0, Di);
+      Gi = Gi * (in ? Go : 1.0);
     }
     const double A_t = fma(Gi, carry, Di);                 // A_t = v_t - V(x_t)
     double A_n = shfl_down_d(A_t, CT_COLS);                // A_{t+1}
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
     if (row_ok) {
       const long long row = (long long)(t0 + tl) * B + b0 + c;
       // pg_adv = rho_pg (r + gamma v_{t+1} - V) = rho_pg (td + gamma A_{t+1})
-      const float pgr = (float)(fmin(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
+      const float pgr = (float)(dmin_t(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
       if (P.vs) P.vs[row] = (float)((double)Vt + A_t);
       if (P.pg_adv) P.pg_adv[row] = pgr;
       if constexpr (LOSS) {

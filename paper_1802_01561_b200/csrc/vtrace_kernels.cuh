@@ -220,9 +220,12 @@ template <>
 struct Elem<__nv_bfloat16> {
   static constexpr int bytes = 2;
   static __device__ __forceinline__ float get(const __nv_bfloat16* p, int i) {
-    return __bfloat162float(p[i]);
+    return __uint_as_float((uint32_t)reinterpret_cast<const unsigned short*>(p)[i] << 16);
   }
 };
+
+// min(bound, x) for a threshold that is never NaN (compare + select, no NaN fixups)
+__device__ __forceinline__ double dmin_t(double bound, double x) { return x < bound ? x : bound; }
 
 // Loads a row of A_CT logits from shared memory into registers (exact upcast).
 template <typename LT, int A_CT>
@@ -259,7 +262,7 @@ __device__ __forceinline__ double exp64(double x) {
   const double LN2_HI = 6.93147180369123816490e-01;
   const double LN2_LO = 1.90821492927058770002e-10;
   const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer shifter
-  x = fmin(fmax(x, -700.0), 700.0);
+  x = (x < -700.0) ? -700.0 : ((x > 700.0) ? 700.0 : x);  // (NaN passes through)
   double t = fma(x, LOG2E, MAGIC);
   double n = t - MAGIC;
   int ni = __double2loint(t);
