@@ -155,6 +155,67 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   }
 }
 
+// Both policies' statistics of one row in one interleaved loop (MUFU mode, compile-
+// time A): four independent compensated-sum chains (2 per policy, even/odd j)
+// instead of two long serial ones, for instruction-level parallelism.
+struct RowStat {
+  float m, sed, ea_f;
+  double S, xa;
+  bool finite;
+};
+
+template <typename LT, int A_CT>
+__device__ __forceinline__ void row_stats2(const RowRegs<LT, A_CT>& Rp, const RowRegs<LT, A_CT>& Rm,
+                                           int a, RowStat& sp, RowStat& sm) {
+  static_assert(A_CT > 0, "compile-time A only");
+  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);
+  constexpr float L16 = 1.44268798828125f;
+  constexpr float L32 = 1.44269502f;
+  constexpr float CORR = EXACT_DIFF ? 4.8884952e-06f : 1.3349930e-08f;
+  float mp = Rp.get(0), mm = Rm.get(0);
+#pragma unroll
+  for (int j = 1; j < A_CT; ++j) {
+    mp = fmaxf(mp, Rp.get(j));
+    mm = fmaxf(mm, Rm.get(j));
+  }
+  const float mLp = mp * L16, mLm = mm * L16;
+  float hp[2] = {1.f, 1.f}, lp[2] = {0.f, 0.f}, hm[2] = {1.f, 1.f}, lm[2] = {0.f, 0.f};
+  float sdp = 0.f, sdm = 0.f;
+#pragma unroll
+  for (int j = 0; j < A_CT; ++j) {
+    const int q = j & 1;
+    const float zp = Rp.get(j), zm = Rm.get(j);
+    const float dp = zp - mp, dm = zm - mm;
+    float ep, em;
+    if constexpr (EXACT_DIFF) {
+      ep = ex2_approx(fmaf(zp, L16, -mLp));
+      em = ex2_approx(fmaf(zm, L16, -mLm));
+    } else {
+      ep = ex2_approx(dp * L32);
+      em = ex2_approx(dm * L32);
+    }
+    sdp = fmaf(ep, dp, sdp);
+    sdm = fmaf(em, dm, sdm);
+    const float np = hp[q] + ep, nm = hm[q] + em;  // Fast2Sum: h >= 1 >= e
+    lp[q] += (hp[q] - np) + ep;
+    lm[q] += (hm[q] - nm) + em;
+    hp[q] = np;
+    hm[q] = nm;
+  }
+  // each chain started at 1: h - 1 is exact
+  const double Sp = ((double)(hp[0] - 1.f) + (double)(hp[1] - 1.f)) +
+                    ((double)lp[0] + (double)lp[1]) + (double)(sdp * CORR);
+  const double Sm = ((double)(hm[0] - 1.f) + (double)(hm[1] - 1.f)) +
+                    ((double)lm[0] + (double)lm[1]) + (double)(sdm * CORR);
+  const float zap = Elem<LT>::get(Rp.src, a), zam = Elem<LT>::get(Rm.src, a);
+  sp.m = mp; sp.sed = sdp; sp.S = Sp; sp.xa = (double)zap - (double)mp;
+  sp.ea_f = ex2_approx((zap - mp) * 1.44269504088896341f);
+  sp.finite = isfinite(Sp) && isfinite(sdp) && isfinite(mp);
+  sm.m = mm; sm.sed = sdm; sm.S = Sm; sm.xa = (double)zam - (double)mm;
+  sm.ea_f = 1.f;
+  sm.finite = isfinite(Sm) && isfinite(sdm) && isfinite(mm);
+}
+
 __device__ __forceinline__ double reward_transform(float r, int mode) {
   if (mode == 1) return (double)fminf(1.f, fmaxf(-1.f, r));  // P:944 (exact in fp32)
   double x = (double)r;

@@ -128,8 +128,15 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       double S_p, S_m, xa_p, xa_m;
       bool fin_p, fin_m;
       zp.load(zrow);
-      row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, xa_p, ea_p, sed_p, fin_p);
-      {
+      if constexpr (A_CT > 0 && MODE == EXP_MUFU) {
+        RowRegs<LT, A_CT> zm;
+        zm.load(reinterpret_cast<const LT*>(sb + C.mu) + (size_t)r * A);
+        RowStat sp, sm;
+        row_stats2<LT, A_CT>(zp, zm, a, sp, sm);
+        m_p = sp.m; S_p = sp.S; xa_p = sp.xa; ea_p = sp.ea_f; sed_p = sp.sed; fin_p = sp.finite;
+        m_m = sm.m; S_m = sm.S; xa_m = sm.xa; ea_m = sm.ea_f; sed_m = sm.sed; fin_m = sm.finite;
+      } else {
+        row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, xa_p, ea_p, sed_p, fin_p);
         RowRegs<LT, A_CT> zm;
         zm.load(reinterpret_cast<const LT*>(sb + C.mu) + (size_t)r * A);
         row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, xa_m, ea_m, sed_m, fin_m);
