@@ -185,17 +185,19 @@ __device__ __forceinline__ void row_stats2(const RowRegs<LT, A_CT>& Rp, const Ro
   for (int j = 0; j < A_CT; ++j) {
     const int q = j & 1;
     const float zp = Rp.get(j), zm = Rm.get(j);
-    const float dp = zp - mp, dm = zm - mm;
     float ep, em;
     if constexpr (EXACT_DIFF) {
       ep = ex2_approx(fmaf(zp, L16, -mLp));
       em = ex2_approx(fmaf(zm, L16, -mLm));
+      sdp = fmaf(ep, zp, sdp);  // sum e z; (z - m) applied once per row below
+      sdm = fmaf(em, zm, sdm);
     } else {
+      const float dp = zp - mp, dm = zm - mm;
       ep = ex2_approx(dp * L32);
       em = ex2_approx(dm * L32);
+      sdp = fmaf(ep, dp, sdp);
+      sdm = fmaf(em, dm, sdm);
     }
-    sdp = fmaf(ep, dp, sdp);
-    sdm = fmaf(em, dm, sdm);
     const float np = hp[q] + ep, nm = hm[q] + em;  // Fast2Sum: h >= 1 >= e
     lp[q] += (hp[q] - np) + ep;
     lm[q] += (hm[q] - nm) + em;
@@ -203,6 +205,11 @@ __device__ __forceinline__ void row_stats2(const RowRegs<LT, A_CT>& Rp, const Ro
     hm[q] = nm;
   }
   // each chain started at 1: h - 1 is exact
+  const float Sp_hi = (hp[0] - 1.f) + (hp[1] - 1.f), Sm_hi = (hm[0] - 1.f) + (hm[1] - 1.f);
+  if constexpr (EXACT_DIFF) {  // sum e (z - m) = sum e z - m sum e (entropy/correction only)
+    sdp = fmaf(-mp, Sp_hi, sdp);
+    sdm = fmaf(-mm, Sm_hi, sdm);
+  }
   const double Sp = ((double)(hp[0] - 1.f) + (double)(hp[1] - 1.f)) +
                     ((double)lp[0] + (double)lp[1]) + (double)(sdp * CORR);
   const double Sm = ((double)(hm[0] - 1.f) + (double)(hm[1] - 1.f)) +

@@ -14,14 +14,17 @@
 //          (3 shuffle levels), A_t = D_t + G_t * carry          (Remark 1)
 //   a9     q_t / pg_adv_t from A_{t+1}
 //   a10-11 dL/dz written in place over the z^pi tile, one TMA store per chunk
-// TMA: 3-stage ring per warp (2 chunks in flight while one is computed).
+// TMA: CT_NSTAGE-stage ring per warp (CT_NSTAGE-1 chunks in flight while one is computed).
 #pragma once
 // (included inside namespace vtb200 by vtrace_api.cu)
 
 constexpr int CT_COLS = 4;
 constexpr int CT_STEPS = 8;
 constexpr int CT_ROWS = CT_COLS * CT_STEPS;  // 32 == warp size
-constexpr int CT_NSTAGE = 3;
+#ifndef VTRACE_CT_NSTAGE
+#define VTRACE_CT_NSTAGE 5
+#endif
+constexpr int CT_NSTAGE = VTRACE_CT_NSTAGE;  // chunks in flight + the one computed
 constexpr int CT_WARPS = 1;                  // warps (tasks) per CTA
 constexpr int CT_GROUP = 32;                 // tasks per partials group
 static_assert(CT_ROWS == 32, "one row per lane");
@@ -271,11 +274,11 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       __syncwarp();
     }
     if (lane == 0 && it >= 1) {
-      // stage (it-1)%3 == (it+2)%3: its gradient store must have read it (allow this
-      // iteration's store to stay in flight), then refill it with iteration it+2
+      // the stage of iteration it-1 (== that of it + NSTAGE - 1): its gradient store
+      // must have read it (this iteration's store may stay in flight); then refill
       if constexpr (LOSS) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       fence_proxy_async_smem();
-      load_iter(it + 2);
+      load_iter(it + CT_NSTAGE - 1);
     }
     __syncwarp();
     if (++st == CT_NSTAGE) {
