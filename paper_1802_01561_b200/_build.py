@@ -31,8 +31,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for flag in ("VTRACE_SUM_F64",):  # A/B experiments only
             if os.environ.get(flag):
                 extra.append("-D" + flag)
-        if os.environ.get("VTRACE_CT_NSTAGE"):
-            extra.append("-DVTRACE_CT_NSTAGE=" + os.environ["VTRACE_CT_NSTAGE"])
         cmd = [NVCC, *FLAGS, *extra, "-o", SO + ".tmp", *SOURCES]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

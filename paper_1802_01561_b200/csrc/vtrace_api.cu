@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/vtrace.h"
 #include "vtrace_kernels.cuh"
@@ -836,8 +837,6 @@ __global__ void __launch_bounds__(NTHREADS, 4)
 
 #include "vtrace_ct.cuh"
 
-#include "vtrace_ct.cuh"
-
 // ---------------------------------------------------------------------------
 // host side
 
@@ -1056,6 +1055,10 @@ static vt_status ct_launch_one(const Params& P, const CtParams& C, const TmaMaps
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    // one-warp CTAs: occupancy is set by shared memory, so take the largest carveout
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared);
   });
   if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
   const unsigned grid = (unsigned)((C.tasks + CT_WARPS - 1) / CT_WARPS);
@@ -1190,22 +1193,16 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
     const bool ok =
         encode_2d(&cm.mu, mu, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
         encode_2d(&cm.pi, pi, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
-        encode_2d(&cm.a, actions, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, B, T, CT_COLS, CT_STEPS) &&
-        encode_2d(&cm.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, CT_COLS, CT_STEPS) &&
-        encode_2d(&cm.g, disc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, CT_COLS, CT_STEPS) &&
-        encode_2d(&cm.v, val, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, CT_COLS, CT_STEPS + 1) &&
-        encode_1d(&cm.boot, boot, B, CT_COLS) &&
         (!loss || encode_2d(&cm.dz, dlogits, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS));
     if (ok) {
       const CtLayout cl = make_ct_layout((int)A, elem);
       CtParams C;
       std::memset(&C, 0, sizeof(C));
-      C.pi = (unsigned)cl.pi; C.mu = (unsigned)cl.mu; C.a = (unsigned)cl.a; C.r = (unsigned)cl.r;
-      C.g = (unsigned)cl.g; C.v = (unsigned)cl.v; C.stage = (unsigned)cl.stage;
-      C.boot = (unsigned)cl.boot; C.warp_bytes = (unsigned)cl.warp_bytes;
+      C.pi = (unsigned)cl.pi; C.mu = (unsigned)cl.mu; C.stage = (unsigned)cl.stage;
+      C.warp_bytes = (unsigned)cl.warp_bytes;
       C.tasks = (int)tasks;
-      C.groups = (int)((tasks + CT_GROUP - 1) / CT_GROUP);
       C.K = (int)((T + CT_STEPS - 1) / CT_STEPS);
+      C.groups = (C.tasks + CT_GROUP - 1) / CT_GROUP;
       const WsLayout wl2 = ws_layout(plan);
       C.task_partials = reinterpret_cast<double*>(wsb + wl2.ct_task);
       C.group_partials = reinterpret_cast<double*>(wsb + wl2.ct_group);

@@ -295,3 +295,19 @@ def test_column_task_shard_equals_slice_bitwise():
         o = pkg.loss_and_grad(*[_dev(sh)[k] for k in NAMES], reward_mode=1)
         for k in ("grad_target_logits", "grad_values", "vs", "pg_advantages"):
             assert torch.equal(o[k], full[k][:, b0:b1]), (k, b0, b1)
+
+
+def test_column_task_deterministic_repeated_calls():
+    """Repeated calls on one workspace, alternating two inputs: bitwise equal results
+    (fixed-order partial reductions; the re-armed group counters leave no state)."""
+    a = wl.make_inputs("large", seed=51, B=8192, T=100)
+    b = wl.make_inputs("large", seed=52, B=8192, T=100)
+    da, db = _dev(a), _dev(b)
+    ra = {k: v.clone() for k, v in pkg.loss_and_grad(*[da[k] for k in NAMES], reward_mode=1).items()}
+    rb = {k: v.clone() for k, v in pkg.loss_and_grad(*[db[k] for k in NAMES], reward_mode=1).items()}
+    ws = pkg.Workspace(a["T"], a["B"], a["A"], a["dtype"])
+    for i in range(4):
+        d, r = (da, ra) if i % 2 == 0 else (db, rb)
+        o = pkg.loss_and_grad(*[d[k] for k in NAMES], workspace=ws, reward_mode=1)
+        for k in r:
+            assert torch.equal(o[k], r[k]), (i, k)
