@@ -376,8 +376,8 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
-        "dtype": "bf16 logits; f64 row sums / ratio / scan, f32 gradient epilogue"
-                 if elem == 2 else "f32 logits; f64 row sums / ratio / scan, f32 epilogue",
+        "dtype": ("bf16" if elem == 2 else "f32") + " logits; f32 exps with compensated "
+                 "(exact-order) sums, f64 ratio and scan, f32 gradient epilogue",
         "data": "synthetic (seeded, DMLab/Atari-shaped; DESIGN.md input recipe)",
         "config": {"workload": cfg.name, "T": T, "B_per_gpu": B, "A": A,
                    "logits_dtype": "bf16" if elem == 2 else "fp32",
@@ -389,7 +389,7 @@ def run_ours(args):
                    if world > 1 else "none"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "vtrace_fused_kernel", "kernel_ms": kernel_ms,
+                     "kernel": vt.kernel_for(T, B, A, inp["dtype"]), "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
         "gpu_launches": K,
         "clocks": clocks,

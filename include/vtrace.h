@@ -191,6 +191,14 @@ const char* vtrace_status_string(vt_status status);
 /* Library ABI version (major*10000 + minor*100 + patch). */
 int32_t vtrace_version(void);
 
+/* Name of the kernel a call with this shape takes when every pointer is 16-byte
+ * aligned (as torch / cudaMalloc allocations are): "vtrace_ct_kernel" (wide
+ * batches: one warp per 4 trajectories over the whole unroll),
+ * "vtrace_fused_kernel" (look-back kernel, TMA staging) or
+ * "vtrace_fused_kernel (plain loads)".  Host-only, no CUDA call; static string.
+ * Used by bench.py to name the kernel its roofline line describes. */
+const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype);
+
 #ifdef __cplusplus
 }
 #endif

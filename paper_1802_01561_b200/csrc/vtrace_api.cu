@@ -1091,6 +1091,23 @@ static vt_status check_params(const vt_vtrace_params* p) {
   return VT_OK;
 }
 
+enum KernelChoice { K_CT = 0, K_LOOKBACK_TMA = 1, K_LOOKBACK_PLAIN = 2 };
+
+// Which kernel a call takes (a pure function of the shape and pointer alignment):
+// the column-task kernel for wide batches, else the look-back kernel, with TMA
+// staging when pitches and bases are 16-byte aligned.
+static KernelChoice choose_kernel(long long T, long long B, long long A, int elem,
+                                  const Plan& plan, bool ptrs16) {
+  const bool tma = (A * BC <= 256) && (B * A < (1LL << 31)) && (T < (1LL << 31)) &&
+                   ((B * A * elem) % 16 == 0) && ((B * 4) % 16 == 0) && ptrs16 &&
+                   plan.Tc + 1 <= 256 && plan.smem <= kMaxSmem;
+  if (!tma) return K_LOOKBACK_PLAIN;
+  const long long tasks = (B + CT_COLS - 1) / CT_COLS;
+  const bool ct = ct_enabled() && tasks >= kCtMinTasks && (A * elem) % 4 == 0 &&
+                  CT_COLS * A <= 256 && (B % CT_COLS) == 0;
+  return ct ? K_CT : K_LOOKBACK_TMA;
+}
+
 static vt_status common_launch(bool loss, long long T, long long B, long long A, vt_dtype dt,
                                const void* mu, const void* pi, const int32_t* actions,
                                const float* disc, const float* rew, const float* val,
@@ -1162,11 +1179,11 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   // TMA eligibility: 16-byte aligned bases and row pitches, box inner <= 256 elements
   TmaMaps maps;
   std::memset(&maps, 0, sizeof(maps));
-  bool tma = (A * BC <= 256) && (B * A < (1LL << 31)) && (T < (1LL << 31)) && ((B * A * elem) % 16 == 0) && ((B * 4) % 16 == 0) &&
-             aligned(mu, 16) && aligned(pi, 16) && aligned(actions, 16) && aligned(disc, 16) &&
-             aligned(rew, 16) && aligned(val, 16) && aligned(boot, 16) &&
-             (!loss || aligned(dlogits, 16)) &&
-             plan.Tc + 1 <= 256 && plan.smem <= kMaxSmem;
+  const bool ptrs16 = aligned(mu, 16) && aligned(pi, 16) && aligned(actions, 16) &&
+                      aligned(disc, 16) && aligned(rew, 16) && aligned(val, 16) &&
+                      aligned(boot, 16) && (!loss || aligned(dlogits, 16));
+  const KernelChoice kc = choose_kernel(T, B, A, elem, plan, ptrs16);
+  bool tma = kc != K_LOOKBACK_PLAIN;
   if (tma) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -1183,8 +1200,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
 
   // column-task kernel: wide batches (enough 4-trajectory tasks to fill the GPU)
   const long long tasks = (B + CT_COLS - 1) / CT_COLS;
-  const bool ct = tma && ct_enabled() && tasks >= kCtMinTasks && (A * elem) % 4 == 0 &&
-                  CT_COLS * A <= 256 && (B % CT_COLS) == 0;
+  const bool ct = tma && kc == K_CT;
   if (ct) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -1346,6 +1362,18 @@ const char* vtrace_status_string(vt_status s) {
 }
 
 int32_t vtrace_version(void) { return 100; }
+
+const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype) {
+  if (T <= 0 || B <= 0 || A <= 0 || A > VT_MAX_ACTIONS) return "none (invalid shape)";
+  if (logits_dtype != VT_FLOAT32 && logits_dtype != VT_BFLOAT16) return "none (invalid dtype)";
+  const int elem = logits_dtype == VT_BFLOAT16 ? 2 : 4;
+  const Plan plan = make_plan(T, B, (int)A, elem);
+  switch (choose_kernel(T, B, A, elem, plan, true)) {
+    case K_CT: return "vtrace_ct_kernel";
+    case K_LOOKBACK_TMA: return "vtrace_fused_kernel";
+    default: return "vtrace_fused_kernel (plain loads)";
+  }
+}
 
 // Debug hook, not declared in include/vtrace.h: while set, every launch records
 // clock64() per CTA and iteration into buf[grid][iters][8] (device memory).

@@ -33,7 +33,8 @@ DATA_ERRORS = {0: "ok", 1: "action", 2: "logits", 3: "reward", 4: "value", 5: "d
 
 EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_from_logits",
                     "vtrace_loss_and_grad", "vtrace_loss_and_grad_from_host",
-                    "vtrace_read_device_status", "vtrace_status_string", "vtrace_version")
+                    "vtrace_read_device_status", "vtrace_status_string", "vtrace_version",
+                    "vtrace_kernel_for")
 
 
 class VtraceError(RuntimeError):
@@ -86,6 +87,8 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_status_string.restype = ctypes.c_char_p
     lib.vtrace_version.argtypes = []
     lib.vtrace_version.restype = ctypes.c_int32
+    lib.vtrace_kernel_for.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
+    lib.vtrace_kernel_for.restype = ctypes.c_char_p
     _lib = lib
     return lib
 
@@ -258,6 +261,14 @@ def read_device_status(workspace: Workspace):
 
 def version() -> int:
     return int(load_library().vtrace_version())
+
+
+def kernel_for(T: int, B: int, A: int, dtype) -> str:
+    """Name of the kernel a (T, B, A, dtype) call takes (16-byte aligned tensors);
+    dtype: torch.float32 / torch.bfloat16 or the library code (0 / 1)."""
+    code = dtype if isinstance(dtype, int) else {torch.float32: VT_FLOAT32,
+                                                  torch.bfloat16: VT_BFLOAT16}[dtype]
+    return load_library().vtrace_kernel_for(int(T), int(B), int(A), int(code)).decode()
 
 
 # ---------------------------------------------------------------------------

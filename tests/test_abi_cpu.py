@@ -111,3 +111,16 @@ def test_binding_has_no_cpu_fallback(lib):
     with pytest.raises((ValueError, RuntimeError, AssertionError)):
         pkg.loss_and_grad(x, x, torch.zeros(2, 2, dtype=torch.int32), torch.zeros(2, 2),
                           torch.zeros(2, 2), torch.zeros(2, 2), torch.zeros(2))
+
+
+def test_kernel_choice(lib):
+    """Host-only query of the kernel a shape takes: wide batches (>= 1024 tasks of 4
+    trajectories) the column-task kernel, else the look-back kernel (TMA when the
+    pitches are 16-byte multiples)."""
+    assert vt.kernel_for(100, 8192, 18, 1) == "vtrace_ct_kernel"          # large
+    assert vt.kernel_for(100, 4096, 18, 1) == "vtrace_ct_kernel"
+    assert vt.kernel_for(100, 4092, 18, 1) == "vtrace_fused_kernel"       # 1023 tasks
+    assert vt.kernel_for(2000, 1024, 9, 0) == "vtrace_fused_kernel"       # stress
+    assert vt.kernel_for(5, 2, 3, 0) == "vtrace_fused_kernel (plain loads)"  # toy: pitch 24 B
+    assert vt.kernel_for(0, 8, 3, 0).startswith("none")
+    assert vt.kernel_for(5, 8, 3, 7).startswith("none")
