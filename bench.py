@@ -391,7 +391,7 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": vt.kernel_for(T, B, A, inp["dtype"]), "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
-        "gpu_launches": K,
+        "gpu_launches": K,  # one fused kernel per step
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -476,7 +476,12 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
-        run_reference(a)
-    else:
-        run_ours(a)
+    try:
+        if a.impl == "reference":
+            run_reference(a)
+        else:
+            run_ours(a)
+    finally:
+        import torch.distributed as _dist
+        if _dist.is_available() and _dist.is_initialized():
+            _dist.destroy_process_group()

@@ -192,11 +192,14 @@ const char* vtrace_status_string(vt_status status);
 int32_t vtrace_version(void);
 
 /* Name of the kernel a call with this shape takes when every pointer is 16-byte
- * aligned (as torch / cudaMalloc allocations are): "vtrace_ct_kernel" (wide
- * batches: one warp per 4 trajectories over the whole unroll),
+ * aligned (as torch / cudaMalloc allocations are): "vtrace_ctb_kernel" (wide
+ * batches, one 16-warp CTA per SM: one warp per 4 trajectories, the remainder
+ * cut into time segments to balance the SM sub-partitions; needs the current
+ * device's SM count), "vtrace_ct_kernel" (wide batches, one-warp CTAs),
  * "vtrace_fused_kernel" (look-back kernel, TMA staging) or
- * "vtrace_fused_kernel (plain loads)".  Host-only, no CUDA call; static string.
- * Used by bench.py to name the kernel its roofline line describes. */
+ * "vtrace_fused_kernel (plain loads)".  Host-only (at most a device-attribute
+ * query, no launch); static string.  Used by bench.py to name the kernel its
+ * roofline line describes. */
 const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype);
 
 #ifdef __cplusplus

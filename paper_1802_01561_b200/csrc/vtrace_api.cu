@@ -885,8 +885,8 @@ static WsLayout ws_layout(const Plan& p) {
   w.ct_task = a128(w.cta + (size_t)kMaxCtas * NPART * sizeof(double));
   const size_t tasks = (size_t)(p.G * BC + CT_COLS - 1) / CT_COLS;  // >= ceil(B / 4)
   const size_t groups = (tasks + CT_GROUP - 1) / CT_GROUP;
-  w.ct_group = a128(w.ct_task + tasks * NPART * sizeof(double));
-  w.ct_count = a128(w.ct_group + groups * NPART * sizeof(double));
+  w.ct_group = a128(w.ct_task + tasks * NPART * sizeof(TagRec));
+  w.ct_count = a128(w.ct_group + groups * NPART * sizeof(TagRec));
   w.total = a128(w.ct_count + (groups + 1) * sizeof(unsigned int));
   return w;
 }
@@ -1046,9 +1046,64 @@ static bool ct_enabled() {  // VTRACE_KERNEL=lookback forces the look-back kerne
   return v == 1;
 }
 
+static int num_sms_cached() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// Work split of the balanced kernel (one CTB_WARPS-warp CTA per SM): f whole tasks
+// per SM sub-partition (f4 = 4 f warps per CTA), the remaining R tasks cut into
+// `segs` time segments, `tpc` cut tasks per CTA; chosen to minimise the largest
+// per-sub-partition load f + ceil(segs tpc / 4) / segs.  False if it does not fit.
+static bool plan_balanced(CtParams& C, int S) {
+  const char* e = getenv("VTRACE_CT_BALANCED");  // "0": one-warp CTAs (A/B, tests)
+  if ((e && e[0] == '0') || S <= 0) return false;
+  if ((size_t)CTB_WARPS * C.warp_bytes > kMaxSmem) return false;  // e.g. fp32 logits, A = 18
+  const long long N = C.tasks;
+  const int f = (int)std::min<long long>(N / (4LL * S), 4);
+  if (f < 1) return false;
+  const long long R = N - 4LL * f * S;
+  if (R == 0) {
+    C.f4 = 4 * f; C.segs = 1; C.seg_len = C.K; C.tpc = 0;
+    return true;
+  }
+  const int tpc = (int)((R + S - 1) / S);
+  double best = 1e30;
+  int best_p = 0;
+  for (int segs = 1; segs <= 4 && segs <= C.K; ++segs) {
+    if (4 * f + segs * tpc > CTB_WARPS) continue;
+    const double load = f + (double)((segs * tpc + 3) / 4) / segs;
+    if (load < best - 1e-9) { best = load; best_p = segs; }
+  }
+  if (best_p == 0) return false;
+  C.f4 = 4 * f; C.segs = best_p; C.tpc = tpc;
+  C.seg_len = (C.K + best_p - 1) / best_p;
+  // every segment non-empty (a later one waits for the carry of an earlier one)
+  if ((best_p - 1) * C.seg_len >= C.K) return false;
+  return true;
+}
+
 template <typename LT, int A_CT, bool LOSS, int MODE>
-static vt_status ct_launch_one(const Params& P, const CtParams& C, const TmaMaps& maps,
+static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
                                cudaStream_t st) {
+  const int S = num_sms_cached();
+  if (plan_balanced(C, S)) {
+    auto kern = vtrace_ctb_kernel<LT, A_CT, LOSS, MODE>;
+    const size_t smem = (size_t)CTB_WARPS * C.warp_bytes;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    });
+    if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
+    kern<<<S, CTB_WARPS * 32, smem, st>>>(P, C, maps);
+    return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+  }
   auto kern = vtrace_ct_kernel<LT, A_CT, LOSS, MODE>;
   const size_t smem = (size_t)CT_WARPS * C.warp_bytes;
   static std::once_flag once;
@@ -1104,7 +1159,8 @@ static KernelChoice choose_kernel(long long T, long long B, long long A, int ele
   if (!tma) return K_LOOKBACK_PLAIN;
   const long long tasks = (B + CT_COLS - 1) / CT_COLS;
   const bool ct = ct_enabled() && tasks >= kCtMinTasks && (A * elem) % 4 == 0 &&
-                  CT_COLS * A <= 256 && (B % CT_COLS) == 0;
+                  CT_COLS * A <= 256 && (B % CT_COLS) == 0 &&
+                  (T + CT_STEPS) * B < (1LL << 31);  // 32-bit row offsets
   return ct ? K_CT : K_LOOKBACK_TMA;
 }
 
@@ -1218,12 +1274,12 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
       C.warp_bytes = (unsigned)cl.warp_bytes;
       C.tasks = (int)tasks;
       C.K = (int)((T + CT_STEPS - 1) / CT_STEPS);
-      C.groups = (C.tasks + CT_GROUP - 1) / CT_GROUP;
       const WsLayout wl2 = ws_layout(plan);
-      C.task_partials = reinterpret_cast<double*>(wsb + wl2.ct_task);
-      C.group_partials = reinterpret_cast<double*>(wsb + wl2.ct_group);
+      C.task_recs = reinterpret_cast<TagRec*>(wsb + wl2.ct_task);
+      C.timing = g_timing;
+      C.group_recs = reinterpret_cast<TagRec*>(wsb + wl2.ct_group);
       C.group_count = reinterpret_cast<unsigned int*>(wsb + wl2.ct_count);
-      C.top_count = C.group_count + C.groups;
+      C.top_count = C.group_count + (C.tasks + CT_GROUP - 1) / CT_GROUP;
       if (dt == VT_BFLOAT16)
         return loss ? ct_dispatch<__nv_bfloat16, true>(P, C, cm, st)
                     : ct_dispatch<__nv_bfloat16, false>(P, C, cm, st);
@@ -1369,7 +1425,19 @@ const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_d
   const int elem = logits_dtype == VT_BFLOAT16 ? 2 : 4;
   const Plan plan = make_plan(T, B, (int)A, elem);
   switch (choose_kernel(T, B, A, elem, plan, true)) {
-    case K_CT: return "vtrace_ct_kernel";
+    case K_CT: {
+      CtParams C;
+      std::memset(&C, 0, sizeof(C));
+      C.warp_bytes = (unsigned)make_ct_layout((int)A, elem).warp_bytes;
+      C.tasks = (int)((B + CT_COLS - 1) / CT_COLS);
+      C.K = (int)((T + CT_STEPS - 1) / CT_STEPS);
+      int S = 0, dev = 0;  // the balanced split needs the SM count of the current device
+      if (cudaGetDevice(&dev) == cudaSuccess &&
+          cudaDeviceGetAttribute(&S, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+          plan_balanced(C, S))
+        return "vtrace_ctb_kernel";
+      return "vtrace_ct_kernel";
+    }
     case K_LOOKBACK_TMA: return "vtrace_fused_kernel";
     default: return "vtrace_fused_kernel (plain loads)";
   }

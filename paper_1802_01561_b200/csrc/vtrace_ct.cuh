@@ -25,7 +25,6 @@ constexpr int CT_STEPS = 8;
 constexpr int CT_ROWS = CT_COLS * CT_STEPS;  // 32 == warp size
 constexpr int CT_NSTAGE = 4;                 // logits stages: chunks in flight + the one computed
 constexpr int CT_WARPS = 1;                  // warps (tasks) per CTA
-constexpr int CT_GROUP = 32;                 // tasks per partials group
 static_assert(CT_ROWS == 32, "one row per lane");
 
 struct CtLayout {
@@ -44,10 +43,13 @@ __host__ __device__ inline CtLayout make_ct_layout(int A, int elem) {
 
 struct CtParams {
   unsigned int pi, mu, stage, warp_bytes;  // CtLayout, 32-bit
-  int tasks, K, groups;
-  double* task_partials;   // [tasks][NPART]
-  double* group_partials;  // [groups][NPART]
-  unsigned int* group_count;  // [groups], re-armed to 0 by the last arriver
+  int tasks, K;
+  int f4, segs, seg_len, tpc;  // balanced kernel: whole-task warps per CTA, segments per
+                               // cut task, chunks per segment, cut tasks per CTA
+  unsigned long long* timing;  // debug: per task [start, own end, group done, exit] (ns)
+  TagRec* task_recs;   // [tasks][NPART] (value, epoch tag)
+  TagRec* group_recs;  // [groups][NPART]
+  unsigned int* group_count;  // [groups] tickets, re-armed by the last arrival
   unsigned int* top_count;
 };
 
@@ -155,60 +157,102 @@ __device__ __forceinline__ void ct_stats_fast(const LT* zrow, const LT* mrow, in
   R.finite = isfinite(sd.x) && isfinite(sd.y) && isfinite(mp) && isfinite(mm);
 }
 
-// a12 for one task: its partial sums -> group of CT_GROUP tasks -> total, in fixed
-// orders (the last arriver of a group reduces it; the last group the total).
-__device__ __forceinline__ void ct_unit_partials(const Params& P, const CtParams& C, int u,
-                                                 int lane, double (&part)[NPART]) {
+constexpr int CT_GROUP = 32;  // tasks per partials group
+
+// Waits until the N partial-sum records at p[0 .. N) carry this call's tag (relaxed
+// 16-byte loads: value and tag arrive together, so no fence on either side); all N
+// loads of a poll are in flight at once.
+template <int N, int SLEEP_NS = 1000>
+__device__ __forceinline__ int wait_recs(const TagRec* p, unsigned long long tag,
+                                         double (&v)[N]) {
+  int spins = 0;
+  while (true) {
+    unsigned long long t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) ld_tag16(p + i, v[i], t[i]);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ok = ok && (t[i] == tag);
+    if (ok) return spins;
+    ++spins;
+    __nanosleep(SLEEP_NS);
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return g;
+}
+
+// a12: task sums -> group of CT_GROUP tasks -> total, in fixed orders.  Every task
+// publishes its 8 sums as epoch-tagged 16-byte (value, tag) records (st.relaxed.v2:
+// value and tag arrive together, no fence) and takes a ticket from its group's
+// counter (relaxed atomic); the last to arrive reduces the group in task order,
+// reading the records by index and checking their tags.  Likewise the last group to
+// arrive reduces the groups, writes the result and re-arms the counters.  The sums
+// are formed in index order whatever the arrival order: bitwise reproducible.
+__device__ __forceinline__ void ct_partials(const Params& P, const CtParams& C, int task,
+                                            int lane, unsigned long long tag,
+                                            double (&part)[NPART]) {
 #pragma unroll
   for (int k = 0; k < NPART; ++k) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part[k] += __shfl_xor_sync(0xffffffffu, part[k], o);
   }
-  if (lane < NPART) {
-    double v = part[0];
+  auto pick = [&](const double (&x)[NPART]) {  // x[lane] for lane < NPART
+    double v = x[0];
 #pragma unroll
-    for (int k = 1; k < NPART; ++k) v = (lane == k) ? part[k] : v;
-    C.task_partials[(size_t)u * NPART + lane] = v;
-  }
-  __threadfence();
-  __syncwarp();
-  const int grp = u / CT_GROUP;
+    for (int k = 1; k < NPART; ++k) v = (lane == k) ? x[k] : v;
+    return v;
+  };
+  const int grp = task / CT_GROUP;
   const int g0 = grp * CT_GROUP, gn = min(CT_GROUP, C.tasks - g0);
+  {
+    const double v = pick(part);
+    if (lane < NPART) st_tag16(C.task_recs + (size_t)task * NPART + lane, v, tag);
+  }
   unsigned int prev = 0;
   if (lane == 0) prev = atomicAdd(C.group_count + grp, 1u);
   prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != (unsigned int)(gn - 1)) return;  // not the last task of the group
-  __threadfence();
-  // lane l holds task g0 + l; reduce the group in a fixed tree per partial
+  if (C.timing && lane == 0) C.timing[(size_t)task * 4 + 1] = gtimer();
+  if (prev != (unsigned int)(gn - 1)) return;
+  if (lane == 0) C.group_count[grp] = 0u;  // every ticket of this group is taken: re-arm
+  // the group's last arrival: lane l reads task g0 + l (its own from registers)
   double gp[NPART];
 #pragma unroll
-  for (int k = 0; k < NPART; ++k)
-    gp[k] = lane < gn ? __ldcg(C.task_partials + (size_t)(g0 + lane) * NPART + k) : 0.0;
+  for (int k = 0; k < NPART; ++k) gp[k] = (g0 + lane == task) ? part[k] : 0.0;
+  if (lane < gn && g0 + lane != task)
+    wait_recs<NPART, 32>(C.task_recs + (size_t)(g0 + lane) * NPART, tag, gp);
 #pragma unroll
   for (int k = 0; k < NPART; ++k) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gp[k] += __shfl_xor_sync(0xffffffffu, gp[k], o);
   }
-  if (lane < NPART) {
-    double v = gp[0];
-#pragma unroll
-    for (int k = 1; k < NPART; ++k) v = (lane == k) ? gp[k] : v;
-    C.group_partials[(size_t)grp * NPART + lane] = v;
+  {
+    const double v = pick(gp);
+    if (lane < NPART) st_tag16(C.group_recs + (size_t)grp * NPART + lane, v, tag);
   }
-  if (lane == 0) C.group_count[grp] = 0u;  // re-arm for the next call
-  __threadfence();
-  __syncwarp();
+  const int ng = (C.tasks + CT_GROUP - 1) / CT_GROUP;
   if (lane == 0) prev = atomicAdd(C.top_count, 1u);
   prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != (unsigned int)(C.groups - 1)) return;
-  __threadfence();
-  // the last group: lanes stride the groups (fixed order), then a fixed tree
+  if (C.timing && lane == 0) C.timing[(size_t)task * 4 + 2] = gtimer();
+  if (prev != (unsigned int)(ng - 1)) return;
+  if (lane == 0) *C.top_count = 0u;
+  // the last group: lane l adds groups l, l + 32, ... in order, then a fixed tree
   double tp[NPART];
 #pragma unroll
   for (int k = 0; k < NPART; ++k) tp[k] = 0.0;
-  for (int gi = lane; gi < C.groups; gi += 32) {
+  for (int gi = lane; gi < ng; gi += 32) {
+    double x[NPART];
+    if (gi == grp) {
 #pragma unroll
-    for (int k = 0; k < NPART; ++k) tp[k] += __ldcg(C.group_partials + (size_t)gi * NPART + k);
+      for (int k = 0; k < NPART; ++k) x[k] = gp[k];
+    } else {
+      wait_recs<NPART, 32>(C.group_recs + (size_t)gi * NPART, tag, x);
+    }
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) tp[k] += x[k];
   }
 #pragma unroll
   for (int k = 0; k < NPART; ++k) {
@@ -220,34 +264,41 @@ __device__ __forceinline__ void ct_unit_partials(const Params& P, const CtParams
         tp[VT_P_PG_LOSS] + P.c_v * tp[VT_P_BASELINE_LOSS] - P.c_e * tp[VT_P_ENTROPY_SUM];
 #pragma unroll
     for (int k = 0; k < NPART; ++k) P.partials[k] = tp[k];
-    *C.top_count = 0u;
+    if (C.timing) C.timing[(size_t)task * 4 + 3] = gtimer();
+    // every record of this call has been read: the next call uses the next tag
+    *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) =
+        (unsigned int)((tag >> 2) + 1u) & 0x3fffffffu;
   }
 }
 
+// Tail / data accumulators of one warp's work.
+struct CtAcc {
+  float pg, v, H, dz, dv, rho, clip;
+};
+
+// One warp runs iterations [it_begin, it_end) of task `task` (4 trajectories): its
+// TMA ring (`base`, barriers `wb`), the per-step loads, a3-a11 per chunk.  The
+// carry A just after the segment comes from `cin` (another warp of the CTA, when
+// `cin_bar` completes) or is A_T = 0; the carry at the segment's first step goes
+// to `cout` / `cout_bar` for the warp running the earlier segment.
 template <typename LT, int A_CT, bool LOSS, int MODE>
-__global__ void __launch_bounds__(CT_WARPS * 32)
-    vtrace_ct_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[CT_WARPS][CT_NSTAGE];
+__device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const TmaMaps& maps,
+                                       unsigned char* base, uint64_t* wb, const int lane,
+                                       const int task, const int it_begin, const int it_end,
+                                       const double* cin, uint64_t* cin_bar, double* cout,
+                                       uint64_t* cout_bar, CtAcc& acc_out) {
   constexpr bool kFast = (A_CT > 0) && (A_CT % 2 == 0) && (MODE == EXP_MUFU);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * CT_WARPS + warp;
-  if (task >= C.tasks) return;  // warp-uniform
   const int A = (A_CT > 0) ? A_CT : P.A;
   const int T = P.T32, B = P.B32;
   const int K = C.K;
   const int b0 = task * CT_COLS;
   const int blen = min(CT_COLS, B - b0);
-  unsigned char* base = smem + (size_t)warp * C.warp_bytes;
-  uint64_t* wb = bar[warp];
   const uint32_t tile_bytes = (uint32_t)((size_t)CT_ROWS * A * sizeof(LT));
-  constexpr int it_begin = 0;
-  const int it_end = K;
 
   // chunk of iteration `it` (reverse time): k = K - 1 - it, t0 = 8 k; stage it mod NSTAGE
   auto load_iter = [&](int it) {  // lane 0 only
     if (it >= it_end) return;
-    const int stg = it % CT_NSTAGE;
+    const int stg = (it - it_begin) % CT_NSTAGE;
     const int t0 = (K - 1 - it) * CT_STEPS;
     unsigned char* sb = base + (size_t)stg * C.stage;
     mbar_expect_tx(&wb[stg], 2 * tile_bytes);
@@ -257,7 +308,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
   if (lane == 0) {
     for (int s = 0; s < CT_NSTAGE; ++s) mbar_init(&wb[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < CT_NSTAGE; ++i) load_iter(i);
+    for (int i = 0; i < CT_NSTAGE; ++i) load_iter(it_begin + i);
   }
   __syncwarp();
   uint32_t phase_bits = 0;  // bit s: parity of stage s's next completion
@@ -266,7 +317,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
   const float cv = (float)P.c_v;
   const float rho_bar_f = (float)P.rho_bar;
   const int tl = lane >> 2, c = lane & 3;  // row (tl, c) of the [8 steps][4 columns] chunk
-  const long long stepB = (long long)CT_STEPS * B;
+  const int stepB = CT_STEPS * B;  // T * B < 2^31 on this path (host check)
   float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
         acc_clip = 0.f;
   double carry = 0.0;  // A = v - V just after the current chunk, for column c (A_T = 0)
@@ -277,9 +328,9 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
     int a;
     float r, g, v, vn;
   };
-  const long long off0 = (long long)((K - 1) * CT_STEPS + tl) * B + b0 + c;
+  const int off0 = ((K - 1 - it_begin) * CT_STEPS + tl) * B + b0 + c;
   const float* const bootp = P.boot + b0 + c;
-  auto load_step = [&](int it, long long off, StepIn& s) {
+  auto load_step = [&](int it, int off, StepIn& s) {
     const int t = (K - 1 - it) * CT_STEPS + tl;
     s.a = 0; s.r = 0.f; s.g = 0.f; s.v = 0.f; s.vn = 0.f;
     if (t < T && c < blen) {
@@ -291,13 +342,12 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       s.vn = __ldg((t + 1 < T) ? P.val + off + B : bootp);
     }
   };
-  StepIn cur, nxt;
-  load_step(0, off0, cur);
-  nxt = cur;
 
   int st = 0;  // (it - it_begin) mod NSTAGE
-  long long off = off0;  // this iteration's row
-  for (int it = it_begin; it < it_end; ++it, off -= stepB) {
+  int off = off0;  // this iteration's row
+  // one chunk; `cur` holds its per-step inputs, `nxt` receives the next chunk's (two
+  // register sets used alternately: no copy that would wait on loads in flight)
+  auto chunk = [&](const int it, const StepIn& cur, StepIn& nxt) {
     if (it + 1 < it_end) load_step(it + 1, off - stepB, nxt);
     const int t0 = (K - 1 - it) * CT_STEPS;
     const int tlen = min(CT_STEPS, T - t0);
@@ -334,7 +384,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       fin = fin_p && fin_m;
     }
     // pi(a)/mu(a) = exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) S_mu / S_pi
-    const double ratio = exp64(xa_p - xa_m) * (S_m / S_p);
+    const double ratio = exp64(xa_p - xa_m) * ddiv_pos(S_m, S_p);
     const float rt = cur.r, gm = cur.g, Vt = cur.v, Vn = cur.vn;
     const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
     double dl = dmin_t(P.rho_bar, ratio) * td;                         // delta_t V
@@ -349,7 +399,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
     }
     if (!LOSS && row_ok) {
-      const long long row = off;
+      const int row = off;
       if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
       if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
       if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
@@ -361,7 +411,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       gc = 1.0;
     }
     if (bad) {
-      const long long row = off;
+      const int row = off;
       if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
       if (!fin) record_bad(P.ws, row, VT_DATA_LOGITS);
       if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
@@ -374,6 +424,11 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
     // ---- a8: suffix scan of the chunk's affine maps, per column ----------------
     // lanes c, c+4, ..., c+28 are steps 0..7 of column c; composing later steps:
     // (G1, D1) o (G2, D2) = (G1 G2, D1 + G1 D2)
+    if (cin != nullptr && it == it_begin) {
+      // A just after this segment = A at the first step of the later segment
+      mbar_wait_sleep(cin_bar, 0u, 500);
+      carry = cin[c];
+    }
     double Gi = gc, Di = dl;
 #pragma unroll
     for (int o = CT_COLS; o < 32; o <<= 1) {
@@ -389,7 +444,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
 
     // ---- a9-a11: advantages, value gradient, policy gradient ------------------
     if (row_ok) {
-      const long long row = off;
+      const int row = off;
       // pg_adv = rho_pg (r + gamma v_{t+1} - V) = rho_pg (td + gamma A_{t+1})
       const float pgr = (float)(dmin_t(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
       if (P.vs) P.vs[row] = (float)((double)Vt + A_t);
@@ -471,14 +526,170 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
       load_iter(it + CT_NSTAGE - 1);
     }
     __syncwarp();
-    cur = nxt;
+    off -= stepB;
     if (++st == CT_NSTAGE) st = 0;
+  };
+  StepIn sA, sB;
+  load_step(it_begin, off0, sA);
+  for (int it = it_begin; it < it_end; it += 2) {
+    chunk(it, sA, sB);
+    if (it + 1 < it_end) chunk(it + 1, sB, sA);
+  }
+  if (cout != nullptr) {  // hand the carry at this segment's first step on
+    if (tl == 0) cout[c] = carry;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cout_bar);
   }
   if constexpr (LOSS) {
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // the gradient stores must have read the stages before the CTA's smem goes away
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  acc_out = CtAcc{acc_pg, acc_v, acc_H, acc_dz, acc_dv, acc_rho, acc_clip};
+}
+
+template <typename LT, int A_CT, bool LOSS, int MODE>
+__global__ void __launch_bounds__(CT_WARPS * 32)
+    vtrace_ct_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[CT_NSTAGE];
+  const int lane = threadIdx.x & 31;
+  const int task = blockIdx.x;
+  if (task >= C.tasks) return;
+  if (C.timing && lane == 0) C.timing[(size_t)task * 4 + 0] = gtimer();
+  CtAcc acc;
+  ct_run<LT, A_CT, LOSS, MODE>(P, C, maps, smem, bar, lane, task, 0, C.K, nullptr, nullptr,
+                               nullptr, nullptr, acc);
+  if constexpr (LOSS) {
     if (P.partials != nullptr) {
-      double part[NPART] = {acc_pg, acc_v, acc_H, 0.0, acc_dz, acc_dv, acc_rho, acc_clip};
-      ct_unit_partials(P, C, task, lane, part);
+      const unsigned int epoch =
+          *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+      const unsigned long long tag = ((unsigned long long)epoch << 2) | 3ull;
+      double part[NPART] = {acc.pg, acc.v, acc.H, 0.0, acc.dz, acc.dv, acc.rho, acc.clip};
+      ct_partials(P, C, task, lane, tag, part);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Balanced column-task kernel: one CTA of CTB_WARPS = 16 warps per SM, so warp w
+// runs on SM sub-partition w mod 4.  The first f4 = 4 f warps take whole tasks
+// (f per sub-partition); the remaining tasks are cut into P time segments run by
+// P consecutive warps (on different sub-partitions), the carry passed down the
+// chain through shared memory and an mbarrier.  With B = 8192 on 148 SMs: 12 whole
+// tasks + 4 half tasks per SM, i.e. 3.5 tasks of work per sub-partition instead of
+// the 4/4/3/3 split of one-warp CTAs.  Partials: warp sums -> CTA sum (warp order)
+// -> the last CTA to finish adds the CTA sums in CTA order.
+constexpr int CTB_WARPS = 16;
+
+template <typename LT, int A_CT, bool LOSS, int MODE>
+__global__ void __launch_bounds__(CTB_WARPS * 32, 1)
+    vtrace_ctb_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[CTB_WARPS][CT_NSTAGE];
+  __shared__ __align__(8) uint64_t hbar[CTB_WARPS];
+  __shared__ double hcarry[CTB_WARPS][CT_COLS];
+  __shared__ double wpart[CTB_WARPS][NPART];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cta = blockIdx.x, S = gridDim.x;
+  if (lane == 0) {
+    mbar_init(&hbar[w], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // this warp's share: a whole task, or segment p of a task cut in C.segs.  Slots
+  // are laid over the warps diagonally (slot j -> warp 4 ((j + j/4) mod 4) + j mod 4),
+  // so any 4 consecutive slots fall on 4 different sub-partitions whether the
+  // hardware maps warp w to sub-partition w mod 4 or w / 4; the segment slots come
+  // first (j < 16 - f4), the whole tasks take the rest.
+  int task = -1, it_begin = 0, it_end = C.K, p = 0;
+  const int jslot = ((w >> 2) - (w & 3) + 4) & 3;  // block of the inverse diagonal map
+  const int slot = 4 * jslot + (w & 3);
+  const int nseg = CTB_WARPS - C.f4;  // segment slots
+  if (slot >= nseg) {
+    task = cta * C.f4 + (slot - nseg);
+  } else {
+    const int j = slot, i = j / C.segs;
+    p = j - i * C.segs;
+    if (i < C.tpc) {
+      const int t = C.f4 * S + cta * C.tpc + i;
+      if (t < C.tasks) {
+        task = t;
+        it_begin = p * C.seg_len;
+        it_end = min(C.K, it_begin + C.seg_len);
+      }
+    }
+  }
+  CtAcc acc = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (task >= 0) {
+    const bool whole = slot >= nseg;
+    const bool first = whole || p == 0, last = whole || p == C.segs - 1;
+    // segment hand-over slots: slot j feeds slot j + 1 (same task)
+    ct_run<LT, A_CT, LOSS, MODE>(P, C, maps, smem + (size_t)w * C.warp_bytes, bar[w], lane,
+                                 task, it_begin, it_end, first ? nullptr : hcarry[slot - 1],
+                                 &hbar[first ? slot : slot - 1], last ? nullptr : hcarry[slot],
+                                 &hbar[slot], acc);
+  }
+  if constexpr (LOSS) {
+    if (P.partials == nullptr) return;
+    double part[NPART] = {acc.pg, acc.v, acc.H, 0.0, acc.dz, acc.dv, acc.rho, acc.clip};
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part[k] += __shfl_xor_sync(0xffffffffu, part[k], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) wpart[w][k] = part[k];
+    }
+    __syncthreads();
+    if (w != 0) return;
+    double cs[NPART];  // this CTA's sums, warps in order
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) {
+      double x = 0.0;
+      for (int v = 0; v < CTB_WARPS; ++v) x += wpart[v][k];
+      cs[k] = x;
+    }
+    const unsigned int epoch =
+        *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+    const unsigned long long tag = ((unsigned long long)epoch << 2) | 3ull;
+    {
+      double v = cs[0];
+#pragma unroll
+      for (int k = 1; k < NPART; ++k) v = (lane == k) ? cs[k] : v;
+      if (lane < NPART) st_tag16(C.task_recs + (size_t)cta * NPART + lane, v, tag);
+    }
+    unsigned int prev = 0;
+    if (lane == 0) prev = atomicAdd(C.top_count, 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned int)(S - 1)) return;
+    if (lane == 0) *C.top_count = 0u;
+    // the last CTA: lane l adds CTAs l, l + 32, ... in order, then a fixed tree
+    double tp[NPART];
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) tp[k] = 0.0;
+    for (int ci = lane; ci < S; ci += 32) {
+      double x[NPART];
+      if (ci == cta) {
+#pragma unroll
+        for (int k = 0; k < NPART; ++k) x[k] = cs[k];
+      } else {
+        wait_recs<NPART, 32>(C.task_recs + (size_t)ci * NPART, tag, x);
+      }
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) tp[k] += x[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NPART; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tp[k] += __shfl_xor_sync(0xffffffffu, tp[k], o);
+    }
+    if (lane == 0) {
+      tp[VT_P_TOTAL_LOSS] =
+          tp[VT_P_PG_LOSS] + P.c_v * tp[VT_P_BASELINE_LOSS] - P.c_e * tp[VT_P_ENTROPY_SUM];
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) P.partials[k] = tp[k];
+      *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
     }
   }
 }

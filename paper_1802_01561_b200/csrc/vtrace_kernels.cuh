@@ -119,6 +119,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// mbar_wait for long waits: test without blocking, sleep between tests (a waiting
+// warp should not take issue slots from the warps sharing its sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, int ns) {
+  const uint32_t addr = smem_u32(bar);
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(phase)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // release.cta semantics
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -251,6 +273,19 @@ __device__ __forceinline__ void load_row(const LT* row, float (&z)[A_CT]) {
 #pragma unroll
     for (int j = 0; j < A_CT; ++j) z[j] = Elem<LT>::get(row, j);
   }
+}
+
+// a / b in fp64 for b in [1, 2^30] (a row sum): MUFU reciprocal seed, two Newton steps
+// and one residual correction (within an ulp; no slow-path branch as in div.rn.f64).
+__device__ __forceinline__ double ddiv_pos(double a, double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
 }
 
 // fp64 exp, argument clamped to [-700, 700].  Cody-Waite reduction

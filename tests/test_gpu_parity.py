@@ -311,3 +311,23 @@ def test_column_task_deterministic_repeated_calls():
         o = pkg.loss_and_grad(*[d[k] for k in NAMES], workspace=ws, reward_mode=1)
         for k in r:
             assert torch.equal(o[k], r[k]), (i, k)
+
+
+@pytest.mark.parametrize("T,B", [(100, 8192), (60, 6000), (17, 4800), (100, 9472)])
+def test_balanced_kernel_matches_one_warp_ctas(T, B, monkeypatch):
+    """The balanced column-task kernel (16-warp CTA per SM, remainder tasks cut into
+    time segments with the carry handed over in shared memory) gives bitwise the
+    outputs of the one-warp-CTA kernel; partials agree to fp32 accumulation order."""
+    inp = wl.make_inputs("large", seed=T + B, T=T, B=B)
+    dev = _dev(inp)
+    args = [dev[k] for k in NAMES]
+    monkeypatch.setenv("VTRACE_CT_BALANCED", "0")
+    ref = {k: v.clone() for k, v in pkg.loss_and_grad(*args, reward_mode=1).items()}
+    monkeypatch.setenv("VTRACE_CT_BALANCED", "1")
+    o = pkg.loss_and_grad(*args, reward_mode=1)
+    for k in ("grad_target_logits", "grad_values", "vs", "pg_advantages"):
+        assert torch.equal(o[k], ref[k]), k
+    np.testing.assert_allclose(o["partials"].cpu().numpy(), ref["partials"].cpu().numpy(),
+                               rtol=1e-6)
+    ro = oracle.loss_and_grad(inp, reward_mode=1)["partials"]
+    np.testing.assert_allclose(o["partials"].cpu().numpy()[:7], ro[:7], rtol=1e-5)
