@@ -31,6 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for flag in ("VTRACE_SUM_F64",):  # A/B experiments only
             if os.environ.get(flag):
                 extra.append("-D" + flag)
+        if os.environ.get("VTRACE_ABLATE"):  # timing experiments only (wrong results)
+            extra.append("-DVTRACE_ABLATE=" + os.environ["VTRACE_ABLATE"])
         cmd = [NVCC, *FLAGS, *extra, "-o", SO + ".tmp", *SOURCES]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -297,6 +297,9 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
 
   // chunk of iteration `it` (reverse time): k = K - 1 - it, t0 = 8 k; stage it mod NSTAGE
   auto load_iter = [&](int it) {  // lane 0 only
+#if defined(VTRACE_ABLATE) && VTRACE_ABLATE == 8
+    return;  // ablation: no logits loads
+#endif
     if (it >= it_end) return;
     const int stg = (it - it_begin) % CT_NSTAGE;
     const int t0 = (K - 1 - it) * CT_STEPS;
@@ -333,7 +336,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
   auto load_step = [&](int it, int off, StepIn& s) {
     const int t = (K - 1 - it) * CT_STEPS + tl;
     s.a = 0; s.r = 0.f; s.g = 0.f; s.v = 0.f; s.vn = 0.f;
+#if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 7 || VTRACE_ABLATE == 8)
+    if (false) {  // ablation: no per-step loads
+#else
     if (t < T && c < blen) {
+#endif
       s.a = __ldg(P.actions + off);
       s.r = __ldg(P.rew + off);
       s.g = __ldg(P.disc + off);
@@ -345,10 +352,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
 
   int st = 0;  // (it - it_begin) mod NSTAGE
   int off = off0;  // this iteration's row
-  // one chunk; `cur` holds its per-step inputs, `nxt` receives the next chunk's (two
-  // register sets used alternately: no copy that would wait on loads in flight)
+  // one chunk; `cur` holds its per-step inputs, `nxt` receives those of the chunk two
+  // ahead (three register sets in rotation: no copy that would wait on loads in flight)
   auto chunk = [&](const int it, const StepIn& cur, StepIn& nxt) {
-    if (it + 1 < it_end) load_step(it + 1, off - stepB, nxt);
+    // per-step inputs two chunks ahead (three register sets in rotation)
+    if (it + 2 < it_end) load_step(it + 2, off - 2 * stepB, nxt);
     const int t0 = (K - 1 - it) * CT_STEPS;
     const int tlen = min(CT_STEPS, T - t0);
     unsigned char* sb = base + (size_t)st * C.stage;
@@ -357,8 +365,10 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
     const LT* mrow = reinterpret_cast<const LT*>(sb + C.mu) + lane * A;
     const int a_raw = cur.a;
     const int a = min(max(a_raw, 0), A - 1);
+#if !(defined(VTRACE_ABLATE) && VTRACE_ABLATE == 8)
     mbar_wait(&wb[st], (phase_bits >> st) & 1u);
     phase_bits ^= 1u << st;
+#endif
 
     // ---- a3-a7: statistics of this lane's row ----------------------------------
     // Every lane computes its row; rows past the end of the unroll (the first
@@ -368,8 +378,23 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
     bool fin;
     [[maybe_unused]] CtStats<LT, (kFast ? A_CT : 2)> F;
     [[maybe_unused]] RowRegs<LT, A_CT> zp;
+#if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 1 || VTRACE_ABLATE == 5 || VTRACE_ABLATE == 6 || VTRACE_ABLATE == 7)
+    if constexpr (kFast) {  // ablation: no row statistics (loads only)
+      const uint32_t* zw = reinterpret_cast<const uint32_t*>(zrow);
+      const uint32_t* mw = reinterpret_cast<const uint32_t*>(mrow);
+      uint32_t acc = 0;
+#pragma unroll
+      for (int k = 0; k < A_CT / 2; ++k) {
+        acc ^= zw[k] ^ mw[k];
+        F.z[k] = make_float2(__uint_as_float(zw[k] << 16), 0.f);
+        F.e[k] = make_float2(1.f, 1.f);
+      }
+      F.m_p = __uint_as_float(acc & 0x3f000000u); F.sd_p = 0.f; F.ea_p = 1.f; F.S_p = 18.0;
+      F.S_m = 18.0; F.xa_p = 0.0; F.xa_m = 0.0; F.finite = true;
+#else
     if constexpr (kFast) {
       ct_stats_fast<LT, A_CT>(zrow, mrow, a, F);
+#endif
       m_p = F.m_p; sed_p = F.sd_p; ea_p = F.ea_p; S_p = F.S_p; S_m = F.S_m;
       xa_p = F.xa_p; xa_m = F.xa_m;
       fin = F.finite;
@@ -384,7 +409,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       fin = fin_p && fin_m;
     }
     // pi(a)/mu(a) = exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) S_mu / S_pi
+#if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 2 || VTRACE_ABLATE == 5 || VTRACE_ABLATE == 6 || VTRACE_ABLATE == 7)
+    const double ratio = 1.0 + (xa_p - xa_m) + (S_m - S_p);  // ablation: no exp64 / division
+#else
     const double ratio = exp64(xa_p - xa_m) * ddiv_pos(S_m, S_p);
+#endif
     const float rt = cur.r, gm = cur.g, Vt = cur.v, Vn = cur.vn;
     const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
     double dl = dmin_t(P.rho_bar, ratio) * td;                         // delta_t V
@@ -410,7 +439,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       dl = 0.0;  // identity map for steps past the end of the unroll
       gc = 1.0;
     }
+#if defined(VTRACE_ABLATE) && VTRACE_ABLATE == 8
+    if (false) {  // (garbage inputs)
+#else
     if (bad) {
+#endif
       const int row = off;
       if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
       if (!fin) record_bad(P.ws, row, VT_DATA_LOGITS);
@@ -430,7 +463,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       carry = cin[c];
     }
     double Gi = gc, Di = dl;
+#if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 3 || VTRACE_ABLATE == 5 || VTRACE_ABLATE == 6 || VTRACE_ABLATE == 7)
+    if (false)  // ablation: no scan
+#else
 #pragma unroll
+#endif
     for (int o = CT_COLS; o < 32; o <<= 1) {
       const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
       const bool in = lane + o < 32;  // beyond the chunk: identity map
@@ -447,8 +484,10 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       const int row = off;
       // pg_adv = rho_pg (r + gamma v_{t+1} - V) = rho_pg (td + gamma A_{t+1})
       const float pgr = (float)(dmin_t(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
+#if !(defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 7 || VTRACE_ABLATE == 8))
       if (P.vs) P.vs[row] = (float)((double)Vt + A_t);
       if (P.pg_adv) P.pg_adv[row] = pgr;
+#endif
       if constexpr (LOSS) {
         const float Ar = (float)A_t;
         const float za = Elem<LT>::get(zrow, a);
@@ -463,7 +502,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
           const float2 u1 = f2(CORR * inv_S), u0 = f2(inv_S * fmaf(-CORR, m_p, 1.f));
           const float2 ce2 = f2(ce), al2 = f2(alpha);
           float2 sq2 = f2(0.f);
+#if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 4 || VTRACE_ABLATE == 5 || VTRACE_ABLATE == 6 || VTRACE_ABLATE == 7)
+          if (false)  // ablation: no gradient loop
+#else
 #pragma unroll
+#endif
           for (int k = 0; k < A_CT / 2; ++k) {
             const float2 t2 = __ffma2_rn(ce2, F.z[k], al2);
             const float2 w2 = __ffma2_rn(u1, F.z[k], u0);
@@ -500,7 +543,9 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
         zrow[a] = store_cvt<LT>(d_a);
         sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
         const float dv = -cv * Ar;  // c_v (V - v)
+#if !(defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 7 || VTRACE_ABLATE == 8))
         P.dvalues[row] = dv;
+#endif
         acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)
         acc_v = fmaf(0.5f * Ar, Ar, acc_v);
         acc_H += lse - cshift;
@@ -508,7 +553,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
         acc_dv = fmaf(dv, dv, acc_dv);
       }
     }
+#if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 6 || VTRACE_ABLATE == 8)
+    if (false) {  // ablation: no gradient store
+#else
     if constexpr (LOSS) {
+#endif
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -529,11 +578,13 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
     off -= stepB;
     if (++st == CT_NSTAGE) st = 0;
   };
-  StepIn sA, sB;
+  StepIn sA, sB, sC;
   load_step(it_begin, off0, sA);
-  for (int it = it_begin; it < it_end; it += 2) {
-    chunk(it, sA, sB);
+  if (it_begin + 1 < it_end) load_step(it_begin + 1, off0 - stepB, sB);
+  for (int it = it_begin; it < it_end; it += 3) {
+    chunk(it, sA, sC);
     if (it + 1 < it_end) chunk(it + 1, sB, sA);
+    if (it + 2 < it_end) chunk(it + 2, sC, sB);
   }
   if (cout != nullptr) {  // hand the carry at this segment's first step on
     if (tl == 0) cout[c] = carry;
