@@ -46,7 +46,12 @@ def build(force: bool = False) -> str:
 class _Params(ctypes.Structure):
     _fields_ = [("rho_bar", ctypes.c_double), ("c_bar", ctypes.c_double),
                 ("pg_rho_bar", ctypes.c_double), ("lambda_", ctypes.c_double),
-                ("reward_mode", ctypes.c_int32)]
+                ("reward_mode", ctypes.c_int32), ("correction", ctypes.c_int32),
+                ("epsilon", ctypes.c_double), ("q_from_values", ctypes.c_int32)]
+
+
+# Section 5.2.2 off-policy correction variants
+CORR_VTRACE, CORR_NONE, CORR_EPSILON, CORR_ONE_STEP_IS = 0, 1, 2, 3
 
 
 class _Weights(ctypes.Structure):
@@ -81,10 +86,11 @@ class OracleError(RuntimeError):
         super().__init__(f"oracle status {code} (bad index {bad_index})")
 
 
-def _params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=REWARD_NONE):
+def _params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=REWARD_NONE,
+            correction=CORR_VTRACE, epsilon=1e-6, q_from_values=0):
     return _Params(float(rho_bar), float(c_bar),
                    float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
-                   int(reward_mode))
+                   int(reward_mode), int(correction), float(epsilon), int(q_from_values))
 
 
 def _ptr(a):

@@ -36,7 +36,33 @@ bool params_ok(const vto_params* p) {
   if (p->c_bar > p->rho_bar) return false;  // "we assume rho_bar >= c_bar", reading c6
   if (p->lambda_ < 0 || p->lambda_ > 1) return false;  // Remark 2, lambda in [0,1]
   if (p->reward_mode < 0 || p->reward_mode > 2) return false;
+  if (p->correction < VTO_CORR_VTRACE || p->correction > VTO_CORR_ONE_STEP_IS) return false;
+  if (p->correction == VTO_CORR_EPSILON && !(p->epsilon > 0 && std::isfinite(p->epsilon)))
+    return false;
+  if (p->q_from_values != 0 && p->q_from_values != 1) return false;
   return true;
+}
+
+// The weights each variant uses at one step, from the importance ratio pi/mu
+// (Section 5.2.2; readings r5-r7 in DESIGN.md):
+//   V-trace (4):        rho = min(rho_bar, ratio), c = lambda min(c_bar, ratio),
+//                       rho_pg = min(pg_rho_bar, ratio)
+//   No-correction (1):  "No off-policy correction": rho = 1, c = lambda, rho_pg = 1
+//   epsilon-corr. (2):  as no-correction (the epsilon enters the log in the PG term)
+//   1-step IS (3):      "No off-policy correction when optimising V(x)": rho = 1,
+//                       c = lambda; "multiply the advantage at each time step by the
+//                       corresponding importance weight": rho_pg = min(pg_rho_bar, ratio)
+void variant_weights(const vto_params* p, double ratio, double* rho, double* c,
+                     double* rho_pg) {
+  if (p->correction == VTO_CORR_VTRACE) {
+    *rho = std::min(p->rho_bar, ratio);
+    *c = p->lambda_ * std::min(p->c_bar, ratio);
+    *rho_pg = std::min(p->pg_rho_bar, ratio);
+  } else {
+    *rho = 1.0;
+    *c = p->lambda_;
+    *rho_pg = (p->correction == VTO_CORR_ONE_STEP_IS) ? std::min(p->pg_rho_bar, ratio) : 1.0;
+  }
 }
 
 // Records the data error with the smallest (row, kind).
@@ -72,6 +98,7 @@ bool row_logits_finite(const void* logits, int32_t dtype, int64_t row, int64_t A
 
 // Per-column V-trace given log importance ratios, per Section 4.1:
 //   rho_t = min(rho_bar, pi/mu), c_t = lambda * min(c_bar, pi/mu)
+//   (or the weights of a Section 5.2.2 variant, variant_weights above)
 //   delta_t V = rho_t (r_t + gamma_t V(x_{t+1}) - V(x_t))
 //   v_s = V(x_s) + delta_s V + gamma_s c_s (v_{s+1} - V(x_{s+1}))     (Remark 1)
 //   with v_T = V(x_T) = bootstrap (reading c2), gamma_t = discounts[t] (reading c1).
@@ -82,9 +109,7 @@ void vtrace_column(int64_t T, int64_t B, int64_t b, const double* lr, const doub
   std::vector<double> rho(T), c(T), rho_pg(T), Vn(T + 1);
   for (int64_t t = 0; t < T; ++t) {
     double ratio = std::exp(lr[t]);
-    rho[t] = std::min(p->rho_bar, ratio);
-    c[t] = p->lambda_ * std::min(p->c_bar, ratio);
-    rho_pg[t] = std::min(p->pg_rho_bar, ratio);
+    variant_weights(p, ratio, &rho[t], &c[t], &rho_pg[t]);
     Vn[t] = V[t];
   }
   Vn[T] = boot;
@@ -95,7 +120,8 @@ void vtrace_column(int64_t T, int64_t B, int64_t b, const double* lr, const doub
     v[t] = Vn[t] + delta + g[t] * c[t] * (v[t + 1] - Vn[t + 1]);
   }
   for (int64_t t = 0; t < T; ++t) {
-    double q = r[t] + g[t] * v[t + 1];
+    // q_s = r_s + gamma_s v_{s+1}, or r_s + gamma_s V(x_{s+1}) (App. E.3)
+    double q = r[t] + g[t] * (p->q_from_values ? Vn[t + 1] : v[t + 1]);
     vs_col[t] = v[t];
     adv_col[t] = rho_pg[t] * (q - Vn[t]);
     if (rho_col) rho_col[t] = rho[t];
@@ -253,13 +279,19 @@ int vtrace_oracle_loss_and_grad(int64_t T, int64_t B, int64_t A, int32_t dtype,
       log_softmax_row(target_logits, dtype, row, A, logp);
       double H = 0;
       for (int64_t j = 0; j < A; ++j) H -= std::exp(logp[j]) * logp[j];
-      L_pg += -adv[row] * logp[ac];
+      // epsilon-correction: log(pi(a) + eps) in the policy-gradient term (reading
+      // c11); its logit gradient is the plain one scaled by pi(a) / (pi(a) + eps)
+      const bool eps_corr = p->correction == VTO_CORR_EPSILON;
+      const double pa = std::exp(logp[ac]);
+      const double logpa = eps_corr ? std::log(pa + p->epsilon) : logp[ac];
+      const double wpg = eps_corr ? pa / (pa + p->epsilon) : 1.0;
+      L_pg += -adv[row] * logpa;
       double res = v[row] - (double)values[row];
       L_v += 0.5 * res * res;
       H_sum += H;
       for (int64_t j = 0; j < A; ++j) {
         double pj = std::exp(logp[j]);
-        double dz = adv[row] * (pj - (j == ac ? 1.0 : 0.0)) +
+        double dz = adv[row] * wpg * (pj - (j == ac ? 1.0 : 0.0)) +
                     w->entropy_cost * pj * (logp[j] + H);
         grad_target_logits[row * A + j] = dz;
         sq_dz += dz * dz;
@@ -267,8 +299,9 @@ int vtrace_oracle_loss_and_grad(int64_t T, int64_t B, int64_t A, int32_t dtype,
       double dv = w->baseline_cost * ((double)values[row] - v[row]);
       grad_values[row] = dv;
       sq_dv += dv * dv;
+      // the rho_t the variant uses in delta_t V; truncations counted for V-trace only (r6)
       sum_rho += rho[row];
-      if (std::exp(lr[row]) > p->rho_bar) n_clip += 1.0;
+      if (p->correction == VTO_CORR_VTRACE && std::exp(lr[row]) > p->rho_bar) n_clip += 1.0;
       if (vs) vs[row] = v[row];
       if (pg_advantages) pg_advantages[row] = adv[row];
     }
@@ -300,12 +333,13 @@ int vtrace_oracle_vs_eq1(int64_t T, int64_t B, const double* log_rhos, const dou
       for (int64_t t = s; t < T; ++t) {
         double disc_prod = 1.0, c_prod = 1.0;
         for (int64_t i = s; i < t; ++i) {
-          double ratio = std::exp(log_rhos[i * B + b]);
+          double rho_i, c_i, pg_i;
+          variant_weights(p, std::exp(log_rhos[i * B + b]), &rho_i, &c_i, &pg_i);
           disc_prod *= discounts[i * B + b];
-          c_prod *= p->lambda_ * std::min(p->c_bar, ratio);
+          c_prod *= c_i;
         }
-        double ratio_t = std::exp(log_rhos[t * B + b]);
-        double rho_t = std::min(p->rho_bar, ratio_t);
+        double rho_t, c_t, pg_t;
+        variant_weights(p, std::exp(log_rhos[t * B + b]), &rho_t, &c_t, &pg_t);
         double V_next = (t + 1 < T) ? values[(t + 1) * B + b] : bootstrap_value[b];
         double delta = rho_t * (rewards[t * B + b] + discounts[t * B + b] * V_next -
                                 values[t * B + b]);

@@ -16,6 +16,9 @@
  *     summed over batch and time, and their gradients w.r.t. the
  *     target logits and the values
  *   - reward transforms clip[-1,1] and optimistic asymmetric
+ *   - the off-policy correction variants of Section 5.2.2
+ *     (no-correction, epsilon-correction, 1-step IS) and the
+ *     q_s = r_s + gamma V(x_{s+1}) estimate of App. E.3
  *
  * Layout: time-major.  Logits are [T][B][A] (A fastest), per-step arrays are
  * [T][B], bootstrap is [B].  Logits are given as fp32 (dtype 0) or as raw
@@ -48,12 +51,22 @@ extern "C" {
 #define VTO_DATA_VALUE 4       /* non-finite value or bootstrap      */
 #define VTO_DATA_DISCOUNT 5    /* discount non-finite or not in [0,1] */
 
+/* Off-policy correction variants of Section 5.2.2. */
+#define VTO_CORR_VTRACE 0      /* 4. V-trace (Section 4)                          */
+#define VTO_CORR_NONE 1        /* 1. No-correction: rho = c = 1, unweighted PG    */
+#define VTO_CORR_EPSILON 2     /* 2. epsilon-correction: as 1, PG uses log(pi+eps) */
+#define VTO_CORR_ONE_STEP_IS 3 /* 3. 1-step IS: as 1 for V, PG weighted by rho_pg  */
+
 typedef struct {
   double rho_bar;     /* truncation of rho_t; +inf = none          */
   double c_bar;       /* truncation of c_t; must be <= rho_bar     */
   double pg_rho_bar;  /* truncation of the rho_s in the PG term    */
   double lambda_;     /* Remark 2, in [0, 1]                       */
   int32_t reward_mode;/* 0 none, 1 clip[-1,1], 2 asym tanh */
+  int32_t correction; /* VTO_CORR_* (P:410-416); 0 = V-trace               */
+  double epsilon;     /* epsilon-correction constant (1e-6)         */
+  int32_t q_from_values; /* 0: q_s = r_s + gamma v_{s+1};
+                            1: q_s = r_s + gamma V(x_{s+1}) (App. E.3) */
 } vto_params;
 
 typedef struct {

@@ -432,3 +432,141 @@ def test_param_errors():
     assert e.value.code == 4
     with pytest.raises(oracle.OracleError):
         oracle.from_logits(inp, lambda_=1.5)
+
+
+# --------------------------------------------------------------------------
+# Section 5.2.2 correction variants and the App. E.3 q estimate
+
+
+def _col_inputs(ex):
+    n = len(ex["rewards"])
+    g = np.full((n, 1), ex["gamma"])
+    r = np.array(ex["rewards"], float).reshape(n, 1)
+    V = np.array(ex["values"], float).reshape(n, 1)
+    boot = np.array([ex["bootstrap"]], float)
+    lr = np.log(np.array(ex["ratios"], float)).reshape(n, 1)
+    return lr, g, r, V, boot
+
+
+def test_spec_variant_examples():
+    """SPEC.md:90-91 worked examples: no-correction and 1-step IS on the same column."""
+    for ex in _load("spec_examples.json")["variants"]:
+        lr, g, r, V, boot = _col_inputs(ex)
+        vs, adv = oracle.vs_recursion(lr, g, r, V, boot, correction=ex["correction"])
+        np.testing.assert_allclose(vs[:, 0], ex["vs"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(adv[:, 0], ex["pg_advantages"], rtol=1e-12, atol=1e-12)
+        vs1 = oracle.vs_eq1(lr, g, r, V, boot, correction=ex["correction"])
+        np.testing.assert_allclose(vs1[:, 0], ex["vs"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_uncorrected_variants_are_nstep_bellman(seed):
+    """No-correction, epsilon-correction and 1-step IS use rho = c = 1 for the value
+    targets: v_s is the n-step Bellman target Eq.(2), written
+    out here, whatever the importance ratios; the V-trace targets differ off-policy."""
+    rng = np.random.default_rng(300 + seed)
+    inp = _batch(int(rng.integers(2, 10)), 4, 5, 300 + seed, p_done=0.15, lag=0.8)
+    T, B = inp["T"], inp["B"]
+    g = inp["discounts"].astype(np.float64)
+    r = inp["rewards"].astype(np.float64)
+    boot = inp["bootstrap_value"].astype(np.float64)
+    ref = np.zeros((T, B))
+    for b in range(B):
+        for s in range(T):
+            acc, w = 0.0, 1.0
+            for t in range(s, T):
+                acc += w * r[t, b]
+                w *= g[t, b]
+            ref[s, b] = acc + w * boot[b]
+    for corr in (oracle.CORR_NONE, oracle.CORR_EPSILON, oracle.CORR_ONE_STEP_IS):
+        o = oracle.from_logits(inp, correction=corr)
+        np.testing.assert_allclose(o["vs"], ref, rtol=1e-12, atol=1e-12)
+    assert np.max(np.abs(oracle.from_logits(inp)["vs"] - ref)) > 1e-3
+
+
+def test_variant_advantages_closed_forms():
+    """pg_adv per variant from its definition: no-/epsilon-correction the plain
+    advantage q - V; 1-step IS the same times min(pg_rho_bar, pi/mu); with
+    q_from_values, q_s = r_s + gamma_s V(x_{s+1}) for every variant."""
+    inp = _batch(9, 6, 4, 77, p_done=0.2, lag=0.8)
+    V = inp["values"].astype(np.float64)
+    Vn = np.concatenate([V[1:], inp["bootstrap_value"][None].astype(np.float64)], 0)
+    g = inp["discounts"].astype(np.float64)
+    r = inp["rewards"].astype(np.float64)
+    ratio = np.exp(oracle.from_logits(inp)["log_rhos"])
+    none = oracle.from_logits(inp, correction=oracle.CORR_NONE)
+    vs_next = np.concatenate([none["vs"][1:], inp["bootstrap_value"][None].astype(np.float64)], 0)
+    np.testing.assert_allclose(none["pg_advantages"], r + g * vs_next - V, rtol=1e-12, atol=1e-12)
+    eps = oracle.from_logits(inp, correction=oracle.CORR_EPSILON)
+    np.testing.assert_allclose(eps["pg_advantages"], none["pg_advantages"], rtol=0, atol=0)
+    for pg_bar in (1.0, 2.0):
+        one = oracle.from_logits(inp, correction=oracle.CORR_ONE_STEP_IS, pg_rho_bar=pg_bar)
+        np.testing.assert_allclose(one["pg_advantages"],
+                                   np.minimum(pg_bar, ratio) * none["pg_advantages"],
+                                   rtol=1e-12, atol=1e-12)
+    for corr in (0, 1, 2, 3):
+        q = oracle.from_logits(inp, correction=corr, q_from_values=1)
+        w = np.minimum(1.0, ratio) if corr in (0, 3) else 1.0
+        np.testing.assert_allclose(q["pg_advantages"], w * (r + g * Vn - V), rtol=1e-12,
+                                   atol=1e-12)
+        # the targets themselves do not depend on the q estimate
+        np.testing.assert_allclose(q["vs"], oracle.from_logits(inp, correction=corr)["vs"],
+                                   rtol=0, atol=0)
+
+
+def test_on_policy_all_variants_agree():
+    """pi = mu: every variant gives the same targets and advantages."""
+    inp = _batch(7, 5, 6, 91)
+    inp["behaviour_logits"] = inp["target_logits"].copy()
+    ref = oracle.from_logits(inp)
+    for corr in (1, 2, 3):
+        o = oracle.from_logits(inp, correction=corr)
+        np.testing.assert_allclose(o["vs"], ref["vs"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(o["pg_advantages"], ref["pg_advantages"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_epsilon_correction_gradient_finite_difference(seed):
+    """epsilon-correction loss -pg_adv log(pi(a) + eps) (reading c11): its logit
+    gradient against central differences.  rho = c = 1 under this variant, so v and
+    pg_adv do not depend on pi at all and the differences are exact up to rounding.
+    A large eps (0.05) makes the pi/(pi + eps) factor visible."""
+    rng = np.random.default_rng(seed)
+    inp = _batch(int(rng.integers(1, 4)), 3, 4, 70 + seed, lag=0.5)
+    inp["target_logits"] = (np.round(inp["target_logits"] * 256) / 256).astype(np.float32)
+    kw = dict(correction=oracle.CORR_EPSILON, epsilon=0.05, baseline_cost=0.5, entropy_cost=0.3)
+    grad = oracle.loss_and_grad(inp, **kw)["grad_target_logits"]
+    plain = oracle.loss_and_grad(inp, **dict(kw, correction=oracle.CORR_NONE))["grad_target_logits"]
+    assert np.max(np.abs(grad - plain)) > 1e-4
+    h = 2.0 ** -10
+    zf = inp["target_logits"]
+    for idx in np.ndindex(zf.shape):
+        zp = zf.copy(); zp[idx] += np.float32(h)
+        zm = zf.copy(); zm[idx] -= np.float32(h)
+        ip, im = dict(inp), dict(inp)
+        ip["target_logits"], im["target_logits"] = zp, zm
+        fd = (_total_loss(ip, **kw) - _total_loss(im, **kw)) / (2 * h)
+        assert abs(fd - grad[idx]) < 2e-6 * max(1.0, abs(grad[idx])), (idx, fd, grad[idx])
+
+
+def test_epsilon_to_zero_is_no_correction():
+    inp = _batch(5, 4, 6, 12)
+    a = oracle.loss_and_grad(inp, correction=oracle.CORR_EPSILON, epsilon=1e-300)
+    b = oracle.loss_and_grad(inp, correction=oracle.CORR_NONE)
+    np.testing.assert_allclose(a["grad_target_logits"], b["grad_target_logits"], rtol=1e-12,
+                               atol=1e-15)
+    np.testing.assert_allclose(a["partials"], b["partials"], rtol=1e-12)
+
+
+def test_variant_partials_and_param_checks():
+    """rho partials count the rho_t the variant uses (1 off V-trace, reading r6)."""
+    inp = _batch(6, 5, 4, 5, lag=0.8)
+    for corr in (1, 2, 3):
+        p = oracle.loss_and_grad(inp, correction=corr)["partials"]
+        assert p[6] == inp["T"] * inp["B"] and p[7] == 0
+    p = oracle.loss_and_grad(inp)["partials"]
+    assert p[6] < inp["T"] * inp["B"] and p[7] > 0
+    for bad in (dict(correction=4), dict(correction=-1), dict(correction=2, epsilon=0.0),
+                dict(correction=2, epsilon=float("nan")), dict(q_from_values=2)):
+        with pytest.raises(oracle.OracleError):
+            oracle.from_logits(inp, **bad)
