@@ -85,6 +85,23 @@ typedef enum {
 
 #define VT_MAX_ACTIONS 1024
 
+/* Off-policy correction (Section 5.2.2; readings r5-r7).
+ * Per step, from the importance ratio pi(a_t)/mu(a_t):
+ *   V-trace          rho = min(rho_bar, ratio), c = lambda min(c_bar, ratio),
+ *                    rho_pg = min(pg_rho_bar, ratio)                 (Section 4)
+ *   no-correction    rho = 1, c = lambda, rho_pg = 1
+ *   epsilon          as no-correction; the policy-gradient term uses
+ *                    log(pi(a) + epsilon)
+ *   1-step IS        rho = 1, c = lambda, rho_pg = min(pg_rho_bar, ratio) */
+typedef enum {
+  VT_CORRECTION_VTRACE = 0,
+  VT_CORRECTION_NONE = 1,
+  VT_CORRECTION_EPSILON = 2,
+  VT_CORRECTION_ONE_STEP_IS = 3
+} vt_correction;
+
+/* A zero-initialised struct with the three thresholds and lambda set is plain
+ * V-trace with q_s = r_s + gamma_s v_{s+1}. */
 typedef struct {
   float clip_rho_threshold;    /* rho_bar; +INFINITY = no truncation         */
   float clip_c_threshold;      /* c_bar; must be <= clip_rho_threshold       */
@@ -92,6 +109,11 @@ typedef struct {
                                   the paper uses rho_bar (reading c4)                */
   float lambda_;               /* Remark 2, in [0, 1]; 1 = plain V-trace     */
   int32_t reward_mode;         /* vt_reward_mode                                     */
+  int32_t correction;          /* vt_correction; 0 = V-trace                         */
+  float epsilon;               /* epsilon of VT_CORRECTION_EPSILON (1e-6);
+                                  must be finite and > 0 with that correction        */
+  int32_t q_from_values;       /* 0: q_s = r_s + gamma_s v_{s+1};
+                                  1: q_s = r_s + gamma_s V(x_{s+1}) (App. E.3) */
 } vt_vtrace_params;
 
 typedef struct {

@@ -1,6 +1,11 @@
-"""Builds libvtrace.so (the C-ABI library) in-tree with nvcc for sm_100a."""
+"""Builds libvtrace.so (the C-ABI library) in-tree with nvcc for sm_100a.
+
+Three objects (the look-back kernel + the C ABI; the column-task kernels for bf16
+and for fp32 logits) are compiled in parallel and linked into one shared library.
+"""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -8,35 +13,60 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libvtrace.so")
-SOURCES = [os.path.join(HERE, "csrc", "vtrace_api.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "vtrace_kernels.cuh"),
-                  os.path.join(HERE, "csrc", "vtrace_ct.cuh"),
-                  os.path.join(ROOT, "include", "vtrace.h")]
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = [os.path.join(CSRC, "vtrace_api.cu"), os.path.join(CSRC, "vtrace_ct_launch.cu")]
+# (source, object, defines): the column-task unit is compiled once per logits dtype
+UNITS = [(SOURCES[0], "vtrace_api.o", []),
+         (SOURCES[1], "vtrace_ct_bf16.o", ["-DVT_CT_PART=0"]),
+         (SOURCES[1], "vtrace_ct_f32.o", ["-DVT_CT_PART=1"])]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", f"-I{os.path.join(ROOT, 'include')}",
-         "-Xptxas", "-warn-spills"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+                f"-I{os.path.join(ROOT, 'include')}", "-Xptxas", "-warn-spills"]
+
+
+def _deps():
+    return (SOURCES + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+            + [os.path.join(ROOT, "include", "vtrace.h")])
 
 
 def needs_build() -> bool:
     if not os.path.exists(SO):
         return True
     t = os.path.getmtime(SO)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    return any(os.path.getmtime(d) > t for d in _deps())
+
+
+def _extra_defines():
+    extra = ["-DVTRACE_TIMING"] if os.environ.get("VTRACE_TIMING") else []
+    for flag in ("VTRACE_SUM_F64",):  # A/B experiments only
+        if os.environ.get(flag):
+            extra.append("-D" + flag)
+    if os.environ.get("VTRACE_ABLATE"):  # timing experiments only (wrong results)
+        extra.append("-DVTRACE_ABLATE=" + os.environ["VTRACE_ABLATE"])
+    return extra
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
-        extra = ["-DVTRACE_TIMING"] if os.environ.get("VTRACE_TIMING") else []
-        for flag in ("VTRACE_SUM_F64",):  # A/B experiments only
-            if os.environ.get(flag):
-                extra.append("-D" + flag)
-        if os.environ.get("VTRACE_ABLATE"):  # timing experiments only (wrong results)
-            extra.append("-DVTRACE_ABLATE=" + os.environ["VTRACE_ABLATE"])
-        cmd = [NVCC, *FLAGS, *extra, "-o", SO + ".tmp", *SOURCES]
+        extra = _extra_defines()
+        objs, procs = [], []
+        for src, oname, defs in UNITS:
+            obj = os.path.join(CSRC, oname)
+            cmd = [NVCC, *FLAGS, *extra, *defs, "-c", "-o", obj + ".tmp", src]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            procs.append((subprocess.Popen(cmd), cmd))
+            objs.append(obj)
+        for p, cmd in procs:
+            if p.wait() != 0:
+                raise subprocess.CalledProcessError(p.returncode, cmd)
+        for obj in objs:
+            os.replace(obj + ".tmp", obj)
+        link = [NVCC, *ARCH, "-shared", "-o", SO + ".tmp", *objs]
         if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+            print(" ".join(link), file=sys.stderr)
+        subprocess.check_call(link)
         os.replace(SO + ".tmp", SO)
     return SO
 

@@ -14,230 +14,10 @@
 
 #include "../../include/vtrace.h"
 #include "vtrace_kernels.cuh"
+#include "vtrace_rows.cuh"
+#include "vtrace_ct_host.h"
 
 namespace vtb200 {
-
-// ---------------------------------------------------------------------------
-// Row arithmetic.  Each thread owns one row
-// (t, b) of the unit for the whole unit: it keeps the target row in registers
-// from the statistics phase to the gradient epilogue.
-
-template <typename T>
-__device__ __forceinline__ T store_cvt(float x);
-template <>
-__device__ __forceinline__ float store_cvt<float>(float x) {
-  return x;
-}
-template <>
-__device__ __forceinline__ __nv_bfloat16 store_cvt<__nv_bfloat16>(float x) {
-  return __float2bfloat16_rn(x);
-}
-
-// A logits row held in registers as fp32 (compile-time A, unpacked once) or
-// read from shared memory (A_CT == 0).
-template <typename LT, int A_CT>
-struct RowRegs {
-  static constexpr bool kPacked = (sizeof(LT) == 2) && (A_CT % 2 == 0) && (A_CT > 0);
-  static constexpr int kN = A_CT > 0 ? A_CT : 1;
-  float z[kN];
-  const LT* src;
-  __device__ __forceinline__ void load(const LT* row) {
-    src = row;
-    if constexpr (kPacked) {
-      const uint32_t* p = reinterpret_cast<const uint32_t*>(row);
-#pragma unroll
-      for (int k = 0; k < A_CT / 2; ++k) {
-        const uint32_t x = p[k];
-        z[2 * k] = __uint_as_float(x << 16);
-        z[2 * k + 1] = __uint_as_float(x & 0xffff0000u);
-      }
-    } else if constexpr (A_CT > 0) {
-      if constexpr (sizeof(LT) == 4 && (A_CT % 2) == 0) {
-        const float2* p = reinterpret_cast<const float2*>(row);
-#pragma unroll
-        for (int k = 0; k < A_CT / 2; ++k) {
-          const float2 x = p[k];
-          z[2 * k] = x.x;
-          z[2 * k + 1] = x.y;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < A_CT; ++j) z[j] = Elem<LT>::get(row, j);
-      }
-    }
-  }
-  __device__ __forceinline__ float get(int j) const {  // j compile-time in unrolled loops
-    if constexpr (A_CT > 0) {
-      return z[j];
-    } else {
-      return Elem<LT>::get(src, j);
-    }
-  }
-};
-
-// Statistics of one logits row: m = max z, S = sum_j exp(z_j - m) (accurate to
-// ~1e-8 relative), xa = z_a - m (exact, fp64), ea_f = exp(z_a - m) (fp32; it is
-// exactly 1 when a is the argmax), and sed = sum_j e_j (z_j - m) (for the
-// entropy, fp32).
-template <typename LT, int A_CT, int MODE>
-__device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int a, float& m,
-                                          double& S, double& xa, float& ea_f, float& sed,
-                                          bool& finite) {
-  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);  // bf16: 8-bit significands
-  constexpr int NA = A_CT > 0 ? A_CT : 1;
-  const int nA = A_CT > 0 ? A_CT : A;
-  m = R.get(0);
-#pragma unroll
-  for (int j = 1; j < NA; ++j) m = fmaxf(m, R.get(j));
-  if constexpr (A_CT == 0)
-    for (int j = 1; j < nA; ++j) m = fmaxf(m, R.get(j));
-  // MUFU mode: e_j = 2^{y_j} with one rounding of the exponent y_j = (z_j - m) L'.
-  //  bf16 logits: y_j = fma(z_j, L16, -m L16) with a 16-bit log2 e, so z L16 and
-  //    m L16 are exact and the max term is exactly 2^0 = 1;
-  //  fp32 logits: y_j = fl(z_j - m) * L32 (the max term again exactly 1).
-  // The truncation of log2 e is a first-order factor 2^{(z_j - m)(log2 e - L')},
-  // applied once per row through sed = sum_j e_j (z_j - m).  The e_j are summed
-  // exactly: Fast2Sum in fp32 (s_hi starts at 1 >= every term), or, with
-  // -DVTRACE_SUM_F64, fp32 -> fp64 conversions and two fp64 accumulators.
-  constexpr float L16 = 1.44268798828125f;          // log2 e to 16 bits
-  constexpr float L32 = 1.44269502f;                // fp32(log2 e)
-  constexpr float CORR16 = 4.8884952e-06f;          // ln2 (log2 e - L16)
-  constexpr float CORR32 = 1.3349930e-08f;          // ln2 (log2 e - L32)
-  const float mL = m * L16;                         // exact for bf16 m
-  double S64a = 0.0;
-  [[maybe_unused]] double S64b = 0.0;
-  float s_hi = 1.f, s_lo = 0.f, sd = 0.f, chk = 0.f;
-  auto term = [&](float z, int j) {
-    if constexpr (MODE == EXP_F64) {
-      const double e = exp64((double)z - (double)m);
-      S64a += e;
-      sd = fmaf((float)e, z - m, sd);
-      chk = __fmaf_rn(z, 0.f, chk);
-    } else {
-      float e, d;
-      if constexpr (EXACT_DIFF) {
-        e = ex2_approx(fmaf(z, L16, -mL));
-        d = z - m;
-      } else {
-        d = z - m;
-        e = ex2_approx(d * L32);
-      }
-      sd = fmaf(e, d, sd);  // NaN if some z is inf/nan (0 * inf for -inf)
-#ifdef VTRACE_SUM_F64
-      if (j & 1) S64b += (double)e; else S64a += (double)e;
-#else
-      const float sum = s_hi + e;
-      s_lo += (s_hi - sum) + e;
-      s_hi = sum;
-#endif
-    }
-  };
-  if constexpr (A_CT > 0) {
-#pragma unroll
-    for (int j = 0; j < A_CT; ++j) term(R.get(j), j);
-  } else {
-    for (int j = 0; j < nA; ++j) term(R.get(j), j);
-  }
-  const float za = Elem<LT>::get(R.src, a);
-  xa = (double)za - (double)m;  // z_a - m, exact
-  ea_f = ex2_approx((za - m) * 1.44269504088896341f);  // exp(z_a - m), fp32 (exactly 1 at the max)
-  sed = sd;
-  if constexpr (MODE == EXP_F64) {
-    S = S64a;
-    finite = (chk == 0.f) && (m == m);
-  } else {
-#ifdef VTRACE_SUM_F64
-    const double S0 = S64a + S64b;
-#else
-    const double S0 = (double)(s_hi - 1.f) + (double)s_lo;
-#endif
-    S = S0 + (double)(sd * (EXACT_DIFF ? CORR16 : CORR32));
-    finite = isfinite(S) && isfinite(sd) && isfinite(m);
-  }
-}
-
-// Both policies' statistics of one row in one interleaved loop (MUFU mode, compile-
-// time A): four independent compensated-sum chains (2 per policy, even/odd j)
-// instead of two long serial ones, for instruction-level parallelism.
-struct RowStat {
-  float m, sed, ea_f;
-  double S, xa;
-  bool finite;
-};
-
-template <typename LT, int A_CT>
-__device__ __forceinline__ void row_stats2(const RowRegs<LT, A_CT>& Rp, const RowRegs<LT, A_CT>& Rm,
-                                           int a, RowStat& sp, RowStat& sm) {
-  static_assert(A_CT > 0, "compile-time A only");
-  constexpr bool EXACT_DIFF = (sizeof(LT) == 2);
-  constexpr float L16 = 1.44268798828125f;
-  constexpr float L32 = 1.44269502f;
-  constexpr float CORR = EXACT_DIFF ? 4.8884952e-06f : 1.3349930e-08f;
-  float mp = Rp.get(0), mm = Rm.get(0);
-#pragma unroll
-  for (int j = 1; j < A_CT; ++j) {
-    mp = fmaxf(mp, Rp.get(j));
-    mm = fmaxf(mm, Rm.get(j));
-  }
-  const float mLp = mp * L16, mLm = mm * L16;
-  float hp[2] = {1.f, 1.f}, lp[2] = {0.f, 0.f}, hm[2] = {1.f, 1.f}, lm[2] = {0.f, 0.f};
-  float sdp = 0.f, sdm = 0.f;
-#pragma unroll
-  for (int j = 0; j < A_CT; ++j) {
-    const int q = j & 1;
-    const float zp = Rp.get(j), zm = Rm.get(j);
-    float ep, em;
-    if constexpr (EXACT_DIFF) {
-      ep = ex2_approx(fmaf(zp, L16, -mLp));
-      em = ex2_approx(fmaf(zm, L16, -mLm));
-      sdp = fmaf(ep, zp, sdp);  // sum e z; (z - m) applied once per row below
-      sdm = fmaf(em, zm, sdm);
-    } else {
-      const float dp = zp - mp, dm = zm - mm;
-      ep = ex2_approx(dp * L32);
-      em = ex2_approx(dm * L32);
-      sdp = fmaf(ep, dp, sdp);
-      sdm = fmaf(em, dm, sdm);
-    }
-    const float np = hp[q] + ep, nm = hm[q] + em;  // Fast2Sum: h >= 1 >= e
-    lp[q] += (hp[q] - np) + ep;
-    lm[q] += (hm[q] - nm) + em;
-    hp[q] = np;
-    hm[q] = nm;
-  }
-  // each chain started at 1: h - 1 is exact
-  const float Sp_hi = (hp[0] - 1.f) + (hp[1] - 1.f), Sm_hi = (hm[0] - 1.f) + (hm[1] - 1.f);
-  if constexpr (EXACT_DIFF) {  // sum e (z - m) = sum e z - m sum e (entropy/correction only)
-    sdp = fmaf(-mp, Sp_hi, sdp);
-    sdm = fmaf(-mm, Sm_hi, sdm);
-  }
-  const double Sp = ((double)(hp[0] - 1.f) + (double)(hp[1] - 1.f)) +
-                    ((double)lp[0] + (double)lp[1]) + (double)(sdp * CORR);
-  const double Sm = ((double)(hm[0] - 1.f) + (double)(hm[1] - 1.f)) +
-                    ((double)lm[0] + (double)lm[1]) + (double)(sdm * CORR);
-  const float zap = Elem<LT>::get(Rp.src, a), zam = Elem<LT>::get(Rm.src, a);
-  sp.m = mp; sp.sed = sdp; sp.S = Sp; sp.xa = (double)zap - (double)mp;
-  sp.ea_f = ex2_approx((zap - mp) * 1.44269504088896341f);
-  sp.finite = isfinite(Sp) && isfinite(sdp) && isfinite(mp);
-  sm.m = mm; sm.sed = sdm; sm.S = Sm; sm.xa = (double)zam - (double)mm;
-  sm.ea_f = 1.f;
-  sm.finite = isfinite(Sm) && isfinite(sdm) && isfinite(mm);
-}
-
-__device__ __forceinline__ double reward_transform(float r, int mode) {
-  if (mode == 1) return (double)fminf(1.f, fmaxf(-1.f, r));  // P:944 (exact in fp32)
-  double x = (double)r;
-  if (mode == 2) {
-    double th = tanh(x);
-    return 0.3 * fmin(th, 0.0) + 5.0 * fmax(th, 0.0);
-  }
-  return x;
-}
-
-__device__ __forceinline__ void record_bad(WsHeader* ws, long long row, int kind) {
-  unsigned long long key = ((unsigned long long)row << 8) | (unsigned long long)kind;
-  atomicMin(&ws->status, key);
-}
 
 // ---------------------------------------------------------------------------
 // Shared-memory layout of one CTA (host and device agree on it).
@@ -259,8 +39,6 @@ struct Layout {
   size_t total;
 };
 
-__host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
-__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Every TMA destination is 128-byte aligned (a tiled cp.async.bulk.tensor into a
 // merely 16-byte aligned address faults with "misaligned address" on sm_100a);
@@ -401,7 +179,6 @@ __global__ void __launch_bounds__(NTHREADS, 4)
 
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
-  const float rho_bar_f = (float)P.rho_bar;
   // per-thread partial sums (fixed assignment of rows to threads: deterministic)
   float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
         acc_clip = 0.f;
@@ -513,8 +290,8 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           reinterpret_cast<float*>(smem + L.lse[par])[r] = lse;
           reinterpret_cast<float*>(smem + L.csh[par])[r] = fmaf(sed_p, inv_S, m_p);  // lse - H
           reinterpret_cast<float*>(smem + L.rest[par])[r] = (float)(S_p - (double)ea_p) * inv_S;
-          acc_rho += fminf(rho_bar_f, (float)ratio);
-          acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
+          acc_rho += (float)step_weights(P, ratio).rho;  // the rho_t in delta_t (reading r6)
+          acc_clip += (P.correction == VT_CORRECTION_VTRACE && ratio > P.rho_bar) ? 1.f : 0.f;
           if constexpr (!LOSS) {
             const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
             if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
@@ -574,8 +351,9 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         if (col_ok && s_beg + k < s_end) {
           const int q = (s_beg + k) * BC + c;
           const double ratio = ratio_s[q];
-          const double dl = dmin_t(P.rho_bar, ratio) * td_s[q];
-          const double gc = (double)g_t[q] * (P.lambda * dmin_t(P.c_bar, ratio));
+          const StepWeights sw = step_weights(P, ratio);  // (Section 5.2.2 variants)
+          const double dl = sw.rho * td_s[q];
+          const double gc = (double)g_t[q] * sw.c;
           adv_s[q] = dl;
           D = fma(gc, D, dl);
           G = gc * G;
@@ -648,7 +426,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
       for (int k = KSEG - 1; k >= 0; --k) {
         if (col_ok && s_beg + k < s_end) {
           const int q = (s_beg + k) * BC + c;
-          const double gc = (double)g_t[q] * (P.lambda * dmin_t(P.c_bar, ratio_s[q]));
+          const double gc = (double)g_t[q] * step_weights(P, ratio_s[q]).c;
           A_next = fma(gc, A_next, adv_s[q]);
           adv_s[q] = A_next;
         }
@@ -677,7 +455,9 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         // v_t = V(x_t) + A_t;  pg_adv_t = rho_pg (r_t + gamma_t v_{t+1} - V(x_t))
         //                              = rho_pg (td_t + gamma_t A_{t+1})
         const float vsr = (float)((double)Vt + A_t);
-        const float pgr = (float)(dmin_t(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
+        // (q_s = r_s + gamma V(x_{s+1}) instead with q_values: App. E.3)
+        const float pgr = (float)(step_weights(P, ratio).rho_pg *
+                                  (P.q_values ? td : fma((double)gm, A_n, td)));
         if (P.vs) P.vs[row] = vsr;
         if (P.pg_adv) P.pg_adv[row] = pgr;
         if constexpr (LOSS) {
@@ -693,7 +473,16 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           const float za = Elem<LT>::get(zrow, a);
           const float L2E = 1.44269504088896341f;
           const float lseL = lse * L2E;
-          const float alpha = fmaf(-ce, cshift, pgr);  // pg + c_e (z_j - cshift) = alpha + c_e z_j
+          // epsilon-correction (readings c11, r7): the policy-gradient term uses
+          // log(pi_a + eps); its logit gradient is the plain one times pi_a / (pi_a + eps)
+          float pge = pgr, logpa = za - lse;
+          if (P.correction == VT_CORRECTION_EPSILON) {
+            const float pa_e = ex2_approx((za - lse) * L2E);  // pi(a), relative accuracy
+            const float rr = P.eps / pa_e;
+            logpa = pa_e > 0.f ? (za - lse) + log1pf(rr) : logf(P.eps);
+            pge = pgr / (1.f + rr);
+          }
+          const float alpha = fmaf(-ce, cshift, pge);  // pg + c_e (z_j - cshift) = alpha + c_e z_j
           float sq = 0.f;
           // dz_j = pi_j (pg + c_e (log pi_j + H))   (j != a)
           if constexpr (RowRegs<LT, A_CT>::kPacked) {
@@ -726,13 +515,13 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           }
           // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
           const float d_wrong = ex2_approx(fmaf(za, L2E, -lseL)) * fmaf(ce, za, alpha);
-          const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
+          const float d_a = fmaf(-pge, rest, ce * pa * (za - cshift));
           zrow[a] = store_cvt<LT>(d_a);
           sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
           if (tim && i < P.timing_iters && tid == 0) tim[i * 8 + 6] = clock64();
           const float dv = -cv * Ar;  // c_v (V - v)
           P.dvalues[row] = dv;
-          acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)
+          acc_pg = fmaf(-pgr, logpa, acc_pg);  // -pg_adv log pi(a)  (log(pi(a) + eps))
           acc_v = fmaf(0.5f * Ar, Ar, acc_v);
           acc_H += lse - cshift;  // H = lse - (lse - H)
           acc_dz += sq;
@@ -835,7 +624,6 @@ __global__ void __launch_bounds__(NTHREADS, 4)
   }
 }
 
-#include "vtrace_ct.cuh"
 
 // ---------------------------------------------------------------------------
 // host side
@@ -845,7 +633,6 @@ struct Plan {
   size_t smem;
 };
 
-constexpr size_t kMaxSmem = 220 * 1024;
 constexpr int kMaxCtas = 4096;  // bound on the persistent grid (workspace sizing)
 
 // Tc (steps per unit) depends only on (T, A, dtype): at most 32 so that a
@@ -956,15 +743,6 @@ static bool encode_1d(CUtensorMap* m, const void* base, long long n, int box) {
   return r == CUDA_SUCCESS;
 }
 
-static int exp_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    // default: compensated MUFU exps; VTRACE_EXP_MODE=f64 selects fp64 exps (reference mode)
-    const char* e = getenv("VTRACE_EXP_MODE");
-    mode = (e && (e[0] == 'f' || e[0] == 'F' || e[0] == '0')) ? EXP_F64 : EXP_MUFU;
-  }
-  return mode;
-}
 
 template <typename LT, int A_CT, bool LOSS, bool TMA, int MODE>
 static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& plan,
@@ -1034,7 +812,7 @@ static vt_status dispatch(const Params& P, const TmaMaps& maps, const Plan& plan
 
 static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
-// ---- column-task kernel launch -------------------------------------------------------
+// ---- column-task kernel selection ----------------------------------------------------
 constexpr long long kCtMinTasks = 1024;  // >= ~7 warps per SM
 
 static bool ct_enabled() {  // VTRACE_KERNEL=lookback forces the look-back kernel (tests)
@@ -1046,93 +824,6 @@ static bool ct_enabled() {  // VTRACE_KERNEL=lookback forces the look-back kerne
   return v == 1;
 }
 
-static int num_sms_cached() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
-
-// Work split of the balanced kernel (one CTB_WARPS-warp CTA per SM): f whole tasks
-// per SM sub-partition (f4 = 4 f warps per CTA), the remaining R tasks cut into
-// `segs` time segments, `tpc` cut tasks per CTA; chosen to minimise the largest
-// per-sub-partition load f + ceil(segs tpc / 4) / segs.  False if it does not fit.
-static bool plan_balanced(CtParams& C, int S) {
-  const char* e = getenv("VTRACE_CT_BALANCED");  // "0": one-warp CTAs (A/B, tests)
-  if ((e && e[0] == '0') || S <= 0) return false;
-  if ((size_t)CTB_WARPS * C.warp_bytes > kMaxSmem) return false;  // e.g. fp32 logits, A = 18
-  const long long N = C.tasks;
-  const int f = (int)std::min<long long>(N / (4LL * S), 4);
-  if (f < 1) return false;
-  const long long R = N - 4LL * f * S;
-  if (R == 0) {
-    C.f4 = 4 * f; C.segs = 1; C.seg_len = C.K; C.tpc = 0;
-    return true;
-  }
-  const int tpc = (int)((R + S - 1) / S);
-  double best = 1e30;
-  int best_p = 0;
-  for (int segs = 1; segs <= 4 && segs <= C.K; ++segs) {
-    if (4 * f + segs * tpc > CTB_WARPS) continue;
-    const double load = f + (double)((segs * tpc + 3) / 4) / segs;
-    if (load < best - 1e-9) { best = load; best_p = segs; }
-  }
-  if (best_p == 0) return false;
-  C.f4 = 4 * f; C.segs = best_p; C.tpc = tpc;
-  C.seg_len = (C.K + best_p - 1) / best_p;
-  // every segment non-empty (a later one waits for the carry of an earlier one)
-  if ((best_p - 1) * C.seg_len >= C.K) return false;
-  return true;
-}
-
-template <typename LT, int A_CT, bool LOSS, int MODE>
-static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
-                               cudaStream_t st) {
-  const int S = num_sms_cached();
-  if (plan_balanced(C, S)) {
-    auto kern = vtrace_ctb_kernel<LT, A_CT, LOSS, MODE>;
-    const size_t smem = (size_t)CTB_WARPS * C.warp_bytes;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-    });
-    if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
-    kern<<<S, CTB_WARPS * 32, smem, st>>>(P, C, maps);
-    return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
-  }
-  auto kern = vtrace_ct_kernel<LT, A_CT, LOSS, MODE>;
-  const size_t smem = (size_t)CT_WARPS * C.warp_bytes;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-    // one-warp CTAs: occupancy is set by shared memory, so take the largest carveout
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      cudaSharedmemCarveoutMaxShared);
-  });
-  if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
-  const unsigned grid = (unsigned)((C.tasks + CT_WARPS - 1) / CT_WARPS);
-  kern<<<grid, CT_WARPS * 32, smem, st>>>(P, C, maps);
-  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
-}
-
-template <typename LT, bool LOSS>
-static vt_status ct_dispatch(const Params& P, const CtParams& C, const TmaMaps& maps,
-                             cudaStream_t st) {
-  if (exp_mode() == EXP_MUFU) {
-    if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_MUFU>(P, C, maps, st);
-    if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_MUFU>(P, C, maps, st);
-    return ct_launch_one<LT, 0, LOSS, EXP_MUFU>(P, C, maps, st);
-  }
-  if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_F64>(P, C, maps, st);
-  if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_F64>(P, C, maps, st);
-  return ct_launch_one<LT, 0, LOSS, EXP_F64>(P, C, maps, st);
-}
 
 static vt_status check_params(const vt_vtrace_params* p) {
   if (!p) return VT_ERR_INVALID_ARG;
@@ -1143,6 +834,11 @@ static vt_status check_params(const vt_vtrace_params* p) {
   if (cb > rb) return VT_ERR_PARAM;  // rho_bar >= c_bar
   if (l < 0.f || l > 1.f) return VT_ERR_PARAM;
   if (p->reward_mode < 0 || p->reward_mode > 2) return VT_ERR_PARAM;
+  if (p->correction < VT_CORRECTION_VTRACE || p->correction > VT_CORRECTION_ONE_STEP_IS)
+    return VT_ERR_PARAM;
+  if (p->correction == VT_CORRECTION_EPSILON && !(p->epsilon > 0.f && std::isfinite(p->epsilon)))
+    return VT_ERR_PARAM;
+  if (p->q_from_values != 0 && p->q_from_values != 1) return VT_ERR_PARAM;
   return VT_OK;
 }
 
@@ -1212,6 +908,9 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   P.pg_rho_bar = (double)prm->clip_pg_rho_threshold;
   P.lambda = (double)prm->lambda_;
   P.reward_mode = prm->reward_mode;
+  P.correction = prm->correction;
+  P.q_values = prm->q_from_values;
+  P.eps = prm->epsilon;
   P.c_v = loss ? (double)w->baseline_cost : 0.0;
   P.c_e = loss ? (double)w->entropy_cost : 0.0;
   unsigned char* wsb = static_cast<unsigned char*>(ws);
@@ -1280,10 +979,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
       C.group_recs = reinterpret_cast<TagRec*>(wsb + wl2.ct_group);
       C.group_count = reinterpret_cast<unsigned int*>(wsb + wl2.ct_count);
       C.top_count = C.group_count + (C.tasks + CT_GROUP - 1) / CT_GROUP;
-      if (dt == VT_BFLOAT16)
-        return loss ? ct_dispatch<__nv_bfloat16, true>(P, C, cm, st)
-                    : ct_dispatch<__nv_bfloat16, false>(P, C, cm, st);
-      return loss ? ct_dispatch<float, true>(P, C, cm, st) : ct_dispatch<float, false>(P, C, cm, st);
+      return ct_launch(dt == VT_BFLOAT16, loss, P, C, cm, st);
     }
   }
   if (dt == VT_BFLOAT16) {
@@ -1434,7 +1130,7 @@ const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_d
       int S = 0, dev = 0;  // the balanced split needs the SM count of the current device
       if (cudaGetDevice(&dev) == cudaSuccess &&
           cudaDeviceGetAttribute(&S, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-          plan_balanced(C, S))
+          ct_plan_balanced(C, S))
         return "vtrace_ctb_kernel";
       return "vtrace_ct_kernel";
     }

@@ -18,7 +18,12 @@
 // per-step a, r, gamma, V, V' by plain coalesced loads one chunk ahead.
 
 #pragma once
-// (included inside namespace vtb200 by vtrace_api.cu)
+#include <type_traits>
+
+#include "vtrace_kernels.cuh"
+#include "vtrace_rows.cuh"
+
+namespace vtb200 {
 
 constexpr int CT_COLS = 4;
 constexpr int CT_STEPS = 8;
@@ -276,12 +281,14 @@ struct CtAcc {
   float pg, v, H, dz, dv, rho, clip;
 };
 
+// GEN: the call uses a Section 5.2.2 variant or the App. E.3 q estimate (false:
+// plain V-trace, the variant logic compiled out).
 // One warp runs iterations [it_begin, it_end) of task `task` (4 trajectories): its
 // TMA ring (`base`, barriers `wb`), the per-step loads, a3-a11 per chunk.  The
 // carry A just after the segment comes from `cin` (another warp of the CTA, when
 // `cin_bar` completes) or is A_T = 0; the carry at the segment's first step goes
 // to `cout` / `cout_bar` for the warp running the earlier segment.
-template <typename LT, int A_CT, bool LOSS, int MODE>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
 __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const TmaMaps& maps,
                                        unsigned char* base, uint64_t* wb, const int lane,
                                        const int task, const int it_begin, const int it_end,
@@ -318,7 +325,6 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
 
   const float ce = (float)P.c_e;
   const float cv = (float)P.c_v;
-  const float rho_bar_f = (float)P.rho_bar;
   const int tl = lane >> 2, c = lane & 3;  // row (tl, c) of the [8 steps][4 columns] chunk
   const int stepB = CT_STEPS * B;  // T * B < 2^31 on this path (host check)
   float acc_pg = 0.f, acc_v = 0.f, acc_H = 0.f, acc_dz = 0.f, acc_dv = 0.f, acc_rho = 0.f,
@@ -416,16 +422,17 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
 #endif
     const float rt = cur.r, gm = cur.g, Vt = cur.v, Vn = cur.vn;
     const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
-    double dl = dmin_t(P.rho_bar, ratio) * td;                         // delta_t V
-    double gc = (double)gm * (P.lambda * dmin_t(P.c_bar, ratio));      // gamma_t c_t
+    const StepWeights sw = step_weights<GEN>(P, ratio);  // rho, c, rho_pg (Section 5.2.2)
+    double dl = sw.rho * td;                        // delta_t V
+    double gc = (double)gm * sw.c;                  // gamma_t c_t
     const float Sf = (float)S_p;
     const float inv_S = rcp_approx(Sf);
     const float lse = m_p + __logf(Sf);
     const float cshift = fmaf(sed_p, inv_S, m_p);  // lse - H
     const float rest = (float)(S_p - (double)ea_p) * inv_S;  // 1 - pi(a)
     if (row_ok) {
-      acc_rho += fminf(rho_bar_f, (float)ratio);
-      acc_clip += (ratio > P.rho_bar) ? 1.f : 0.f;
+      acc_rho += (float)sw.rho;  // the rho_t in delta_t (reading r6)
+      acc_clip += ((!GEN || P.correction == VT_CORRECTION_VTRACE) && ratio > P.rho_bar) ? 1.f : 0.f;
     }
     if (!LOSS && row_ok) {
       const int row = off;
@@ -483,7 +490,9 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
     if (row_ok) {
       const int row = off;
       // pg_adv = rho_pg (r + gamma v_{t+1} - V) = rho_pg (td + gamma A_{t+1})
-      const float pgr = (float)(dmin_t(P.pg_rho_bar, ratio) * fma((double)gm, A_n, td));
+      // (q_s = r_s + gamma V(x_{s+1}) instead with q_values: App. E.3)
+      const float pgr =
+          (float)(sw.rho_pg * ((GEN && P.q_values) ? td : fma((double)gm, A_n, td)));
 #if !(defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 7 || VTRACE_ABLATE == 8))
       if (P.vs) P.vs[row] = (float)((double)Vt + A_t);
       if (P.pg_adv) P.pg_adv[row] = pgr;
@@ -491,7 +500,16 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       if constexpr (LOSS) {
         const float Ar = (float)A_t;
         const float za = Elem<LT>::get(zrow, a);
-        const float alpha = fmaf(-ce, cshift, pgr);  // pg + c_e (z_j - cshift) = alpha + c_e z_j
+        // epsilon-correction (readings c11, r7): the policy-gradient term uses
+        // log(pi_a + eps); its logit gradient is the plain one times pi_a / (pi_a + eps)
+        float pge = pgr, logpa = za - lse;
+        if (GEN && P.correction == VT_CORRECTION_EPSILON) {
+          const float pa_e = ea_p * inv_S;  // pi(a), relative accuracy
+          const float rr = P.eps / pa_e;
+          logpa = pa_e > 0.f ? (za - lse) + log1pf(rr) : logf(P.eps);
+          pge = pgr / (1.f + rr);
+        }
+        const float alpha = fmaf(-ce, cshift, pge);  // pg + c_e (z_j - cshift) = alpha + c_e z_j
         float sq, d_wrong;
         // dz_j = pi_j (pg + c_e (log pi_j + H))   (j != a), in place over z
         if constexpr (kFast) {
@@ -539,14 +557,14 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
         }
         // the taken action: dz_a = -pg (1 - pi_a) + c_e pi_a (log pi_a + H)
         const float pa = 1.f - rest;
-        const float d_a = fmaf(-pgr, rest, ce * pa * (za - cshift));
+        const float d_a = fmaf(-pge, rest, ce * pa * (za - cshift));
         zrow[a] = store_cvt<LT>(d_a);
         sq = __fadd_rn(__fsub_rn(sq, __fmul_rn(d_wrong, d_wrong)), __fmul_rn(d_a, d_a));
         const float dv = -cv * Ar;  // c_v (V - v)
 #if !(defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 7 || VTRACE_ABLATE == 8))
         P.dvalues[row] = dv;
 #endif
-        acc_pg = fmaf(-pgr, za - lse, acc_pg);  // -pg_adv log pi(a)
+        acc_pg = fmaf(-pgr, logpa, acc_pg);  // -pg_adv log pi(a)  (log(pi(a) + eps))
         acc_v = fmaf(0.5f * Ar, Ar, acc_v);
         acc_H += lse - cshift;
         acc_dz += sq;
@@ -598,7 +616,7 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
   acc_out = CtAcc{acc_pg, acc_v, acc_H, acc_dz, acc_dv, acc_rho, acc_clip};
 }
 
-template <typename LT, int A_CT, bool LOSS, int MODE>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
 __global__ void __launch_bounds__(CT_WARPS * 32)
     vtrace_ct_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -608,7 +626,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
   if (task >= C.tasks) return;
   if (C.timing && lane == 0) C.timing[(size_t)task * 4 + 0] = gtimer();
   CtAcc acc;
-  ct_run<LT, A_CT, LOSS, MODE>(P, C, maps, smem, bar, lane, task, 0, C.K, nullptr, nullptr,
+  ct_run<LT, A_CT, LOSS, MODE, GEN>(P, C, maps, smem, bar, lane, task, 0, C.K, nullptr, nullptr,
                                nullptr, nullptr, acc);
   if constexpr (LOSS) {
     if (P.partials != nullptr) {
@@ -632,7 +650,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
 // -> the last CTA to finish adds the CTA sums in CTA order.
 constexpr int CTB_WARPS = 16;
 
-template <typename LT, int A_CT, bool LOSS, int MODE>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
 __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
     vtrace_ctb_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -675,7 +693,7 @@ __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
     const bool whole = slot >= nseg;
     const bool first = whole || p == 0, last = whole || p == C.segs - 1;
     // segment hand-over slots: slot j feeds slot j + 1 (same task)
-    ct_run<LT, A_CT, LOSS, MODE>(P, C, maps, smem + (size_t)w * C.warp_bytes, bar[w], lane,
+    ct_run<LT, A_CT, LOSS, MODE, GEN>(P, C, maps, smem + (size_t)w * C.warp_bytes, bar[w], lane,
                                  task, it_begin, it_end, first ? nullptr : hcarry[slot - 1],
                                  &hbar[first ? slot : slot - 1], last ? nullptr : hcarry[slot],
                                  &hbar[slot], acc);
@@ -744,3 +762,5 @@ __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
     }
   }
 }
+
+}  // namespace vtb200

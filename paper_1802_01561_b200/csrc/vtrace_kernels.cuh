@@ -88,6 +88,9 @@ struct Params {
   double rho_bar, c_bar, pg_rho_bar, lambda;
   double c_v, c_e;
   int reward_mode;
+  int correction;  // vt_correction (Section 5.2.2)
+  int q_values;    // 1: q_s = r_s + gamma V(x_{s+1}) (App. E.3)
+  float eps;       // epsilon-correction constant
   WsHeader* ws;
   TagRec* recs;          // [units][BC][RECS_PER_COL]
   double* cta_partials;
@@ -286,6 +289,28 @@ __device__ __forceinline__ double ddiv_pos(double a, double b) {
   r = fma(r, e, r);
   const double q = a * r;
   return fma(fma(-b, q, a), r, q);
+}
+
+// Weights of step t from its importance ratio under the call's correction
+// (Section 5.2.2; readings r5): rho for delta_t V, c for the trace,
+// rho_pg for the policy-gradient advantage.
+struct StepWeights {
+  double rho, c, rho_pg;
+};
+// GEN = false: the call is plain V-trace (a compile-time fast path, no variant logic).
+template <bool GEN = true>
+__device__ __forceinline__ StepWeights step_weights(const Params& P, double ratio) {
+  StepWeights w;
+  if (!GEN || P.correction == VT_CORRECTION_VTRACE) {
+    w.rho = dmin_t(P.rho_bar, ratio);
+    w.c = P.lambda * dmin_t(P.c_bar, ratio);
+    w.rho_pg = dmin_t(P.pg_rho_bar, ratio);
+  } else {
+    w.rho = 1.0;
+    w.c = P.lambda;
+    w.rho_pg = (P.correction == VT_CORRECTION_ONE_STEP_IS) ? dmin_t(P.pg_rho_bar, ratio) : 1.0;
+  }
+  return w;
 }
 
 // fp64 exp, argument clamped to [-700, 700].  Cody-Waite reduction

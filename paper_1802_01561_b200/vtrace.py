@@ -46,7 +46,12 @@ class VtraceError(RuntimeError):
 class _Params(ctypes.Structure):
     _fields_ = [("clip_rho_threshold", ctypes.c_float), ("clip_c_threshold", ctypes.c_float),
                 ("clip_pg_rho_threshold", ctypes.c_float), ("lambda_", ctypes.c_float),
-                ("reward_mode", ctypes.c_int32)]
+                ("reward_mode", ctypes.c_int32), ("correction", ctypes.c_int32),
+                ("epsilon", ctypes.c_float), ("q_from_values", ctypes.c_int32)]
+
+
+# vt_correction: Section 5.2.2 off-policy correction variants
+CORRECTION_VTRACE, CORRECTION_NONE, CORRECTION_EPSILON, CORRECTION_ONE_STEP_IS = 0, 1, 2, 3
 
 
 class _Weights(ctypes.Structure):
@@ -118,10 +123,11 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise TypeError(f"logits must be float32 or bfloat16, got {t.dtype}")
 
 
-def params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=0) -> _Params:
+def params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=0,
+           correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0) -> _Params:
     return _Params(float(rho_bar), float(c_bar),
                    float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
-                   int(reward_mode))
+                   int(reward_mode), int(correction), float(epsilon), int(q_from_values))
 
 
 def workspace_bytes(T: int, B: int, A: int, dtype_code: int) -> int:
@@ -167,7 +173,8 @@ def _contig(*ts):
 
 def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, values,
                 bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
-                reward_mode=0, workspace: Workspace | None = None, with_log_probs=True,
+                reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
+                workspace: Workspace | None = None, with_log_probs=True,
                 out: dict | None = None):
     """vtrace_from_logits.  Returns dict of fp32 [T, B] tensors: vs,
     pg_advantages (+ log_rhos, target_action_log_probs, behaviour_action_log_probs)."""
@@ -182,7 +189,7 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
         if with_log_probs:
             for k in ("log_rhos", "target_action_log_probs", "behaviour_action_log_probs"):
                 out[k] = torch.empty(T, B, dtype=torch.float32, device=dev)
-    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values)
     st = lib.vtrace_from_logits(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
         _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), _ptr(out["vs"]),
@@ -195,7 +202,8 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
 
 def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, values,
                   bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
-                  reward_mode=0, baseline_cost=0.5, entropy_cost=0.01,
+                  reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
+                  baseline_cost=0.5, entropy_cost=0.01,
                   workspace: Workspace | None = None, with_targets=True, out: dict | None = None):
     """vtrace_loss_and_grad.  Returns dict: grad_target_logits [T,B,A] (logits
     dtype), grad_values [T,B] fp32, partials [8] fp64 (device), and, if
@@ -213,7 +221,7 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
         if with_targets:
             out["vs"] = torch.empty(T, B, dtype=torch.float32, device=dev)
             out["pg_advantages"] = torch.empty(T, B, dtype=torch.float32, device=dev)
-    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values)
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
@@ -226,8 +234,9 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
 
 def loss_and_grad_from_host(host: dict, dev_in: dict, out: dict, workspace: Workspace,
                             partials_host: torch.Tensor, *, rho_bar=1.0, c_bar=1.0,
-                            pg_rho_bar=None, lambda_=1.0, reward_mode=0, baseline_cost=0.5,
-                            entropy_cost=0.01):
+                            pg_rho_bar=None, lambda_=1.0, reward_mode=0,
+                            correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
+                            baseline_cost=0.5, entropy_cost=0.01):
     """vtrace_loss_and_grad_from_host: ``host`` holds pinned CPU tensors of the
     seven inputs, ``dev_in`` same-shaped device staging tensors, ``out`` the
     device outputs (grad_target_logits, grad_values, partials);
@@ -238,7 +247,7 @@ def loss_and_grad_from_host(host: dict, dev_in: dict, out: dict, workspace: Work
     dev = dev_in["target_logits"].device
     names = ("behaviour_logits", "target_logits", "actions", "discounts", "rewards", "values",
              "bootstrap_value")
-    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values)
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad_from_host(
         T, B, A, dt, *[_ptr(host[k]) for k in names], *[_ptr(dev_in[k]) for k in names],

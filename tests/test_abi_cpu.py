@@ -89,6 +89,11 @@ def test_host_checks_return_before_launch(lib):
     assert _call_loss(lib, params=vt.params(lambda_=1.5)) == 4
     assert _call_loss(lib, params=vt.params(rho_bar=float("nan"))) == 4
     assert _call_loss(lib, params=vt.params(reward_mode=9)) == 4
+    assert _call_loss(lib, params=vt.params(correction=4)) == 4
+    assert _call_loss(lib, params=vt.params(correction=-1)) == 4
+    assert _call_loss(lib, params=vt.params(correction=2, epsilon=0.0)) == 4
+    assert _call_loss(lib, params=vt.params(correction=2, epsilon=float("inf"))) == 4
+    assert _call_loss(lib, params=vt.params(q_from_values=2)) == 4
     assert _call_loss(lib, weights=vt._Weights(float("inf"), 0.01)) == 4
     assert _call_loss(lib, ptr=0x10002) == 5         # VT_ERR_ALIGNMENT (fp32 data)
     assert _call_loss(lib, ws_bytes=16) == 6         # VT_ERR_WORKSPACE

@@ -331,3 +331,31 @@ def test_balanced_kernel_matches_one_warp_ctas(T, B, monkeypatch):
                                rtol=1e-6)
     ro = oracle.loss_and_grad(inp, reward_mode=1)["partials"]
     np.testing.assert_allclose(o["partials"].cpu().numpy()[:7], ro[:7], rtol=1e-5)
+
+
+VARIANT_SHAPES = [("atari", None), ("dmlab", None), ("large", dict(B=4096, T=40))]
+
+
+@pytest.mark.parametrize("corr", [1, 2, 3])
+@pytest.mark.parametrize("qv", [0, 1])
+@pytest.mark.parametrize("shape", range(len(VARIANT_SHAPES)))
+def test_parity_correction_variants(corr, qv, shape):
+    """Section 5.2.2 variants (no-correction, epsilon-correction, 1-step IS) and the
+    App. E.3 q estimate, on both kernels (look-back: atari/dmlab shapes; column-task:
+    the wide batch), against the oracle element by element."""
+    name, kw = VARIANT_SHAPES[shape]
+    inp = wl.make_inputs(name, seed=500 + 10 * corr + qv + 100 * shape, **(kw or {}))
+    lg, fl, ref_l, ref_f = run_both(inp, correction=corr, q_from_values=qv)
+    check_all(inp, lg, fl, ref_l, ref_f)
+
+
+@pytest.mark.parametrize("shape", range(len(VARIANT_SHAPES)))
+def test_parity_epsilon_correction_large_eps(shape):
+    """A large epsilon (0.05) makes the pi_a / (pi_a + eps) gradient factor and the
+    log(pi_a + eps) loss term visible in every row."""
+    name, kw = VARIANT_SHAPES[shape]
+    inp = wl.make_inputs(name, seed=900 + shape, **(kw or {}))
+    lg, fl, ref_l, ref_f = run_both(inp, correction=2, epsilon=0.05)
+    check_all(inp, lg, fl, ref_l, ref_f)
+    plain = oracle.loss_and_grad(inp, reward_mode=inp.get("reward_mode", 0), correction=1)
+    assert np.max(np.abs(plain["grad_target_logits"] - ref_l["grad_target_logits"])) > 1e-4
