@@ -47,7 +47,8 @@ class _Params(ctypes.Structure):
     _fields_ = [("rho_bar", ctypes.c_double), ("c_bar", ctypes.c_double),
                 ("pg_rho_bar", ctypes.c_double), ("lambda_", ctypes.c_double),
                 ("reward_mode", ctypes.c_int32), ("correction", ctypes.c_int32),
-                ("epsilon", ctypes.c_double), ("q_from_values", ctypes.c_int32)]
+                ("epsilon", ctypes.c_double), ("q_from_values", ctypes.c_int32),
+                ("behaviour_log_probs", ctypes.c_int32)]
 
 
 # Section 5.2.2 off-policy correction variants
@@ -87,10 +88,11 @@ class OracleError(RuntimeError):
 
 
 def _params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=REWARD_NONE,
-            correction=CORR_VTRACE, epsilon=1e-6, q_from_values=0):
+            correction=CORR_VTRACE, epsilon=1e-6, q_from_values=0, behaviour_log_probs=0):
     return _Params(float(rho_bar), float(c_bar),
                    float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
-                   int(reward_mode), int(correction), float(epsilon), int(q_from_values))
+                   int(reward_mode), int(correction), float(epsilon), int(q_from_values),
+                   int(behaviour_log_probs))
 
 
 def _ptr(a):
@@ -108,18 +110,30 @@ def _logits_array(x, dtype):
 
 
 def _inputs(inp):
+    """The seven input arrays.  With inp["behaviour_log_probs"] (a [T, B] array of
+    log mu(a_t)), that array replaces the behaviour logits (behaviour_log_probs=1)."""
     T, B, A = inp["T"], inp["B"], inp["A"]
     dt = inp["dtype"]
-    mu = _logits_array(inp["behaviour_logits"], dt)
+    if inp.get("behaviour_log_probs") is not None:
+        mu = np.ascontiguousarray(inp["behaviour_log_probs"], dtype=np.float32)
+        assert mu.size == T * B
+    else:
+        mu = _logits_array(inp["behaviour_logits"], dt)
     pi = _logits_array(inp["target_logits"], dt)
     a = np.ascontiguousarray(inp["actions"], dtype=np.int32)
     g = np.ascontiguousarray(inp["discounts"], dtype=np.float32)
     r = np.ascontiguousarray(inp["rewards"], dtype=np.float32)
     V = np.ascontiguousarray(inp["values"], dtype=np.float32)
     boot = np.ascontiguousarray(inp["bootstrap_value"], dtype=np.float32)
-    assert mu.size == T * B * A and pi.size == T * B * A and a.size == T * B
+    assert pi.size == T * B * A and a.size == T * B
     assert boot.size == B
     return T, B, A, dt, (mu, pi, a, g, r, V, boot)
+
+
+def _mu_mode(inp, params):
+    if inp.get("behaviour_log_probs") is not None:
+        return dict(params, behaviour_log_probs=1)
+    return params
 
 
 def from_logits(inp, check=True, **params):
@@ -133,7 +147,7 @@ def from_logits(inp, check=True, **params):
            ("vs", "pg_advantages", "log_rhos", "target_action_log_probs",
             "behaviour_action_log_probs")}
     bad = ctypes.c_int64(-1)
-    p = _params(**params)
+    p = _params(**_mu_mode(inp, params))
     st = lib.vtrace_oracle_from_logits(
         T, B, A, dt, *[_ptr(x) for x in arrs], ctypes.byref(p),
         _ptr(out["vs"]), _ptr(out["pg_advantages"]), _ptr(out["log_rhos"]),
@@ -157,7 +171,7 @@ def loss_and_grad(inp, baseline_cost=0.5, entropy_cost=0.01, check=True, **param
     vs = np.zeros((T, B), np.float64)
     adv = np.zeros((T, B), np.float64)
     bad = ctypes.c_int64(-1)
-    p = _params(**params)
+    p = _params(**_mu_mode(inp, params))
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_oracle_loss_and_grad(
         T, B, A, dt, *[_ptr(x) for x in arrs], ctypes.byref(p), ctypes.byref(w),

@@ -40,6 +40,7 @@ bool params_ok(const vto_params* p) {
   if (p->correction == VTO_CORR_EPSILON && !(p->epsilon > 0 && std::isfinite(p->epsilon)))
     return false;
   if (p->q_from_values != 0 && p->q_from_values != 1) return false;
+  if (p->behaviour_log_probs != 0 && p->behaviour_log_probs != 1) return false;
   return true;
 }
 
@@ -148,8 +149,10 @@ int run_targets(int64_t T, int64_t B, int64_t A, int32_t dtype, const void* mu_l
       const int64_t row = t * B + b;
       int32_t a = actions[row];
       if (a < 0 || a >= A) bad.hit(row, VTO_DATA_ACTION);
+      const bool mu_lp = p->behaviour_log_probs != 0;  // mu given as log mu(a_t) [T][B]
       if (!row_logits_finite(pi_logits, dtype, row, A) ||
-          !row_logits_finite(mu_logits, dtype, row, A))
+          (mu_lp ? !std::isfinite(((const float*)mu_logits)[row])
+                 : !row_logits_finite(mu_logits, dtype, row, A)))
         bad.hit(row, VTO_DATA_LOGITS);
       if (!std::isfinite(rewards[row])) bad.hit(row, VTO_DATA_REWARD);
       if (!std::isfinite(values[row])) bad.hit(row, VTO_DATA_VALUE);
@@ -157,9 +160,13 @@ int run_targets(int64_t T, int64_t B, int64_t A, int32_t dtype, const void* mu_l
         bad.hit(row, VTO_DATA_DISCOUNT);
       int32_t ac = a < 0 ? 0 : (a >= A ? (int32_t)(A - 1) : a);
       log_softmax_row(pi_logits, dtype, row, A, logp);
-      log_softmax_row(mu_logits, dtype, row, A, logm);
       lp[row] = logp[ac];                 // log pi(a_t|x_t)
-      lm[row] = logm[ac];                 // log mu(a_t|x_t)
+      if (mu_lp) {
+        lm[row] = (double)((const float*)mu_logits)[row];  // log mu(a_t|x_t), given
+      } else {
+        log_softmax_row(mu_logits, dtype, row, A, logm);
+        lm[row] = logm[ac];               // log mu(a_t|x_t)
+      }
       lr[row] = lp[row] - lm[row];        // log(pi/mu)
       rew[row] = vtrace_oracle_reward_transform((double)rewards[row], p->reward_mode);
     }

@@ -67,6 +67,10 @@ typedef struct {
   double epsilon;     /* epsilon-correction constant (1e-6)         */
   int32_t q_from_values; /* 0: q_s = r_s + gamma v_{s+1};
                             1: q_s = r_s + gamma V(x_{s+1}) (App. E.3) */
+  int32_t behaviour_log_probs; /* 0: behaviour_logits is [T][B][A] mu logits;
+                                  1: it is log mu(a_t|x_t) [T][B] fp32 (the actors'
+                                  "policy distributions" reduced to the taken action,
+                                  P:152)                        */
 } vto_params;
 
 typedef struct {

@@ -570,3 +570,58 @@ def test_variant_partials_and_param_checks():
                 dict(correction=2, epsilon=float("nan")), dict(q_from_values=2)):
         with pytest.raises(oracle.OracleError):
             oracle.from_logits(inp, **bad)
+
+
+# --------------------------------------------------------------------------
+# behaviour given as log mu(a_t) [T, B]
+
+
+def test_spec_target_examples_with_behaviour_log_probs():
+    """SPEC.md:74-76 worked targets with mu(a_t) given directly: pi(a) = ratio / 2 on a
+    2-action row with pi = (ratio/2, 1 - ratio/2), and log mu(a) = log(1/2)."""
+    for ex in _load("spec_examples.json")["targets"]:
+        n = len(ex["rewards"])
+        zp, _ = _logits_for_ratios(ex["ratios"])
+        g = np.full((n, 1), ex["gamma"], np.float32)
+        inp = dict(T=n, B=1, A=2, dtype=0, target_logits=zp,
+                   behaviour_log_probs=np.full((n, 1), math.log(0.5), np.float32),
+                   actions=np.zeros((n, 1), np.int32),
+                   rewards=np.array(ex["rewards"], np.float32).reshape(n, 1),
+                   values=np.array(ex["values"], np.float32).reshape(n, 1),
+                   bootstrap_value=np.array([ex["bootstrap"]], np.float32), discounts=g)
+        o = oracle.from_logits(inp)
+        np.testing.assert_allclose(o["vs"][:, 0], ex["vs"], rtol=2e-7, atol=2e-7)
+        np.testing.assert_allclose(o["behaviour_action_log_probs"][:, 0], math.log(0.5), rtol=1e-7)
+        if "pg_advantages" in ex:
+            np.testing.assert_allclose(o["pg_advantages"][:, 0], ex["pg_advantages"], rtol=2e-7,
+                                       atol=2e-7)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_behaviour_log_probs_match_logits_mode(seed):
+    """Given log mu(a_t) computed from the behaviour logits by an independent
+    (numpy, fp64) log-softmax and rounded to fp32, every output matches the
+    logits-mode oracle to the fp32 rounding of log mu."""
+    inp = _batch(7, 5, 6, 700 + seed, lag=0.6)
+    zm = inp["behaviour_logits"].astype(np.float64)
+    lse = np.log(np.sum(np.exp(zm - zm.max(-1, keepdims=True)), -1)) + zm.max(-1)
+    a = inp["actions"]
+    lmu = (np.take_along_axis(zm, a[..., None], -1)[..., 0] - lse).astype(np.float32)
+    lp_inp = dict(inp, behaviour_log_probs=lmu)
+    for corr in (0, 3):
+        ref = oracle.loss_and_grad(inp, correction=corr)
+        got = oracle.loss_and_grad(lp_inp, correction=corr)
+        for k in ("vs", "pg_advantages", "grad_values", "grad_target_logits"):
+            np.testing.assert_allclose(got[k], ref[k], rtol=1e-6, atol=1e-6)
+        # (the total loss is a difference of the other terms: absolute tolerance)
+        np.testing.assert_allclose(got["partials"][:6], ref["partials"][:6], rtol=1e-6, atol=2e-5)
+    o = oracle.from_logits(lp_inp)
+    np.testing.assert_array_equal(o["behaviour_action_log_probs"], lmu.astype(np.float64))
+
+
+def test_behaviour_log_probs_data_error():
+    inp = _batch(4, 3, 5, 7)
+    lmu = np.full((4, 3), -1.0, np.float32)
+    lmu[2, 1] = np.nan
+    o = oracle.from_logits(dict(inp, behaviour_log_probs=lmu), check=False)
+    assert o["status"] == 100 + 2 and o["bad_index"] == 2 * 3 + 1
