@@ -114,6 +114,11 @@ typedef struct {
                                   must be finite and > 0 with that correction        */
   int32_t q_from_values;       /* 0: q_s = r_s + gamma_s v_{s+1};
                                   1: q_s = r_s + gamma_s V(x_{s+1}) (App. E.3) */
+  int32_t behaviour_log_probs; /* 0: behaviour_policy_logits is mu's [T][B][A] logits;
+                                  1: it is log mu(a_t|x_t) [T][B] fp32 (the actors ship
+                                  only the taken action's log-probability; SURVEY 8(f)
+                                  NEXT #2), 4-byte aligned; logits_dtype still gives
+                                  the target logits' dtype                           */
 } vt_vtrace_params;
 
 typedef struct {

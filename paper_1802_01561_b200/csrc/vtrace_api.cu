@@ -47,7 +47,7 @@ __host__ __device__ inline Layout make_layout(int nrow, int A, int elem) {
   Layout L;
   size_t off = 0;
   L.pi = off;   off = a128(off + (size_t)nrow * A * elem);
-  L.mu = off;   off = a128(off + (size_t)nrow * A * elem);
+  L.mu = off;   off = a128(off + std::max((size_t)nrow * A * elem, (size_t)nrow * 4));
   L.a = off;    off = a128(off + (size_t)nrow * 4);
   L.r = off;    off = a128(off + (size_t)nrow * 4);
   L.g = off;    off = a128(off + (size_t)nrow * 4);
@@ -117,7 +117,9 @@ struct Unit {
 //                    place over z^pi, then one TMA store
 // so the latency-bound recursion overlaps the row arithmetic of the next unit.
 
-template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE>
+// GEN: the call uses a Section 5.2.2 variant, the App. E.3 q estimate or behaviour
+// log-probs (false: plain V-trace from logits, that logic compiled out).
+template <typename LT, int A_CT, bool LOSS, bool USE_TMA, int MODE, bool GEN>
 __global__ void __launch_bounds__(NTHREADS, 4)
     vtrace_fused_kernel(const Params P, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -161,12 +163,14 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         U.set((int)blockIdx.x + i * stride, P);
         const int st = i % NSTAGE;
         unsigned char* sb = smem + (size_t)st * L.stage;
-        const uint32_t bytes = (uint32_t)(2 * (size_t)nrow * A * sizeof(LT) +
+        const uint32_t bytes = (uint32_t)((size_t)nrow * A * sizeof(LT) +
+                                          ((GEN && P.mu_lp) ? (size_t)nrow * 4
+                                                            : (size_t)nrow * A * sizeof(LT)) +
                                           3 * (size_t)nrow * 4 + (size_t)(nrow + BC) * 4 + BC * 4);
         mbar_expect_tx(&bar[st], bytes);
         const int xb = (int)(U.b0 * A);
         tma_load_2d(sb + L.pi, &maps.pi, xb, U.t0, &bar[st]);
-        tma_load_2d(sb + L.mu, &maps.mu, xb, U.t0, &bar[st]);
+        tma_load_2d(sb + L.mu, &maps.mu, (GEN && P.mu_lp) ? (int)U.b0 : xb, U.t0, &bar[st]);
         tma_load_2d(sb + L.a, &maps.a, (int)U.b0, U.t0, &bar[st]);
         tma_load_2d(sb + L.r, &maps.r, (int)U.b0, U.t0, &bar[st]);
         tma_load_2d(sb + L.g, &maps.g, (int)U.b0, U.t0, &bar[st]);
@@ -230,10 +234,10 @@ __global__ void __launch_bounds__(NTHREADS, 4)
             if (tl < U.tlen && bl < U.blen) {
               const long long gi = (((long long)(U.t0 + tl)) * B + U.b0 + bl) * A + j;
               zp = gpi[gi];
-              zm = gmu[gi];
+              if (!(GEN && P.mu_lp)) zm = gmu[gi];
             }
             wpi[k] = zp;
-            wmu[k] = zm;
+            if (!(GEN && P.mu_lp)) wmu[k] = zm;
           }
           for (int k = tid; k < nrow + BC; k += NROWTHREADS) {
             const int tl = k / BC, bl = k - tl * BC;
@@ -242,6 +246,8 @@ __global__ void __launch_bounds__(NTHREADS, 4)
             const long long gi = t * B + U.b0 + bl;
             if (k < nrow) {
               const bool okr = ok && tl < U.tlen;
+              if (GEN && P.mu_lp)  // log mu(a_t) in the mu region
+                reinterpret_cast<float*>(wmu)[k] = okr ? reinterpret_cast<const float*>(P.mu)[gi] : 0.f;
               wa[k] = okr ? P.actions[gi] : 0;
               wr[k] = okr ? P.rew[gi] : 0.f;
               wg[k] = okr ? P.disc[gi] : 0.f;
@@ -268,7 +274,13 @@ __global__ void __launch_bounds__(NTHREADS, 4)
             zp.load(pi_t + (size_t)r * A);
             row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, xa_p, ea_p, sed_p, fin_p);
           }
-          {
+          if (GEN && P.mu_lp) {  // behaviour as log mu(a_t): ratio = pi(a) / exp(log mu(a))
+            const float lmu = reinterpret_cast<const float*>(mu_t)[r];
+            xa_m = (double)lmu;
+            S_m = 1.0;
+            fin_m = isfinite(lmu);
+            m_m = ea_m = sed_m = 0.f;
+          } else {
             RowRegs<LT, A_CT> zm;
             zm.load(mu_t + (size_t)r * A);
             row_stats<LT, A_CT, MODE>(zm, A, a, m_m, S_m, xa_m, ea_m, sed_m, fin_m);
@@ -290,8 +302,9 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           reinterpret_cast<float*>(smem + L.lse[par])[r] = lse;
           reinterpret_cast<float*>(smem + L.csh[par])[r] = fmaf(sed_p, inv_S, m_p);  // lse - H
           reinterpret_cast<float*>(smem + L.rest[par])[r] = (float)(S_p - (double)ea_p) * inv_S;
-          acc_rho += (float)step_weights(P, ratio).rho;  // the rho_t in delta_t (reading r6)
-          acc_clip += (P.correction == VT_CORRECTION_VTRACE && ratio > P.rho_bar) ? 1.f : 0.f;
+          acc_rho += (float)step_weights<GEN>(P, ratio).rho;  // the rho_t in delta_t (r6)
+          acc_clip += ((!GEN || P.correction == VT_CORRECTION_VTRACE) && ratio > P.rho_bar) ? 1.f
+                                                                                        : 0.f;
           if constexpr (!LOSS) {
             const long long row = (long long)(U.t0 + tl) * B + U.b0 + bl;
             if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
@@ -351,7 +364,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         if (col_ok && s_beg + k < s_end) {
           const int q = (s_beg + k) * BC + c;
           const double ratio = ratio_s[q];
-          const StepWeights sw = step_weights(P, ratio);  // (Section 5.2.2 variants)
+          const StepWeights sw = step_weights<GEN>(P, ratio);  // (Section 5.2.2 variants)
           const double dl = sw.rho * td_s[q];
           const double gc = (double)g_t[q] * sw.c;
           adv_s[q] = dl;
@@ -426,7 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
       for (int k = KSEG - 1; k >= 0; --k) {
         if (col_ok && s_beg + k < s_end) {
           const int q = (s_beg + k) * BC + c;
-          const double gc = (double)g_t[q] * step_weights(P, ratio_s[q]).c;
+          const double gc = (double)g_t[q] * step_weights<GEN>(P, ratio_s[q]).c;
           A_next = fma(gc, A_next, adv_s[q]);
           adv_s[q] = A_next;
         }
@@ -456,8 +469,8 @@ __global__ void __launch_bounds__(NTHREADS, 4)
         //                              = rho_pg (td_t + gamma_t A_{t+1})
         const float vsr = (float)((double)Vt + A_t);
         // (q_s = r_s + gamma V(x_{s+1}) instead with q_values: App. E.3)
-        const float pgr = (float)(step_weights(P, ratio).rho_pg *
-                                  (P.q_values ? td : fma((double)gm, A_n, td)));
+        const float pgr = (float)(step_weights<GEN>(P, ratio).rho_pg *
+                                  ((GEN && P.q_values) ? td : fma((double)gm, A_n, td)));
         if (P.vs) P.vs[row] = vsr;
         if (P.pg_adv) P.pg_adv[row] = pgr;
         if constexpr (LOSS) {
@@ -476,7 +489,7 @@ __global__ void __launch_bounds__(NTHREADS, 4)
           // epsilon-correction (readings c11, r7): the policy-gradient term uses
           // log(pi_a + eps); its logit gradient is the plain one times pi_a / (pi_a + eps)
           float pge = pgr, logpa = za - lse;
-          if (P.correction == VT_CORRECTION_EPSILON) {
+          if (GEN && P.correction == VT_CORRECTION_EPSILON) {
             const float pa_e = ex2_approx((za - lse) * L2E);  // pi(a), relative accuracy
             const float rr = P.eps / pa_e;
             logpa = pa_e > 0.f ? (za - lse) + log1pf(rr) : logf(P.eps);
@@ -744,10 +757,10 @@ static bool encode_1d(CUtensorMap* m, const void* base, long long n, int box) {
 }
 
 
-template <typename LT, int A_CT, bool LOSS, bool TMA, int MODE>
+template <typename LT, int A_CT, bool LOSS, bool TMA, int MODE, bool GEN>
 static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& plan,
                             cudaStream_t st) {
-  auto kern = vtrace_fused_kernel<LT, A_CT, LOSS, TMA, MODE>;
+  auto kern = vtrace_fused_kernel<LT, A_CT, LOSS, TMA, MODE, GEN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   static int num_sms = 0;
@@ -789,25 +802,34 @@ static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& pl
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
-template <typename LT, bool LOSS, bool TMA, int MODE>
+template <typename LT, bool LOSS, bool TMA, int MODE, bool GEN>
 static vt_status dispatch_a(const Params& P, const TmaMaps& maps, const Plan& plan,
                             cudaStream_t st) {
   if constexpr (TMA) {
-    if (P.A == 18) return launch_one<LT, 18, LOSS, TMA, MODE>(P, maps, plan, st);
-    if (P.A == 9) return launch_one<LT, 9, LOSS, TMA, MODE>(P, maps, plan, st);
+    if (P.A == 18) return launch_one<LT, 18, LOSS, TMA, MODE, GEN>(P, maps, plan, st);
+    if (P.A == 9) return launch_one<LT, 9, LOSS, TMA, MODE, GEN>(P, maps, plan, st);
   }
-  return launch_one<LT, 0, LOSS, TMA, MODE>(P, maps, plan, st);
+  return launch_one<LT, 0, LOSS, TMA, MODE, GEN>(P, maps, plan, st);
+}
+
+template <typename LT, bool LOSS, int MODE, bool GEN>
+static vt_status dispatch_t(const Params& P, const TmaMaps& maps, const Plan& plan, bool tma,
+                            cudaStream_t st) {
+  return tma ? dispatch_a<LT, LOSS, true, MODE, GEN>(P, maps, plan, st)
+             : dispatch_a<LT, LOSS, false, MODE, GEN>(P, maps, plan, st);
 }
 
 template <typename LT, bool LOSS>
 static vt_status dispatch(const Params& P, const TmaMaps& maps, const Plan& plan, bool tma,
                           cudaStream_t st) {
+  // plain V-trace from logits takes the instantiation with the GEN logic compiled out
+  // (MUFU mode; the fp64 reference mode always uses the general one)
+  const bool gen = P.correction != VT_CORRECTION_VTRACE || P.q_values != 0 || P.mu_lp != 0;
   if (exp_mode() == EXP_MUFU) {
-    return tma ? dispatch_a<LT, LOSS, true, EXP_MUFU>(P, maps, plan, st)
-               : dispatch_a<LT, LOSS, false, EXP_MUFU>(P, maps, plan, st);
+    return gen ? dispatch_t<LT, LOSS, EXP_MUFU, true>(P, maps, plan, tma, st)
+               : dispatch_t<LT, LOSS, EXP_MUFU, false>(P, maps, plan, tma, st);
   }
-  return tma ? dispatch_a<LT, LOSS, true, EXP_F64>(P, maps, plan, st)
-             : dispatch_a<LT, LOSS, false, EXP_F64>(P, maps, plan, st);
+  return dispatch_t<LT, LOSS, EXP_F64, true>(P, maps, plan, tma, st);
 }
 
 static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
@@ -839,6 +861,7 @@ static vt_status check_params(const vt_vtrace_params* p) {
   if (p->correction == VT_CORRECTION_EPSILON && !(p->epsilon > 0.f && std::isfinite(p->epsilon)))
     return VT_ERR_PARAM;
   if (p->q_from_values != 0 && p->q_from_values != 1) return VT_ERR_PARAM;
+  if (p->behaviour_log_probs != 0 && p->behaviour_log_probs != 1) return VT_ERR_PARAM;
   return VT_OK;
 }
 
@@ -882,7 +905,8 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
     if (!vs || !pg_adv) return VT_ERR_INVALID_ARG;
   }
   const int elem = dt == VT_BFLOAT16 ? 2 : 4;
-  if (!aligned(mu, elem) || !aligned(pi, elem) || !aligned(actions, 4) || !aligned(disc, 4) ||
+  const bool mu_lp = prm->behaviour_log_probs != 0;  // mu given as log mu(a_t) [T][B] fp32
+  if (!aligned(mu, mu_lp ? 4 : elem) || !aligned(pi, elem) || !aligned(actions, 4) || !aligned(disc, 4) ||
       !aligned(rew, 4) || !aligned(val, 4) || !aligned(boot, 4) ||
       (dlogits && !aligned(dlogits, elem)) || (dvalues && !aligned(dvalues, 4)) ||
       (partials && !aligned(partials, 8)) || (vs && !aligned(vs, 4)) ||
@@ -911,6 +935,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   P.correction = prm->correction;
   P.q_values = prm->q_from_values;
   P.eps = prm->epsilon;
+  P.mu_lp = mu_lp ? 1 : 0;
   P.c_v = loss ? (double)w->baseline_cost : 0.0;
   P.c_e = loss ? (double)w->entropy_cost : 0.0;
   unsigned char* wsb = static_cast<unsigned char*>(ws);
@@ -942,7 +967,8 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   if (tma) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    tma = encode_2d(&maps.mu, mu, ldt, elem, B * A, T, BC * (int)A, plan.Tc) &&
+    tma = (mu_lp ? encode_2d(&maps.mu, mu, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc)
+                 : encode_2d(&maps.mu, mu, ldt, elem, B * A, T, BC * (int)A, plan.Tc)) &&
           encode_2d(&maps.pi, pi, ldt, elem, B * A, T, BC * (int)A, plan.Tc) &&
           encode_2d(&maps.a, actions, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, B, T, BC, plan.Tc) &&
           encode_2d(&maps.r, rew, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, T, BC, plan.Tc) &&
@@ -962,7 +988,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
     TmaMaps cm;
     std::memset(&cm, 0, sizeof(cm));
     const bool ok =
-        encode_2d(&cm.mu, mu, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
+        (mu_lp || encode_2d(&cm.mu, mu, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS)) &&
         encode_2d(&cm.pi, pi, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
         (!loss || encode_2d(&cm.dz, dlogits, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS));
     if (ok) {
@@ -1049,6 +1075,7 @@ vt_status vtrace_loss_and_grad_from_host(
   if (!d_mu || !d_pi || !d_a || !d_g || !d_r || !d_v || !d_boot) return VT_ERR_INVALID_ARG;
   const size_t elem = dt == VT_BFLOAT16 ? 2 : 4;
   const size_t nl = (size_t)T * B * A * elem, ns = (size_t)T * B * 4;
+  const size_t nmu = (params && params->behaviour_log_probs) ? ns : nl;  // mu logits or log mu(a)
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // validate before any copy is issued
   vt_status s = check_params(params);
@@ -1060,7 +1087,7 @@ vt_status vtrace_loss_and_grad_from_host(
   if (s) return s;
   const cudaMemcpyKind h2d = cudaMemcpyHostToDevice;
   if (cudaMemcpyAsync(d_pi, h_pi, nl, h2d, st) != cudaSuccess ||
-      cudaMemcpyAsync(d_mu, h_mu, nl, h2d, st) != cudaSuccess ||
+      cudaMemcpyAsync(d_mu, h_mu, nmu, h2d, st) != cudaSuccess ||
       cudaMemcpyAsync(d_a, h_a, ns, h2d, st) != cudaSuccess ||
       cudaMemcpyAsync(d_g, h_g, ns, h2d, st) != cudaSuccess ||
       cudaMemcpyAsync(d_r, h_r, ns, h2d, st) != cudaSuccess ||

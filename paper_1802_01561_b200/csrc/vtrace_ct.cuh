@@ -162,6 +162,68 @@ __device__ __forceinline__ void ct_stats_fast(const LT* zrow, const LT* mrow, in
   R.finite = isfinite(sd.x) && isfinite(sd.y) && isfinite(mp) && isfinite(mm);
 }
 
+// The target row's statistics alone (behaviour given as log mu(a_t): no mu row);
+// same arithmetic as ct_stats_fast for pi.  S_m = 1 and xa_m are set by the caller.
+template <typename LT, int A_CT>
+__device__ __forceinline__ void ct_stats_fast_pi(const LT* zrow, int a, CtStats<LT, A_CT>& R) {
+  constexpr int NP = A_CT / 2;
+  constexpr bool BF16 = sizeof(LT) == 2;
+  constexpr float L16 = 1.44268798828125f;
+  constexpr float L32 = 1.44269502f;
+  constexpr float CORR = BF16 ? 4.8884952e-06f : 1.3349930e-08f;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    if constexpr (BF16) {
+      const uint32_t xp = reinterpret_cast<const uint32_t*>(zrow)[k];
+      R.z[k] = make_float2(__uint_as_float(xp << 16), __uint_as_float(xp & 0xffff0000u));
+    } else {
+      R.z[k] = reinterpret_cast<const float2*>(zrow)[k];
+    }
+  }
+  float mp = fmaxf(R.z[0].x, R.z[0].y);
+#pragma unroll
+  for (int k = 1; k < NP; ++k) mp = fmaxf(mp, fmaxf(R.z[k].x, R.z[k].y));
+  const float2 Lp = f2(BF16 ? L16 : L32);
+  const float2 nmLp = f2(BF16 ? -mp * L16 : 0.f);
+  const float2 nmp = f2(-mp);
+  float2 hp = f2(1.f), lp = f2(0.f), sdp = f2(0.f);
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    float2 yp, dp;
+    if constexpr (BF16) {
+      yp = __ffma2_rn(R.z[k], Lp, nmLp);
+      dp = R.z[k];
+    } else {
+      dp = __fadd2_rn(R.z[k], nmp);
+      yp = __fmul2_rn(dp, Lp);
+    }
+    const float2 ep = make_float2(ex2_approx(yp.x), ex2_approx(yp.y));
+    R.e[k] = ep;
+    sdp = __ffma2_rn(ep, dp, sdp);
+    const float2 np = __fadd2_rn(hp, ep);  // Fast2Sum: h >= 1 >= e
+    lp = __fadd2_rn(lp, __fadd2_rn(__fadd2_rn(hp, make_float2(-np.x, -np.y)), ep));
+    hp = np;
+  }
+  const float h0 = hp.x - 1.f, h1 = hp.y - 1.f;  // exact
+  const float s = h0 + h1;                         // TwoSum of the chain heads
+  const float bb = s - h0;
+  const float err = (h0 - (s - bb)) + (h1 - bb);
+  float sd = sdp.x + sdp.y;
+  if constexpr (BF16) sd = fmaf(-mp, s, sd);
+  const float lo = fmaf(sd, CORR, err + (lp.x + lp.y));
+  R.S_p = (double)s + (double)lo;
+  R.S_m = 1.0;
+  R.m_p = mp;
+  R.sd_p = sd;
+  const float zap = Elem<LT>::get(zrow, a);
+  R.xa_p = (double)zap - (double)mp;
+  R.xa_m = 0.0;
+  const float ya = BF16 ? fmaf(zap, L16, -mp * L16) : (zap - mp) * L32;
+  const float ea = ex2_approx(ya);
+  R.ea_p = fmaf(ea * CORR, zap - mp, ea);
+  R.finite = isfinite(sd) && isfinite(mp);
+}
+
 constexpr int CT_GROUP = 32;  // tasks per partials group
 
 // Waits until the N partial-sum records at p[0 .. N) carry this call's tag (relaxed
@@ -282,13 +344,14 @@ struct CtAcc {
 };
 
 // GEN: the call uses a Section 5.2.2 variant or the App. E.3 q estimate (false:
-// plain V-trace, the variant logic compiled out).
+// plain V-trace, the variant logic compiled out).  MULP: the behaviour is given as
+// log mu(a_t) [T][B] (no mu tile, no mu statistics; implies GEN).
 // One warp runs iterations [it_begin, it_end) of task `task` (4 trajectories): its
 // TMA ring (`base`, barriers `wb`), the per-step loads, a3-a11 per chunk.  The
 // carry A just after the segment comes from `cin` (another warp of the CTA, when
 // `cin_bar` completes) or is A_T = 0; the carry at the segment's first step goes
 // to `cout` / `cout_bar` for the warp running the earlier segment.
-template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN, bool MULP>
 __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const TmaMaps& maps,
                                        unsigned char* base, uint64_t* wb, const int lane,
                                        const int task, const int it_begin, const int it_end,
@@ -311,9 +374,9 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
     const int stg = (it - it_begin) % CT_NSTAGE;
     const int t0 = (K - 1 - it) * CT_STEPS;
     unsigned char* sb = base + (size_t)stg * C.stage;
-    mbar_expect_tx(&wb[stg], 2 * tile_bytes);
+    mbar_expect_tx(&wb[stg], (MULP ? 1u : 2u) * tile_bytes);
     tma_load_2d(sb + C.pi, &maps.pi, b0 * A, t0, &wb[stg]);
-    tma_load_2d(sb + C.mu, &maps.mu, b0 * A, t0, &wb[stg]);
+    if constexpr (!MULP) tma_load_2d(sb + C.mu, &maps.mu, b0 * A, t0, &wb[stg]);
   };
   if (lane == 0) {
     for (int s = 0; s < CT_NSTAGE; ++s) mbar_init(&wb[s], 1);
@@ -335,13 +398,13 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
   // ahead; `off` = flat index t * B + b of this lane's row, stepped back 8 B per chunk
   struct StepIn {
     int a;
-    float r, g, v, vn;
+    float r, g, v, vn, lmu;  // lmu: log mu(a_t) (MULP only)
   };
   const int off0 = ((K - 1 - it_begin) * CT_STEPS + tl) * B + b0 + c;
   const float* const bootp = P.boot + b0 + c;
   auto load_step = [&](int it, int off, StepIn& s) {
     const int t = (K - 1 - it) * CT_STEPS + tl;
-    s.a = 0; s.r = 0.f; s.g = 0.f; s.v = 0.f; s.vn = 0.f;
+    s.a = 0; s.r = 0.f; s.g = 0.f; s.v = 0.f; s.vn = 0.f; s.lmu = 0.f;
 #if defined(VTRACE_ABLATE) && (VTRACE_ABLATE == 7 || VTRACE_ABLATE == 8)
     if (false) {  // ablation: no per-step loads
 #else
@@ -353,6 +416,7 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       s.v = __ldg(P.val + off);
       // V(x_{t+1}); the last step of the unroll bootstraps from V(x_T)
       s.vn = __ldg((t + 1 < T) ? P.val + off + B : bootp);
+      if constexpr (MULP) s.lmu = __ldg(reinterpret_cast<const float*>(P.mu) + off);
     }
   };
 
@@ -399,11 +463,24 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       F.S_m = 18.0; F.xa_p = 0.0; F.xa_m = 0.0; F.finite = true;
 #else
     if constexpr (kFast) {
-      ct_stats_fast<LT, A_CT>(zrow, mrow, a, F);
+      if constexpr (MULP) {
+        ct_stats_fast_pi<LT, A_CT>(zrow, a, F);
+        F.xa_m = (double)cur.lmu;  // log mu(a_t), given (S_m = 1)
+        F.finite = F.finite && isfinite(cur.lmu);
+      } else {
+        ct_stats_fast<LT, A_CT>(zrow, mrow, a, F);
+      }
 #endif
       m_p = F.m_p; sed_p = F.sd_p; ea_p = F.ea_p; S_p = F.S_p; S_m = F.S_m;
       xa_p = F.xa_p; xa_m = F.xa_m;
       fin = F.finite;
+    } else if constexpr (MULP) {
+      bool fin_p;
+      zp.load(zrow);
+      row_stats<LT, A_CT, MODE>(zp, A, a, m_p, S_p, xa_p, ea_p, sed_p, fin_p);
+      xa_m = (double)cur.lmu;  // log mu(a_t), given
+      S_m = 1.0;
+      fin = fin_p && isfinite(cur.lmu);
     } else {
       float m_m, sed_m, ea_m;
       bool fin_p, fin_m;
@@ -616,7 +693,7 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
   acc_out = CtAcc{acc_pg, acc_v, acc_H, acc_dz, acc_dv, acc_rho, acc_clip};
 }
 
-template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN, bool MULP>
 __global__ void __launch_bounds__(CT_WARPS * 32)
     vtrace_ct_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -626,7 +703,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
   if (task >= C.tasks) return;
   if (C.timing && lane == 0) C.timing[(size_t)task * 4 + 0] = gtimer();
   CtAcc acc;
-  ct_run<LT, A_CT, LOSS, MODE, GEN>(P, C, maps, smem, bar, lane, task, 0, C.K, nullptr, nullptr,
+  ct_run<LT, A_CT, LOSS, MODE, GEN, MULP>(P, C, maps, smem, bar, lane, task, 0, C.K, nullptr, nullptr,
                                nullptr, nullptr, acc);
   if constexpr (LOSS) {
     if (P.partials != nullptr) {
@@ -650,7 +727,7 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
 // -> the last CTA to finish adds the CTA sums in CTA order.
 constexpr int CTB_WARPS = 16;
 
-template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN, bool MULP>
 __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
     vtrace_ctb_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -693,7 +770,7 @@ __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
     const bool whole = slot >= nseg;
     const bool first = whole || p == 0, last = whole || p == C.segs - 1;
     // segment hand-over slots: slot j feeds slot j + 1 (same task)
-    ct_run<LT, A_CT, LOSS, MODE, GEN>(P, C, maps, smem + (size_t)w * C.warp_bytes, bar[w], lane,
+    ct_run<LT, A_CT, LOSS, MODE, GEN, MULP>(P, C, maps, smem + (size_t)w * C.warp_bytes, bar[w], lane,
                                  task, it_begin, it_end, first ? nullptr : hcarry[slot - 1],
                                  &hbar[first ? slot : slot - 1], last ? nullptr : hcarry[slot],
                                  &hbar[slot], acc);

@@ -66,12 +66,12 @@ bool ct_plan_balanced(CtParams& C, int S) {
 
 #endif
 
-template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN>
+template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN, bool MULP>
 static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
                                cudaStream_t st) {
   const int S = ct_num_sms();
   if (ct_plan_balanced(C, S)) {
-    auto kern = vtrace_ctb_kernel<LT, A_CT, LOSS, MODE, GEN>;
+    auto kern = vtrace_ctb_kernel<LT, A_CT, LOSS, MODE, GEN, MULP>;
     const size_t smem = (size_t)CTB_WARPS * C.warp_bytes;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -82,7 +82,7 @@ static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
     kern<<<S, CTB_WARPS * 32, smem, st>>>(P, C, maps);
     return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
   }
-  auto kern = vtrace_ct_kernel<LT, A_CT, LOSS, MODE, GEN>;
+  auto kern = vtrace_ct_kernel<LT, A_CT, LOSS, MODE, GEN, MULP>;
   const size_t smem = (size_t)CT_WARPS * C.warp_bytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -99,24 +99,27 @@ static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
+template <typename LT, bool LOSS, int MODE, bool GEN, bool MULP>
+static vt_status ct_dispatch_a(const Params& P, const CtParams& C, const TmaMaps& maps,
+                               cudaStream_t st) {
+  if (P.A == 18) return ct_launch_one<LT, 18, LOSS, MODE, GEN, MULP>(P, C, maps, st);
+  if (P.A == 9) return ct_launch_one<LT, 9, LOSS, MODE, GEN, MULP>(P, C, maps, st);
+  return ct_launch_one<LT, 0, LOSS, MODE, GEN, MULP>(P, C, maps, st);
+}
+
 template <typename LT, bool LOSS>
 static vt_status ct_dispatch(const Params& P, const CtParams& C, const TmaMaps& maps,
                              cudaStream_t st) {
-  // plain V-trace takes the instantiation with the variant logic compiled out
-  const bool gen = P.correction != VT_CORRECTION_VTRACE || P.q_values != 0;
+  // plain V-trace with behaviour logits takes the instantiation with the variant
+  // logic compiled out; behaviour log-probs (MULP) come with the general one
+  const bool gen = P.correction != VT_CORRECTION_VTRACE || P.q_values != 0 || P.mu_lp != 0;
   if (exp_mode() == EXP_MUFU) {
-    if (!gen) {
-      if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_MUFU, false>(P, C, maps, st);
-      if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_MUFU, false>(P, C, maps, st);
-      return ct_launch_one<LT, 0, LOSS, EXP_MUFU, false>(P, C, maps, st);
-    }
-    if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_MUFU, true>(P, C, maps, st);
-    if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_MUFU, true>(P, C, maps, st);
-    return ct_launch_one<LT, 0, LOSS, EXP_MUFU, true>(P, C, maps, st);
+    if (P.mu_lp) return ct_dispatch_a<LT, LOSS, EXP_MUFU, true, true>(P, C, maps, st);
+    if (gen) return ct_dispatch_a<LT, LOSS, EXP_MUFU, true, false>(P, C, maps, st);
+    return ct_dispatch_a<LT, LOSS, EXP_MUFU, false, false>(P, C, maps, st);
   }
-  if (P.A == 18) return ct_launch_one<LT, 18, LOSS, EXP_F64, true>(P, C, maps, st);
-  if (P.A == 9) return ct_launch_one<LT, 9, LOSS, EXP_F64, true>(P, C, maps, st);
-  return ct_launch_one<LT, 0, LOSS, EXP_F64, true>(P, C, maps, st);
+  if (P.mu_lp) return ct_dispatch_a<LT, LOSS, EXP_F64, true, true>(P, C, maps, st);
+  return ct_dispatch_a<LT, LOSS, EXP_F64, true, false>(P, C, maps, st);
 }
 
 // each object instantiates one logits dtype (VT_CT_PART 0: bf16, 1: fp32)

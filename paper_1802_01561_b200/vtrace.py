@@ -47,7 +47,8 @@ class _Params(ctypes.Structure):
     _fields_ = [("clip_rho_threshold", ctypes.c_float), ("clip_c_threshold", ctypes.c_float),
                 ("clip_pg_rho_threshold", ctypes.c_float), ("lambda_", ctypes.c_float),
                 ("reward_mode", ctypes.c_int32), ("correction", ctypes.c_int32),
-                ("epsilon", ctypes.c_float), ("q_from_values", ctypes.c_int32)]
+                ("epsilon", ctypes.c_float), ("q_from_values", ctypes.c_int32),
+                ("behaviour_log_probs", ctypes.c_int32)]
 
 
 # vt_correction: Section 5.2.2 off-policy correction variants
@@ -124,10 +125,12 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 
 def params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=0,
-           correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0) -> _Params:
+           correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
+           behaviour_log_probs=0) -> _Params:
     return _Params(float(rho_bar), float(c_bar),
                    float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
-                   int(reward_mode), int(correction), float(epsilon), int(q_from_values))
+                   int(reward_mode), int(correction), float(epsilon), int(q_from_values),
+                   int(behaviour_log_probs))
 
 
 def workspace_bytes(T: int, B: int, A: int, dtype_code: int) -> int:
@@ -155,12 +158,22 @@ class Workspace:
 
 
 def _shapes(behaviour_logits, target_logits, actions):
-    if behaviour_logits.dim() != 3 or target_logits.shape != behaviour_logits.shape:
-        raise ValueError("logits must be [T, B, A] and equal shapes")
+    """(T, B, A, mu_lp): the behaviour input is either mu's [T, B, A] logits or, in
+    behaviour-log-prob mode, log mu(a_t) as a [T, B] float32 tensor."""
+    if target_logits.dim() != 3:
+        raise ValueError("target logits must be [T, B, A]")
     T, B, A = target_logits.shape
+    if behaviour_logits.dim() == 2:
+        if behaviour_logits.shape != (T, B) or behaviour_logits.dtype != torch.float32:
+            raise ValueError("behaviour log-probs must be a [T, B] float32 tensor")
+        mu_lp = 1
+    elif behaviour_logits.shape != target_logits.shape:
+        raise ValueError("behaviour and target logits must have equal [T, B, A] shapes")
+    else:
+        mu_lp = 0
     if actions.shape != (T, B):
         raise ValueError("actions must be [T, B]")
-    return T, B, A
+    return T, B, A, mu_lp
 
 
 def _contig(*ts):
@@ -179,7 +192,7 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
     """vtrace_from_logits.  Returns dict of fp32 [T, B] tensors: vs,
     pg_advantages (+ log_rhos, target_action_log_probs, behaviour_action_log_probs)."""
     lib = load_library()
-    T, B, A = _shapes(behaviour_logits, target_logits, actions)
+    T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions)
     dt = _dtype_code(target_logits)
     dev = target_logits.device
     _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
@@ -189,7 +202,8 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
         if with_log_probs:
             for k in ("log_rhos", "target_action_log_probs", "behaviour_action_log_probs"):
                 out[k] = torch.empty(T, B, dtype=torch.float32, device=dev)
-    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
+               mu_lp)
     st = lib.vtrace_from_logits(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
         _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), _ptr(out["vs"]),
@@ -209,7 +223,7 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
     dtype), grad_values [T,B] fp32, partials [8] fp64 (device), and, if
     with_targets, vs and pg_advantages [T,B] fp32."""
     lib = load_library()
-    T, B, A = _shapes(behaviour_logits, target_logits, actions)
+    T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions)
     dt = _dtype_code(target_logits)
     dev = target_logits.device
     _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
@@ -221,7 +235,8 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
         if with_targets:
             out["vs"] = torch.empty(T, B, dtype=torch.float32, device=dev)
             out["pg_advantages"] = torch.empty(T, B, dtype=torch.float32, device=dev)
-    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
+               mu_lp)
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
@@ -247,7 +262,9 @@ def loss_and_grad_from_host(host: dict, dev_in: dict, out: dict, workspace: Work
     dev = dev_in["target_logits"].device
     names = ("behaviour_logits", "target_logits", "actions", "discounts", "rewards", "values",
              "bootstrap_value")
-    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values)
+    mu_lp = 1 if host["behaviour_logits"].dim() == 2 else 0  # log mu(a_t) [T, B] mode
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
+               mu_lp)
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad_from_host(
         T, B, A, dt, *[_ptr(host[k]) for k in names], *[_ptr(dev_in[k]) for k in names],
@@ -288,10 +305,17 @@ INPUT_NAMES = ("behaviour_logits", "target_logits", "actions", "discounts", "rew
 
 
 def tensors_from_workload(inp: dict, device="cuda", pin: bool = False) -> dict:
-    """numpy workload dict -> torch tensors (bf16 logits from their uint16 bits)."""
+    """numpy workload dict -> torch tensors (bf16 logits from their uint16 bits).
+    If the dict carries ``behaviour_log_probs`` ([T, B] log mu(a_t)), that array is
+    the behaviour input (the "behaviour_logits" slot) instead of the logits."""
     out = {}
     for k in INPUT_NAMES:
         a = inp[k]
+        if k == "behaviour_logits" and inp.get("behaviour_log_probs") is not None:
+            a = np.ascontiguousarray(inp["behaviour_log_probs"], dtype=np.float32)
+            t = torch.from_numpy(a)
+            out[k] = (t.pin_memory() if pin else t.clone()) if device == "cpu" else t.to(device)
+            continue
         if k.endswith("logits") and inp["dtype"] == _wl.DTYPE_BF16:
             t = torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16)
         else:

@@ -130,3 +130,7 @@ def test_kernel_choice(lib):
     assert vt.kernel_for(5, 2, 3, 0) == "vtrace_fused_kernel (plain loads)"  # toy: pitch 24 B
     assert vt.kernel_for(0, 8, 3, 0).startswith("none")
     assert vt.kernel_for(5, 8, 3, 7).startswith("none")
+
+
+def test_behaviour_log_prob_param_check(lib):
+    assert _call_loss(lib, params=vt.params(behaviour_log_probs=2)) == 4

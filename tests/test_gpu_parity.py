@@ -359,3 +359,32 @@ def test_parity_epsilon_correction_large_eps(shape):
     check_all(inp, lg, fl, ref_l, ref_f)
     plain = oracle.loss_and_grad(inp, reward_mode=inp.get("reward_mode", 0), correction=1)
     assert np.max(np.abs(plain["grad_target_logits"] - ref_l["grad_target_logits"])) > 1e-4
+
+
+def _with_behaviour_log_probs(inp):
+    """The actors' log mu(a_t) for the sampled actions, from the behaviour logits by a
+    plain numpy fp64 log-softmax, rounded to fp32 (SURVEY 8(f) NEXT #2 input mode)."""
+    zm = inp["behaviour_logits"]
+    if inp["dtype"] == wl.DTYPE_BF16:
+        zm = (zm.astype(np.uint32) << 16).view(np.float32)
+    zm = zm.astype(np.float64)
+    mx = zm.max(-1, keepdims=True)
+    lse = np.log(np.exp(zm - mx).sum(-1)) + mx[..., 0]
+    za = np.take_along_axis(zm, inp["actions"][..., None].astype(np.int64), -1)[..., 0]
+    return dict(inp, behaviour_log_probs=(za - lse).astype(np.float32))
+
+
+@pytest.mark.parametrize("name,kw", [("atari", None), ("dmlab", None), ("stress", dict(T=300)),
+                                     ("large", dict(B=4096, T=40)), ("large", None),
+                                     ("toy", None)])
+@pytest.mark.parametrize("corr", [0, 3])
+def test_parity_behaviour_log_probs(name, kw, corr):
+    """Behaviour given as log mu(a_t) [T, B] fp32 (no mu logits read) on every kernel
+    (look-back with TMA / plain loads, column-task) against the oracle in the same
+    mode."""
+    inp = _with_behaviour_log_probs(wl.inputs_for(name) if kw is None else
+                                    wl.make_inputs(name, seed=77, **kw))
+    lg, fl, ref_l, ref_f = run_both(inp, correction=corr)
+    check_all(inp, lg, fl, ref_l, ref_f)
+    np.testing.assert_array_equal(_np(fl["behaviour_action_log_probs"]),
+                                  inp["behaviour_log_probs"].astype(np.float64))
