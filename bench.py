@@ -53,7 +53,26 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--behaviour", choices=["logits", "log_probs"], default="logits",
+                    help="log_probs: the actors ship log mu(a_t) [T,B] instead of mu's "
+                         "[T,B,A] logits (SURVEY 8(f) NEXT #2 input mode)")
     return ap.parse_args()
+
+
+def with_behaviour_log_probs(inp):
+    """Input preparation for --behaviour log_probs (outside any timed region): the
+    actors' log mu(a_t) for the sampled actions, by a plain numpy fp64 log-softmax of
+    the generated behaviour logits, rounded to fp32."""
+    import numpy as np
+    from paper_1802_01561_b200 import workload as wl
+    zm = inp["behaviour_logits"]
+    if inp["dtype"] == wl.DTYPE_BF16:
+        zm = (zm.astype(np.uint32) << 16).view(np.float32)
+    zm = zm.astype(np.float64)
+    mx = zm.max(-1, keepdims=True)
+    lse = np.log(np.exp(zm - mx).sum(-1)) + mx[..., 0]
+    za = np.take_along_axis(zm, inp["actions"][..., None].astype(np.int64), -1)[..., 0]
+    return dict(inp, behaviour_log_probs=(za - lse).astype(np.float32))
 
 
 # ---------------------------------------------------------------------------
@@ -177,9 +196,12 @@ def load_traffic(config_name: str):
         return None
 
 
-def algorithmic_bytes(T, B, A, elem):
+def algorithmic_bytes(T, B, A, elem, mu_lp=False):
     """Bytes the method must move per call: read both logits rows,
-    a, r, gamma, V; write dlogits, dV; plus the bootstrap row and 64 B partials."""
+    a, r, gamma, V; write dlogits, dV; plus the bootstrap row and 64 B partials.
+    Behaviour as log mu(a_t): one logits row + 4 B of log-prob instead of two rows."""
+    if mu_lp:
+        return T * B * (2 * A * elem + 24) + 4 * B + 64
     return T * B * (3 * A * elem + 20) + 4 * B + 64
 
 
@@ -208,6 +230,9 @@ def run_ours(args):
 
     cfg = wl.CONFIGS[args.config]
     inp = make_rank_inputs(cfg, rank, world, args.strong)
+    mu_lp = args.behaviour == "log_probs"
+    if mu_lp:
+        inp = with_behaviour_log_probs(inp)
     T, B, A = inp["T"], inp["B"], inp["A"]
     elem = 2 if inp["dtype"] == wl.DTYPE_BF16 else 4
     host = pkg.tensors_from_workload(inp, "cpu", pin=True)
@@ -368,9 +393,9 @@ def run_ours(args):
     ms_per_step = elapsed_max / K
     value = T * B * world / (ms_per_step * 1e-3)
     peak, peak_src = load_peak()
-    alg = algorithmic_bytes(T, B, A, elem)
+    alg = algorithmic_bytes(T, B, A, elem, mu_lp)
     achieved = alg / (kernel_ms * 1e-3) / 1e9
-    traffic = load_traffic(args.config)
+    traffic = load_traffic(args.config + ("+behaviour_log_probs" if mu_lp else ""))
     clocks = sampler.summary(tw0, tw1) if sampler else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -379,7 +404,8 @@ def run_ours(args):
         "dtype": ("bf16" if elem == 2 else "f32") + " logits; f32 exps with compensated "
                  "(exact-order) sums, f64 ratio and scan, f32 gradient epilogue",
         "data": "synthetic (seeded, DMLab/Atari-shaped; DESIGN.md input recipe)",
-        "config": {"workload": cfg.name, "T": T, "B_per_gpu": B, "A": A,
+        "config": {"workload": cfg.name + ("+behaviour_log_probs" if mu_lp else ""),
+                   "T": T, "B_per_gpu": B, "A": A, "behaviour": args.behaviour,
                    "logits_dtype": "bf16" if elem == 2 else "fp32",
                    "global_batch": B * world, "seq_len": T, "parallelism": f"dp{world}",
                    "l2": f"inputs rotated over {R} HBM-resident copies "
@@ -442,6 +468,8 @@ def run_reference(args):
     from paper_1802_01561_b200 import workload as wl
     cfg = wl.CONFIGS[args.config]
     inp = wl.make_inputs(cfg.name)
+    if args.behaviour == "log_probs":
+        inp = with_behaviour_log_probs(inp)
     T, B = inp["T"], inp["B"]
     # size each step's column sample so the whole run takes ~1-2 minutes
     probe = wl.column_slice(inp, 0, min(B, 32))
@@ -464,7 +492,7 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "T": T, "B_sample": ncols, "A": inp["A"],
+            "config": {"workload": cfg.name + ("+behaviour_log_probs" if args.behaviour == "log_probs" else ""), "T": T, "B_sample": ncols, "A": inp["A"],
                        "global_batch": ncols, "seq_len": T, "parallelism": "cpu-1core"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": desc, "host_cpu": _cpu_model()},

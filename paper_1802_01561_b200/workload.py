@@ -157,7 +157,8 @@ def column_slice(inp: dict, b0: int, b1: int) -> dict:
     out["B"] = b1 - b0
     for k in ("target_logits", "behaviour_logits"):
         out[k] = np.ascontiguousarray(inp[k][:, b0:b1])
-    for k in ("actions", "rewards", "values", "discounts"):
-        out[k] = np.ascontiguousarray(inp[k][:, b0:b1])
+    for k in ("actions", "rewards", "values", "discounts", "behaviour_log_probs"):
+        if inp.get(k) is not None:
+            out[k] = np.ascontiguousarray(inp[k][:, b0:b1])
     out["bootstrap_value"] = np.ascontiguousarray(inp["bootstrap_value"][b0:b1])
     return out
