@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="plain stream order between steps (no programmatic dependent launch)")
     ap.add_argument("--behaviour", choices=["logits", "log_probs"], default="logits",
                     help="log_probs: the actors ship log mu(a_t) [T,B] instead of mu's "
                          "[T,B,A] logits (SURVEY 8(f) NEXT #2 input mode)")
@@ -249,13 +251,17 @@ def run_ours(args):
     ws = pkg.Workspace(T, B, A, inp["dtype"])
     kw = dict(reward_mode=inp["reward_mode"], baseline_cost=wl.BASELINE_COST,
               entropy_cost=wl.ENTROPY_COST, rho_bar=wl.RHO_BAR, c_bar=wl.C_BAR)
+    # consecutive learner steps: each step's inputs are a fresh (rotated) trajectory
+    # batch, never the previous step's outputs, so the step may overlap the previous
+    # kernel's tail (programmatic dependent launch; --no-overlap: plain stream order)
+    kw_step = dict(kw, overlap_previous=not args.no_overlap)
     s_main = torch.cuda.Stream()
     s_comm = torch.cuda.Stream()
 
     def step(i):
         o = outs[i % R]
         x = sets[i % R]
-        pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw)
+        pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw_step)
         if world > 1:
             s_comm.wait_stream(s_main)
             with torch.cuda.stream(s_comm):
@@ -340,7 +346,7 @@ def run_ours(args):
             for i in range(min(Kk, C)):
                 o = outs[i % R]
                 x = sets[i % R]
-                pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw)
+                pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw_step)
     except Exception:  # noqa: BLE001
         gk = None
     torch.cuda.synchronize()
@@ -411,6 +417,8 @@ def run_ours(args):
                    "l2": f"inputs rotated over {R} HBM-resident copies "
                          f"({R} x {working / 1e6:.1f} MB >= 4 x L2)",
                    "timing": graph_mode,
+                   "step_overlap": "none" if args.no_overlap else
+                   "programmatic dependent launch (overlap_previous: inputs are fresh batches)",
                    "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream)"
                    if world > 1 else "none"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -119,6 +119,14 @@ typedef struct {
                                   only the taken action's log-probability; SURVEY 8(f)
                                   NEXT #2), 4-byte aligned; logits_dtype still gives
                                   the target logits' dtype                           */
+  int32_t overlap_previous;    /* 1: this call's inputs are not outputs of the previous
+                                  kernel on `stream` (e.g. consecutive learner steps on
+                                  fresh trajectories).  The wide-batch kernel is then
+                                  launched as a programmatic dependent: its prologue
+                                  (input loads, the first chunk's statistics) overlaps
+                                  the previous kernel's tail, and it waits for that
+                                  kernel before its first global write.  0 = plain
+                                  stream order (always safe)                         */
 } vt_vtrace_params;
 
 typedef struct {

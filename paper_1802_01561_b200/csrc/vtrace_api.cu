@@ -862,6 +862,7 @@ static vt_status check_params(const vt_vtrace_params* p) {
     return VT_ERR_PARAM;
   if (p->q_from_values != 0 && p->q_from_values != 1) return VT_ERR_PARAM;
   if (p->behaviour_log_probs != 0 && p->behaviour_log_probs != 1) return VT_ERR_PARAM;
+  if (p->overlap_previous != 0 && p->overlap_previous != 1) return VT_ERR_PARAM;
   return VT_OK;
 }
 
@@ -936,6 +937,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   P.q_values = prm->q_from_values;
   P.eps = prm->epsilon;
   P.mu_lp = mu_lp ? 1 : 0;
+  P.pdl = prm->overlap_previous;  // honoured by the column-task kernels
   P.c_v = loss ? (double)w->baseline_cost : 0.0;
   P.c_e = loss ? (double)w->entropy_cost : 0.0;
   unsigned char* wsb = static_cast<unsigned char*>(ws);

@@ -517,6 +517,9 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
       if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
     }
+    // (programmatic dependent launch: everything above only read this call's inputs;
+    // the first global write of the task waits for the previous kernel on the stream)
+    if (P.pdl && it == it_begin) asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool bad = row_ok && ((a_raw != a) || !fin || !isfinite(rt) || !isfinite(Vt) ||
                                 !isfinite(Vn) || !(gm >= 0.f && gm <= 1.f));
     if (!row_ok) {
@@ -698,6 +701,8 @@ __global__ void __launch_bounds__(CT_WARPS * 32)
     vtrace_ct_kernel(const Params P, const CtParams C, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[CT_NSTAGE];
+  // a programmatically dependent next kernel may launch (it waits before writing)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int task = blockIdx.x;
   if (task >= C.tasks) return;
@@ -735,6 +740,8 @@ __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
   __shared__ __align__(8) uint64_t hbar[CTB_WARPS];
   __shared__ double hcarry[CTB_WARPS][CT_COLS];
   __shared__ double wpart[CTB_WARPS][NPART];
+  // a programmatically dependent next kernel may launch (it waits before writing)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int cta = blockIdx.x, S = gridDim.x;
   if (lane == 0) {
@@ -777,6 +784,7 @@ __global__ void __launch_bounds__(CTB_WARPS * 32, 1)
   }
   if constexpr (LOSS) {
     if (P.partials == nullptr) return;
+    if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // (idle warps too)
     double part[NPART] = {acc.pg, acc.v, acc.H, 0.0, acc.dz, acc.dv, acc.rho, acc.clip};
 #pragma unroll
     for (int k = 0; k < NPART; ++k) {

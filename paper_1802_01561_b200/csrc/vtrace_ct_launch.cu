@@ -66,6 +66,28 @@ bool ct_plan_balanced(CtParams& C, int S) {
 
 #endif
 
+// Launch, as a programmatic dependent of the previous kernel on the stream when
+// `pdl` (vt_vtrace_params.overlap_previous): the kernel waits (griddepcontrol.wait)
+// before its first global write.
+template <typename Kern>
+static vt_status launch_maybe_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                  bool pdl, const Params& P, const CtParams& C,
+                                  const TmaMaps& maps) {
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, P, C, maps) != cudaSuccess) return VT_ERR_CUDA;
+  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+}
+
 template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN, bool MULP>
 static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
                                cudaStream_t st) {
@@ -79,8 +101,8 @@ static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
       attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
     });
     if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
-    kern<<<S, CTB_WARPS * 32, smem, st>>>(P, C, maps);
-    return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+    return launch_maybe_pdl(kern, dim3(S), dim3(CTB_WARPS * 32), smem, st, P.pdl != 0, P, C,
+                            maps);
   }
   auto kern = vtrace_ct_kernel<LT, A_CT, LOSS, MODE, GEN, MULP>;
   const size_t smem = (size_t)CT_WARPS * C.warp_bytes;
@@ -95,8 +117,8 @@ static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
   });
   if (attr_err != cudaSuccess || smem > kMaxSmem) return VT_ERR_CUDA;
   const unsigned grid = (unsigned)((C.tasks + CT_WARPS - 1) / CT_WARPS);
-  kern<<<grid, CT_WARPS * 32, smem, st>>>(P, C, maps);
-  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+  return launch_maybe_pdl(kern, dim3(grid), dim3(CT_WARPS * 32), smem, st, P.pdl != 0, P, C,
+                          maps);
 }
 
 template <typename LT, bool LOSS, int MODE, bool GEN, bool MULP>

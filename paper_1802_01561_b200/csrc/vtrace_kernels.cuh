@@ -91,6 +91,7 @@ struct Params {
   int correction;  // vt_correction (Section 5.2.2)
   int q_values;    // 1: q_s = r_s + gamma V(x_{s+1}) (App. E.3)
   int mu_lp;       // 1: `mu` is log mu(a_t) [T][B] fp32 instead of [T][B][A] logits
+  int pdl;         // 1: launched as a programmatic dependent (overlap_previous)
   float eps;       // epsilon-correction constant
   WsHeader* ws;
   TagRec* recs;          // [units][BC][RECS_PER_COL]

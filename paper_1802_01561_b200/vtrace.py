@@ -48,7 +48,7 @@ class _Params(ctypes.Structure):
                 ("clip_pg_rho_threshold", ctypes.c_float), ("lambda_", ctypes.c_float),
                 ("reward_mode", ctypes.c_int32), ("correction", ctypes.c_int32),
                 ("epsilon", ctypes.c_float), ("q_from_values", ctypes.c_int32),
-                ("behaviour_log_probs", ctypes.c_int32)]
+                ("behaviour_log_probs", ctypes.c_int32), ("overlap_previous", ctypes.c_int32)]
 
 
 # vt_correction: Section 5.2.2 off-policy correction variants
@@ -126,11 +126,11 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 def params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=0,
            correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
-           behaviour_log_probs=0) -> _Params:
+           behaviour_log_probs=0, overlap_previous=0) -> _Params:
     return _Params(float(rho_bar), float(c_bar),
                    float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
                    int(reward_mode), int(correction), float(epsilon), int(q_from_values),
-                   int(behaviour_log_probs))
+                   int(behaviour_log_probs), int(overlap_previous))
 
 
 def workspace_bytes(T: int, B: int, A: int, dtype_code: int) -> int:
@@ -187,7 +187,7 @@ def _contig(*ts):
 def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, values,
                 bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
                 reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
-                workspace: Workspace | None = None, with_log_probs=True,
+                overlap_previous=False, workspace: Workspace | None = None, with_log_probs=True,
                 out: dict | None = None):
     """vtrace_from_logits.  Returns dict of fp32 [T, B] tensors: vs,
     pg_advantages (+ log_rhos, target_action_log_probs, behaviour_action_log_probs)."""
@@ -203,7 +203,7 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
             for k in ("log_rhos", "target_action_log_probs", "behaviour_action_log_probs"):
                 out[k] = torch.empty(T, B, dtype=torch.float32, device=dev)
     p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
-               mu_lp)
+               mu_lp, int(overlap_previous))
     st = lib.vtrace_from_logits(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
         _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), _ptr(out["vs"]),
@@ -217,7 +217,7 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
 def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, values,
                   bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
                   reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
-                  baseline_cost=0.5, entropy_cost=0.01,
+                  baseline_cost=0.5, entropy_cost=0.01, overlap_previous=False,
                   workspace: Workspace | None = None, with_targets=True, out: dict | None = None):
     """vtrace_loss_and_grad.  Returns dict: grad_target_logits [T,B,A] (logits
     dtype), grad_values [T,B] fp32, partials [8] fp64 (device), and, if
@@ -236,7 +236,7 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
             out["vs"] = torch.empty(T, B, dtype=torch.float32, device=dev)
             out["pg_advantages"] = torch.empty(T, B, dtype=torch.float32, device=dev)
     p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
-               mu_lp)
+               mu_lp, int(overlap_previous))
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
@@ -264,7 +264,7 @@ def loss_and_grad_from_host(host: dict, dev_in: dict, out: dict, workspace: Work
              "bootstrap_value")
     mu_lp = 1 if host["behaviour_logits"].dim() == 2 else 0  # log mu(a_t) [T, B] mode
     p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
-               mu_lp)
+               mu_lp, 0)  # (its inputs come from the copies just before)
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad_from_host(
         T, B, A, dt, *[_ptr(host[k]) for k in names], *[_ptr(dev_in[k]) for k in names],

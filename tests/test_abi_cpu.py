@@ -134,3 +134,7 @@ def test_kernel_choice(lib):
 
 def test_behaviour_log_prob_param_check(lib):
     assert _call_loss(lib, params=vt.params(behaviour_log_probs=2)) == 4
+
+
+def test_overlap_previous_param_check(lib):
+    assert _call_loss(lib, params=vt.params(overlap_previous=2)) == 4

@@ -388,3 +388,45 @@ def test_parity_behaviour_log_probs(name, kw, corr):
     check_all(inp, lg, fl, ref_l, ref_f)
     np.testing.assert_array_equal(_np(fl["behaviour_action_log_probs"]),
                                   inp["behaviour_log_probs"].astype(np.float64))
+
+
+@pytest.mark.parametrize("balanced", ["1", "0"])
+def test_overlap_previous_chain_bitwise(balanced, monkeypatch):
+    """overlap_previous (programmatic dependent launch of the wide-batch kernel):
+    consecutive calls on alternating input/output sets, eager and graph-captured,
+    give bitwise the results of plain stream order."""
+    monkeypatch.setenv("VTRACE_CT_BALANCED", balanced)
+    sets = [wl.make_inputs("large", seed=600 + i, B=8192, T=40) for i in range(3)]
+    devs = [_dev(x) for x in sets]
+    ref = [{k: v.clone() for k, v in pkg.loss_and_grad(*[d[k] for k in NAMES],
+                                                         reward_mode=1).items()} for d in devs]
+    ws = pkg.Workspace(40, 8192, 18, sets[0]["dtype"])
+    outs = [{k: torch.empty_like(v) for k, v in r.items()} for r in ref]
+    for rep in range(2):
+        for i in range(6):
+            j = i % 3
+            pkg.loss_and_grad(*[devs[j][k] for k in NAMES], reward_mode=1, workspace=ws,
+                              out=outs[j], overlap_previous=True)
+        torch.cuda.synchronize()
+        for j in range(3):
+            for k in ref[j]:
+                assert torch.equal(outs[j][k], ref[j][k]), (rep, j, k)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(6):
+                j = i % 3
+                pkg.loss_and_grad(*[devs[j][k] for k in NAMES], reward_mode=1, workspace=ws,
+                                  out=outs[j], overlap_previous=True)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(2):
+        for o in outs:
+            for v in o.values():
+                v.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for j in range(3):
+            for k in ref[j]:
+                assert torch.equal(outs[j][k], ref[j][k]), ("graph", j, k)
