@@ -511,34 +511,11 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
       acc_rho += (float)sw.rho;  // the rho_t in delta_t (reading r6)
       acc_clip += ((!GEN || P.correction == VT_CORRECTION_VTRACE) && ratio > P.rho_bar) ? 1.f : 0.f;
     }
-    if (!LOSS && row_ok) {
-      const int row = off;
-      if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
-      if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
-      if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
-    }
-    // (programmatic dependent launch: everything above only read this call's inputs;
-    // the first global write of the task waits for the previous kernel on the stream)
-    if (P.pdl && it == it_begin) asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool bad = row_ok && ((a_raw != a) || !fin || !isfinite(rt) || !isfinite(Vt) ||
                                 !isfinite(Vn) || !(gm >= 0.f && gm <= 1.f));
     if (!row_ok) {
       dl = 0.0;  // identity map for steps past the end of the unroll
       gc = 1.0;
-    }
-#if defined(VTRACE_ABLATE) && VTRACE_ABLATE == 8
-    if (false) {  // (garbage inputs)
-#else
-    if (bad) {
-#endif
-      const int row = off;
-      if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
-      if (!fin) record_bad(P.ws, row, VT_DATA_LOGITS);
-      if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
-      if (!isfinite(Vt)) record_bad(P.ws, row, VT_DATA_VALUE);
-      if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
-      if (!isfinite(Vn) && t0 + tl + 1 == T)
-        record_bad(P.ws, (long long)T * B + b0 + c, VT_DATA_VALUE);  // the bootstrap
     }
 
     // ---- a8: suffix scan of the chunk's affine maps, per column ----------------
@@ -565,6 +542,30 @@ __device__ __forceinline__ void ct_run(const Params& P, const CtParams& C, const
     double A_n = shfl_down_d(A_t, CT_COLS);                // A_{t+1}
     if (tl + 1 >= tlen) A_n = carry;
     carry = __shfl_sync(0xffffffffu, A_t, c);              // A at the chunk's first step
+
+    // (programmatic dependent launch: everything above only read this call's inputs;
+    // the task's first global write waits for the previous kernel on the stream)
+    if (P.pdl && it == it_begin) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!LOSS && row_ok) {
+      const int row = off;
+      if (P.has_lr) P.log_rhos[row] = (float)log(ratio);
+      if (P.has_lp) P.lp_out[row] = (float)(xa_p - log(S_p));
+      if (P.has_lm) P.lm_out[row] = (float)(xa_m - log(S_m));
+    }
+#if defined(VTRACE_ABLATE) && VTRACE_ABLATE == 8
+    if (false) {  // (garbage inputs)
+#else
+    if (bad) {
+#endif
+      const int row = off;
+      if (a_raw != a) record_bad(P.ws, row, VT_DATA_ACTION);
+      if (!fin) record_bad(P.ws, row, VT_DATA_LOGITS);
+      if (!isfinite(rt)) record_bad(P.ws, row, VT_DATA_REWARD);
+      if (!isfinite(Vt)) record_bad(P.ws, row, VT_DATA_VALUE);
+      if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
+      if (!isfinite(Vn) && t0 + tl + 1 == T)
+        record_bad(P.ws, (long long)T * B + b0 + c, VT_DATA_VALUE);  // the bootstrap
+    }
 
     // ---- a9-a11: advantages, value gradient, policy gradient ------------------
     if (row_ok) {

@@ -430,3 +430,23 @@ def test_overlap_previous_chain_bitwise(balanced, monkeypatch):
         for j in range(3):
             for k in ref[j]:
                 assert torch.equal(outs[j][k], ref[j][k]), ("graph", j, k)
+
+
+def test_overlap_previous_from_logits_chain_bitwise():
+    """from_logits (writes log_rhos / log-probs too) chained with overlap_previous."""
+    sets = [wl.make_inputs("large", seed=650 + i, B=8192, T=24) for i in range(2)]
+    devs = [_dev(x) for x in sets]
+    ref = [{k: v.clone() for k, v in pkg.from_logits(*[d[k] for k in NAMES], reward_mode=1).items()}
+           for d in devs]
+    ws = pkg.Workspace(24, 8192, 18, sets[0]["dtype"])
+    outs = [{k: torch.empty_like(v) for k, v in r.items()} for r in ref]
+    for i in range(6):
+        j = i % 2
+        pkg.loss_and_grad(*[devs[1 - j][k] for k in NAMES], reward_mode=1, workspace=ws,
+                          overlap_previous=True)
+        pkg.from_logits(*[devs[j][k] for k in NAMES], reward_mode=1, workspace=ws, out=outs[j],
+                        overlap_previous=True)
+    torch.cuda.synchronize()
+    for j in range(2):
+        for k in ref[j]:
+            assert torch.equal(outs[j][k], ref[j][k]), (j, k)
