@@ -254,7 +254,11 @@ def run_ours(args):
     # consecutive learner steps: each step's inputs are a fresh (rotated) trajectory
     # batch, never the previous step's outputs, so the step may overlap the previous
     # kernel's tail (programmatic dependent launch; --no-overlap: plain stream order)
-    kw_step = dict(kw, overlap_previous=not args.no_overlap)
+    # (single GPU only: with a side-stream NCCL collective per step, the next step's
+    # CTAs take every SM as the previous step's exit and the collective waits behind
+    # them -- measured 40.3 vs 37.9 us per step at N=2 -- so N > 1 keeps stream order)
+    overlap = not args.no_overlap and world == 1
+    kw_step = dict(kw, overlap_previous=overlap)
     s_main = torch.cuda.Stream()
     s_comm = torch.cuda.Stream()
 
@@ -417,8 +421,8 @@ def run_ours(args):
                    "l2": f"inputs rotated over {R} HBM-resident copies "
                          f"({R} x {working / 1e6:.1f} MB >= 4 x L2)",
                    "timing": graph_mode,
-                   "step_overlap": "none" if args.no_overlap else
-                   "programmatic dependent launch (overlap_previous: inputs are fresh batches)",
+                   "step_overlap": "programmatic dependent launch (overlap_previous: inputs are "
+                                   "fresh batches)" if overlap else "none",
                    "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream)"
                    if world > 1 else "none"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

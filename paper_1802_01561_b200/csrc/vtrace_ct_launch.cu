@@ -48,9 +48,13 @@ bool ct_plan_balanced(CtParams& C, int S) {
     return true;
   }
   const int tpc = (int)((R + S - 1) / S);
-  double best = 1e30;
+  // one-warp CTAs put ceil(N / S) tasks on an SM, i.e. ceil(that / 4) on its busiest
+  // sub-partition: the balanced split must beat that; and a task is cut into at most
+  // 2 segments (a longer chain serialises its segments' hand-overs; measured slower)
+  const double one_warp_max = (double)((((N + S - 1) / S) + 3) / 4);
+  double best = one_warp_max - 0.01;
   int best_p = 0;
-  for (int segs = 1; segs <= 4 && segs <= C.K; ++segs) {
+  for (int segs = 1; segs <= 2 && segs <= C.K; ++segs) {
     if (4 * f + segs * tpc > CTB_WARPS) continue;
     // every segment non-empty (a later one waits for the carry of an earlier one)
     const int sl = (C.K + segs - 1) / segs;
