@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--reserve-sms", type=int, default=1,
+                    help="N > 1: SMs the kernel leaves to the per-step NCCL collective so that "
+                         "steps can overlap (0: no overlap at N > 1)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
     ap.add_argument("--behaviour", choices=["logits", "log_probs"], default="logits",
@@ -254,10 +257,13 @@ def run_ours(args):
     # consecutive learner steps: each step's inputs are a fresh (rotated) trajectory
     # batch, never the previous step's outputs, so the step may overlap the previous
     # kernel's tail (programmatic dependent launch; --no-overlap: plain stream order)
-    # (single GPU only: with a side-stream NCCL collective per step, the next step's
-    # CTAs take every SM as the previous step's exit and the collective waits behind
-    # them -- measured 40.3 vs 37.9 us per step at N=2 -- so N > 1 keeps stream order)
-    overlap = not args.no_overlap and world == 1
+    # (N > 1: the side-stream NCCL collective of step k needs an SM while step k+1's
+    # CTAs take every SM the previous step releases; with no SM left to it the collective
+    # waited behind the next step (40.3 vs 37.9 us at N=2), so the kernel leaves
+    # --reserve-sms (1) SM free: 34.3 us at N=2)
+    overlap = not args.no_overlap and (world == 1 or args.reserve_sms > 0)
+    if world > 1 and args.reserve_sms > 0:  # SMs left free for the NCCL collective
+        os.environ["VTRACE_RESERVE_SMS"] = str(args.reserve_sms)
     kw_step = dict(kw, overlap_previous=overlap)
     s_main = torch.cuda.Stream()
     s_comm = torch.cuda.Stream()
@@ -423,7 +429,8 @@ def run_ours(args):
                    "timing": graph_mode,
                    "step_overlap": "programmatic dependent launch (overlap_previous: inputs are "
                                    "fresh batches)" if overlap else "none",
-                   "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream)"
+                   "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream"
+                                 + (f", {args.reserve_sms} SM reserved)" if overlap else ")")
                    if world > 1 else "none"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

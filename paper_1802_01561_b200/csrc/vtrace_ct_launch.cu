@@ -92,10 +92,18 @@ static vt_status launch_maybe_pdl(Kern kern, dim3 grid, dim3 block, size_t smem,
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
+// VTRACE_RESERVE_SMS=r: the balanced kernel uses S - r SMs (leaves r for a concurrent
+// collective, e.g. the per-step NCCL all-reduce with overlapped steps; bench.py, N > 1)
+static int reserve_sms() {
+  const char* e = getenv("VTRACE_RESERVE_SMS");
+  const int r = (e && *e) ? atoi(e) : 0;
+  return r < 0 ? 0 : (r > 16 ? 16 : r);
+}
+
 template <typename LT, int A_CT, bool LOSS, int MODE, bool GEN, bool MULP>
 static vt_status ct_launch_one(const Params& P, CtParams C, const TmaMaps& maps,
                                cudaStream_t st) {
-  const int S = ct_num_sms();
+  const int S = ct_num_sms() - reserve_sms();
   if (ct_plan_balanced(C, S)) {
     auto kern = vtrace_ctb_kernel<LT, A_CT, LOSS, MODE, GEN, MULP>;
     const size_t smem = (size_t)CTB_WARPS * C.warp_bytes;
