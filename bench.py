@@ -261,7 +261,11 @@ def run_ours(args):
     # CTAs take every SM the previous step releases; with no SM left to it the collective
     # waited behind the next step (40.3 vs 37.9 us at N=2), so the kernel leaves
     # --reserve-sms (1) SM free: 34.3 us at N=2)
-    overlap = not args.no_overlap and (world == 1 or args.reserve_sms > 0)
+    # (only the balanced kernel can leave SMs free; with one-warp CTAs the collective
+    # still waits -- strong scaling at N=2: 31.1 vs 25.7 us -- so those keep stream order)
+    overlap = not args.no_overlap and (
+        world == 1 or (args.reserve_sms > 0 and vt.kernel_for(T, B, A, inp["dtype"])
+                       == "vtrace_ctb_kernel"))
     if world > 1 and args.reserve_sms > 0:  # SMs left free for the NCCL collective
         os.environ["VTRACE_RESERVE_SMS"] = str(args.reserve_sms)
     kw_step = dict(kw, overlap_previous=overlap)
