@@ -450,3 +450,19 @@ def test_overlap_previous_from_logits_chain_bitwise():
     for j in range(2):
         for k in ref[j]:
             assert torch.equal(outs[j][k], ref[j][k]), (j, k)
+
+
+@pytest.mark.parametrize("T,B,A,dtype", [(5, 16, 1024, 0), (4, 9, 1024, 1), (3, 40, 700, 1),
+                                          (40, 4096, 64, 1), (33, 4096, 65, 1),
+                                          (9, 4100, 18, 1), (17, 4096, 18, 0)])
+def test_parity_edge_action_counts_and_widths(T, B, A, dtype):
+    """A at VT_MAX_ACTIONS (plain-load look-back path), A = 64 (the column-task kernel's
+    box limit 4A = 256) and A = 65 just past it, B not a multiple of 4 at column-task
+    widths, fp32 logits on the column-task path."""
+    inp = wl.make_inputs("large", seed=T + B + A, T=T, B=B, A=A, dtype=dtype)
+    lg, fl, ref_l, ref_f = run_both(inp)
+    check_all(inp, lg, fl, ref_l, ref_f)
+    import paper_1802_01561_b200 as p
+    assert p.kernel_for(T, B, A, dtype) in ("vtrace_ctb_kernel", "vtrace_ct_kernel",
+                                            "vtrace_fused_kernel",
+                                            "vtrace_fused_kernel (plain loads)")
