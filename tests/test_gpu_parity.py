@@ -466,3 +466,35 @@ def test_parity_edge_action_counts_and_widths(T, B, A, dtype):
     assert p.kernel_for(T, B, A, dtype) in ("vtrace_ctb_kernel", "vtrace_ct_kernel",
                                             "vtrace_fused_kernel",
                                             "vtrace_fused_kernel (plain loads)")
+
+
+@pytest.mark.parametrize("lp", [False, True])
+def test_data_errors_reported_column_task(lp):
+    """Data errors on the wide-batch kernel: the smallest offending row and its kind
+    (r3), with and without behaviour log-probs; the status word is read and cleared."""
+    inp = wl.make_inputs("large", seed=21, B=8192, T=30)
+    if lp:
+        inp = _with_behaviour_log_probs(inp)
+    ws = pkg.Workspace(inp["T"], inp["B"], inp["A"], inp["dtype"])
+    dev = _dev(inp)
+    pkg.loss_and_grad(*[dev[k] for k in NAMES], workspace=ws, reward_mode=1)
+    assert pkg.read_device_status(ws) == (0, -1)
+    bad = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    bad["actions"][25, 7000] = 18              # row 25 * 8192 + 7000
+    bad["rewards"][11, 4097] = np.inf          # row 11 * 8192 + 4097 (smallest)
+    bad["discounts"][29, 5] = -0.5
+    dev = _dev(bad)
+    pkg.loss_and_grad(*[dev[k] for k in NAMES], workspace=ws, reward_mode=1)
+    assert pkg.read_device_status(ws) == (3, 11 * 8192 + 4097)
+    assert pkg.read_device_status(ws) == (0, -1)
+    bad2 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in inp.items()}
+    bad2["bootstrap_value"][123] = np.nan
+    if lp:
+        bad2["behaviour_log_probs"][29, 8000] = np.nan
+        expect = (2, 29 * 8192 + 8000)
+    else:
+        bad2["values"][29, 8000] = np.nan
+        expect = (4, 29 * 8192 + 8000)
+    dev = _dev(bad2)
+    pkg.from_logits(*[dev[k] for k in NAMES], workspace=ws, reward_mode=1)
+    assert pkg.read_device_status(ws) == expect
