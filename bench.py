@@ -375,6 +375,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     kernel_ms = e0.elapsed_time(e1) / (reps * min(Kk, C))
 
+    # eager launches (no graph): the latency-bound configs' per-call time
+    Ke = min(K, 500)
+    with torch.cuda.stream(s_main):
+        for i in range(5):
+            step(i)
+    torch.cuda.synchronize()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for i in range(Ke):
+            step(i)
+        if world > 1:
+            s_main.wait_stream(s_comm)
+    ee1.record(s_main)
+    torch.cuda.synchronize()
+    eager_ms = max_over_ranks(ee0.elapsed_time(ee1), world) / Ke
+
     # end-to-end through the public host-input API
     e2e = None
     if not args.no_e2e:
@@ -404,9 +421,10 @@ def run_ours(args):
     if code != 0:
         raise SystemExit(f"device status reported data error {code} at row {idx}")
 
-    cpu = None
+    cpu = cpu_par = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(inp, args.cpu_seconds)
+        cpu_par = cpu_baseline_parallel(inp)
 
     if rank != 0:
         return
@@ -444,6 +462,8 @@ def run_ours(args):
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "cpu_baseline_parallel": cpu_par,
+        "eager_ms_per_step": eager_ms,
     }
     print(json.dumps(line), flush=True)
 
@@ -453,6 +473,8 @@ def run_ours(args):
 
 
 def cpu_baseline(inp, seconds):
+    """The oracle as it stands (single-threaded fp64) on the host cores: whole-batch
+    passes (or a column sample of one) repeated for about `seconds`."""
     import oracle
     from paper_1802_01561_b200 import workload as wl
     T, B = inp["T"], inp["B"]
@@ -463,13 +485,37 @@ def cpu_baseline(inp, seconds):
     rate_cols = small["B"] / max(dt, 1e-6)
     ncols = int(max(1, min(B, rate_cols * seconds)))
     sample = wl.column_slice(inp, 0, ncols)
-    t0 = time.perf_counter()
-    oracle.loss_and_grad(sample, reward_mode=inp["reward_mode"])
-    dt = time.perf_counter() - t0
-    return {"value": T * ncols / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    reps, t_all = 0, 0.0
+    while reps == 0 or (t_all < seconds and reps < 50):
+        t0 = time.perf_counter()
+        oracle.loss_and_grad(sample, reward_mode=inp["reward_mode"])
+        t_all += time.perf_counter() - t0
+        reps += 1
+    return {"value": T * ncols * reps / t_all, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"columns [0,{ncols}) of the {inp['T']}x{B} batch (T={T}), "
-                      f"oracle.loss_and_grad single-threaded fp64, {dt:.1f} s",
+                      f"oracle.loss_and_grad single-threaded fp64, {reps} pass(es) in {t_all:.1f} s",
             "host_cpu": _cpu_model()}
+
+
+def cpu_baseline_parallel(inp, passes=3):
+    """the same oracle function over column ranges on every host core
+    (ctypes releases the GIL during the call); whole-batch passes."""
+    import concurrent.futures as cf
+    import oracle
+    from paper_1802_01561_b200 import workload as wl
+    T, B = inp["T"], inp["B"]
+    n = max(1, min(os.cpu_count() or 1, B))
+    bounds = [(i * B // n, (i + 1) * B // n) for i in range(n)]
+    parts = [wl.column_slice(inp, b0, b1) for b0, b1 in bounds if b1 > b0]
+    oracle.loss_and_grad(parts[0], reward_mode=inp["reward_mode"])  # build / load first
+    with cf.ThreadPoolExecutor(max_workers=len(parts)) as ex:
+        t0 = time.perf_counter()
+        for _ in range(passes):
+            list(ex.map(lambda x: oracle.loss_and_grad(x, reward_mode=inp["reward_mode"]), parts))
+        dt = time.perf_counter() - t0
+    return {"value": T * B * passes / dt, "unit": UNIT, "cores": len(parts), "kind": "oracle",
+            "sample": f"the whole {T}x{B} batch, {passes} passes, columns split over "
+                      f"{len(parts)} threads, {dt:.1f} s", "host_cpu": _cpu_model()}
 
 
 def _cpu_model():
