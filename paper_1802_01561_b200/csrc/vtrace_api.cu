@@ -837,14 +837,17 @@ static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 // ---- column-task kernel selection ----------------------------------------------------
 constexpr long long kCtMinTasks = 1024;  // >= ~7 warps per SM
 
-static bool ct_enabled() {  // VTRACE_KERNEL=lookback forces the look-back kernel (tests)
+// VTRACE_KERNEL=lookback forces the look-back kernel, =ct the column-task kernel where
+// it applies (tests, A/B)
+static int kernel_override() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("VTRACE_KERNEL");
-    v = (e && e[0] == 'l') ? 0 : 1;
+    v = (e && e[0] == 'l') ? 0 : ((e && e[0] == 'c') ? 2 : 1);
   }
-  return v == 1;
+  return v;
 }
+static bool ct_enabled() { return kernel_override() != 0; }
 
 
 static vt_status check_params(const vt_vtrace_params* p) {
@@ -878,7 +881,11 @@ static KernelChoice choose_kernel(long long T, long long B, long long A, int ele
                    plan.Tc + 1 <= 256 && plan.smem <= kMaxSmem;
   if (!tma) return K_LOOKBACK_PLAIN;
   const long long tasks = (B + CT_COLS - 1) / CT_COLS;
-  const bool ct = ct_enabled() && tasks >= kCtMinTasks && (A * elem) % 4 == 0 &&
+  // wide batches, or short unrolls at any width: a task's ceil(T / 8) chunks then take
+  // less than the look-back pipeline's fixed latency (atari T=20: 5.4 vs 8.6 us)
+  const bool wide_or_short = tasks >= kCtMinTasks || (T + CT_STEPS - 1) / CT_STEPS <= 4;
+  const bool ct = ct_enabled() && (wide_or_short || kernel_override() == 2) &&
+                  (A * elem) % 4 == 0 &&
                   CT_COLS * A <= 256 && (B % CT_COLS) == 0 &&
                   (T + CT_STEPS) * B < (1LL << 31);  // 32-bit row offsets
   return ct ? K_CT : K_LOOKBACK_TMA;

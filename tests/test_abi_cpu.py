@@ -120,13 +120,15 @@ def test_binding_has_no_cpu_fallback(lib):
 
 def test_kernel_choice(lib):
     """Host-only query of the kernel a shape takes: wide batches (>= 1024 tasks of 4
-    trajectories) the column-task kernel, else the look-back kernel (TMA when the
-    pitches are 16-byte multiples)."""
+    trajectories) or short unrolls (<= 4 chunks of 8 steps) the column-task kernel,
+    else the look-back kernel (TMA when the pitches are 16-byte multiples)."""
     wide = ("vtrace_ct_kernel", "vtrace_ctb_kernel")  # ctb needs a device's SM count
     assert vt.kernel_for(100, 8192, 18, 1) in wide                        # large
     assert vt.kernel_for(100, 4096, 18, 1) in wide
     assert vt.kernel_for(100, 4092, 18, 1) == "vtrace_fused_kernel"       # 1023 tasks
     assert vt.kernel_for(2000, 1024, 9, 0) == "vtrace_fused_kernel"       # stress
+    assert vt.kernel_for(20, 32, 18, 0) == "vtrace_ct_kernel"             # atari: short T
+    assert vt.kernel_for(33, 32, 18, 0) == "vtrace_fused_kernel"          # 5 chunks
     assert vt.kernel_for(5, 2, 3, 0) == "vtrace_fused_kernel (plain loads)"  # toy: pitch 24 B
     assert vt.kernel_for(0, 8, 3, 0).startswith("none")
     assert vt.kernel_for(5, 8, 3, 7).startswith("none")
