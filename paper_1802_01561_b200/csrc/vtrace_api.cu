@@ -106,13 +106,14 @@ struct Unit {
 // units c, c + grid, ...  (unit ids run in reverse time order, so a unit only
 // ever waits, in the look-back, on units of earlier or the same rounds, all
 // resident).  Warp-specialised software pipeline over the CTA's units; in
-// iteration i:
-//   row warps 0..6 : P1(i)   row statistics + TD errors of unit i
-//   scan warp 7    : SCAN(i-1) the reverse recursion of unit i-1 (affine maps on
-//                    A = v - V), look-back, publication
+// iteration i (NWARPS = 6, 192 threads; a unit is 8 columns x Tc <= 20 steps):
+//   row warps 0..4 : P1(i)   row statistics + TD errors of unit i (one row per thread)
+//   scan warp 5    : SCAN(i-1) the reverse recursion of unit i-1 (affine maps on
+//                    A = v - V; 4 lanes per column, each over a segment of steps),
+//                    look-back on the later units' aggregates, publication
 //   thread 0       : waits for the TMA store of unit i-2's gradient, reloads that
 //                    stage with unit i+1
-//   -- barrier 1 (256 threads) --
+//   -- barrier 1 (192 threads) --
 //   row warps      : P3(i-1) v, pg_adv, dL/dV and dL/dz of unit i-1, dz written in
 //                    place over z^pi, then one TMA store
 // so the latency-bound recursion overlaps the row arithmetic of the next unit.
@@ -648,9 +649,9 @@ struct Plan {
 
 constexpr int kMaxCtas = 4096;  // bound on the persistent grid (workspace sizing)
 
-// Tc (steps per unit) depends only on (T, A, dtype): at most 32 so that a
-// unit's Tc * 8 rows map one-to-one onto the 256 threads, and small enough for
-// two input stages plus the staging tile to fit in shared memory.
+// Tc (steps per unit) depends only on (T, A, dtype): at most 20 so that a unit's
+// Tc * 8 rows map one-to-one onto the 160 row threads, and small enough for the
+// NSTAGE input stages plus the row-state buffers to fit in 100 KB of shared memory.
 static int tc_max_for(int A, int elem) {
   for (int tc = NROWTHREADS / BC; tc > 1; --tc)
     if (make_layout(tc * BC, A, elem).total <= 100 * 1024) return tc;

@@ -1,8 +1,10 @@
-// vtrace_kernels.cuh -- fused V-trace + actor-critic loss + gradient kernel for sm_100a.
+// vtrace_kernels.cuh -- shared types and device helpers of the fused V-trace +
+// actor-critic loss + gradient kernels for sm_100a (the look-back kernel in
+// vtrace_api.cu, the column-task kernels in vtrace_ct.cuh).
 //
-// A work unit = (column group of BC=8 trajectories) x (time chunk of Tc <= 32
-// steps); unit ids run in REVERSE time order.  A co-resident persistent grid
-// walks the units round-robin; the reverse V-trace recursion (Remark 1)
+// Look-back kernel: a work unit = (column group of BC=8 trajectories) x (time chunk
+// of Tc <= 20 steps); unit ids run in REVERSE time order.  A co-resident persistent
+// grid walks the units round-robin; the reverse V-trace recursion (Remark 1)
 // crosses chunk boundaries through a decoupled look-back on per-unit affine
 // aggregates (G, D):  A_start = D + G * A_end  with A = v - V.
 //
@@ -21,6 +23,8 @@
 // Precision: every quantity that feeds the recursion (sum_j exp, the ratio,
 // delta, the scan) is carried well beyond fp32 (fp64 or compensated fp32);
 // the gradient epilogue is fp32 (its outputs are fp32/bf16).  See DESIGN.md.
+// The column-task kernels (vtrace_ct.cuh) follow the same steps with one warp per
+// 4 trajectories over the whole unroll.
 #pragma once
 
 #include <cuda.h>
