@@ -44,6 +44,9 @@ def _extra_defines():
             extra.append("-D" + flag)
     if os.environ.get("VTRACE_ABLATE"):  # timing experiments only (wrong results)
         extra.append("-DVTRACE_ABLATE=" + os.environ["VTRACE_ABLATE"])
+    # A/B experiments: extra -D flags, separated by commas (e.g. "VT_CT_NSTAGE=5,FOO")
+    for d in filter(None, os.environ.get("VTRACE_DEFINES", "").split(",")):
+        extra.append("-D" + d)
     return extra
 
 

@@ -28,7 +28,10 @@ namespace vtb200 {
 constexpr int CT_COLS = 4;
 constexpr int CT_STEPS = 8;
 constexpr int CT_ROWS = CT_COLS * CT_STEPS;  // 32 == warp size
-constexpr int CT_NSTAGE = 4;                 // logits stages: chunks in flight + the one computed
+#ifndef VT_CT_NSTAGE
+#define VT_CT_NSTAGE 4  // (A/B: 3 same, 5 and 6 slower -- profiles/r1_perf_analysis.md)
+#endif
+constexpr int CT_NSTAGE = VT_CT_NSTAGE;      // logits stages: chunks in flight + the one computed
 constexpr int CT_WARPS = 1;                  // warps (tasks) per CTA
 static_assert(CT_ROWS == 32, "one row per lane");
 
