@@ -58,6 +58,13 @@ def parse():
                          "steps can overlap (0: no overlap at N > 1)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
+    ap.add_argument("--path", choices=["vtrace", "update"], default="vtrace",
+                    help="update: the learner's parameter update after the backward "
+                         "(SURVEY 8(f) NEXT #4: gradient all-reduce at N > 1, global-norm "
+                         "clip, RMSProp) instead of the V-trace path")
+    ap.add_argument("--update-size", default="deep",
+                    help="parameters of the update path: shallow (1.2M), deep (1.6M, "
+                         "P:285-286) or an integer")
     ap.add_argument("--behaviour", choices=["logits", "log_probs"], default="logits",
                     help="log_probs: the actors ship log mu(a_t) [T,B] instead of mu's "
                          "[T,B,A] logits (SURVEY 8(f) NEXT #2 input mode)")
@@ -571,10 +578,149 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# --path update: the learner's parameter update
+
+
+def run_update(args):
+    """K synchronous learner updates of n parameters: (N > 1) NCCL SUM all-reduce of
+    the fp32 gradient, then vtrace_rmsprop_step (clip 40, RMSProp) on every
+    replica.  `value` = parameters updated per second (the replicas update the same
+    parameters: the job's rate, not N times it)."""
+    world, rank, local = dist_env()
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dist = init_dist(world, local)
+    torch.cuda.set_device(local)
+    import paper_1802_01561_b200 as pkg
+    from paper_1802_01561_b200 import learner
+    from paper_1802_01561_b200 import workload as wl
+    size = args.update_size
+    n = wl.UPDATE_SIZES[size] if size in wl.UPDATE_SIZES else int(size)
+    inp = wl.update_inputs(n, seed=1 + rank, norm=80.0 / math.sqrt(world))
+    lr, decay, eps, clip = 6e-4, 0.99, 0.01, 40.0  # P:950-953 (decay: reading r9)
+    per = 3 * 4 * n  # params, mean square, grads resident per copy
+    R = max(1, math.ceil(4 * L2_BYTES / per))
+    theta = [torch.from_numpy(inp["params"]).cuda() for _ in range(R)]
+    ms = [torch.from_numpy(inp["mean_square"]).cuda() for _ in range(R)]
+    grads = [torch.from_numpy(inp["grads"][0]).cuda() for _ in range(R)]
+    norm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = pkg.RmspropWorkspace(n)
+    s_main = torch.cuda.Stream()
+
+    red = torch.empty_like(grads[0]) if world > 1 else None
+
+    def step(i, allreduce=True):
+        j = i % R
+        g = grads[j]
+        if allreduce and world > 1:
+            # a fresh local gradient each step (the backward's output), summed in place
+            red.copy_(grads[j])
+            learner.allreduce_grads(red)
+            g = red
+        pkg.rmsprop_step(theta[j], ms[j], g, lr, decay, eps, clip,
+                         global_norm_out=norm, workspace=ws)
+
+    with torch.cuda.stream(s_main):
+        for i in range(max(args.warmup, 3)):
+            step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    K = args.steps
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tw0 = time.time()
+    e0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for i in range(K):
+            step(i)
+    e1.record(s_main)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    barrier(world)
+    if sampler:
+        sampler.stop()
+    step_ms = max_over_ranks(e0.elapsed_time(e1), world) / K
+    # the update kernel alone (roofline): same loop without the collective
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for i in range(K):
+            step(i, allreduce=False)
+    k1.record(s_main)
+    torch.cuda.synchronize()
+    kernel_ms = max_over_ranks(k0.elapsed_time(k1), world) / K
+    # end to end: this step's gradient from pinned host memory, the norm read back
+    e2e = None
+    if not args.no_e2e:
+        g_host = torch.from_numpy(inp["grads"][0]).pin_memory()
+        n_host = torch.zeros(1, dtype=torch.float64).pin_memory()
+        Ke = min(K, 200)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s_main)
+        with torch.cuda.stream(s_main):
+            for i in range(Ke):
+                grads[i % R].copy_(g_host, non_blocking=True)
+                step(i)
+                n_host.copy_(norm, non_blocking=True)
+        a1.record(s_main)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(a0.elapsed_time(a1), world) / Ke
+        e2e = {"value": n / (e2e_ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import rmsprop_oracle as ro
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < min(args.cpu_seconds, 5.0) or reps == 0:
+            ro.rmsprop_step(inp["params"], inp["mean_square"], inp["grads"][0], lr, decay, eps,
+                            clip)
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        cpu = {"value": n / dt, "unit": "params/s", "cores": 1, "kind": "oracle",
+               "sample": f"{reps} full updates of the same {n} parameters (numpy fp64)"}
+    if rank != 0:
+        return
+    peak, peak_src = load_peak()
+    alg = 20 * n  # g 4 B + ms 4+4 B + theta 4+4 B per parameter
+    achieved = alg / (kernel_ms * 1e-3) / 1e9
+    line = {
+        "metric": "learner_update_params_per_s", "value": n / (step_ms * 1e-3),
+        "unit": "params/s", "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "replicated",
+        "vs_baseline": None, "dtype": "f32 (f64 global norm)", "path": "update",
+        "data": "synthetic (seeded gradient of global norm 80, N(0, 0.05^2) parameters)",
+        "config": {"workload": f"learner update, {size} model ({n} parameters)",
+                   "n_params": n, "optimizer": "RMSProp momentum 0, decay 0.99, eps 0.01, "
+                   "lr 6e-4, clip global norm 40 (P:950-953)",
+                   "collective": "per step: copy of the local fp32 gradient + NCCL all_reduce "
+                                 "SUM of it" if world > 1 else "none",
+                   "l2": f"state rotated over {R} HBM-resident copies ({R} x {per / 1e6:.1f} MB "
+                         ">= 4 x L2)", "parallelism": f"dp{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "rmsprop_kernel",
+                     "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg,
+                     "peak_source": peak_src},
+        "gpu_launches": K,
+        "clocks": sampler.summary(tw0, tw1) if sampler else None,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 if __name__ == "__main__":
     a = parse()
     try:
-        if a.impl == "reference":
+        if a.path == "update":
+            if a.impl == "reference":
+                print(json.dumps({"impl": "reference", "path": "update", "unavailable":
+                                  "the update path's CPU baseline is in the ours line"}))
+            else:
+                run_update(a)
+        elif a.impl == "reference":
             run_reference(a)
         else:
             run_ours(a)

@@ -237,6 +237,43 @@ int32_t vtrace_version(void);
  * roofline line describes. */
 const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype);
 
+/* ---- The learner's parameter update -------------------
+ * The step after the network backward: clip the global gradient norm at
+ * max_global_norm (40), then RMSProp with momentum 0.
+ * The paper gives no formula; the TensorFlow form is used (its implementation is
+ * TF), epsilon inside the square root (readings r9, r10):
+ *     g'    = g * c / max(||g||_2, c)          (||.|| over all n parameters)
+ *     ms    <- decay * ms + (1 - decay) * g'^2
+ *     theta <- theta - lr * g' / sqrt(ms + epsilon)
+ * With several learners the caller first SUM-all-reduces the
+ * gradient (the loss is summed over the batch; reading r11), then every
+ * learner applies the same update to its replica. */
+typedef struct {
+  float learning_rate;   /* > 0; the paper anneals it linearly to 0, caller's job */
+  float decay;           /* RMSProp mean-square decay, in [0, 1) (not given by the paper)  */
+  float epsilon;         /* > 0, inside the square root (0.01; sweep P:786)        */
+  float max_global_norm; /* > 0: clip threshold c (40); 0: no clipping             */
+} vt_rmsprop_params;
+
+/* Workspace bytes for vtrace_rmsprop_step (initialise once with
+ * vtrace_workspace_init; not shared with a V-trace call or a concurrent update). */
+size_t vtrace_rmsprop_workspace_bytes(int64_t n);
+
+/* One clipped RMSProp step over n fp32 parameters, in place.
+ *   params       theta [n]  fp32 device, updated in place
+ *   mean_square  ms    [n]  fp32 device, updated in place (the caller initialises it)
+ *   grads        g     [n]  fp32 device, read only (the batch's summed gradient)
+ *   global_norm_out         optional fp64 device scalar: ||g||_2 before clipping
+ * The three arrays must not overlap; 4-byte alignment is required, 16-byte
+ * alignment of all three takes the vector path.  n = 0 is a no-op (norm 0).
+ * Non-finite gradients propagate (the norm reports them).  Errors: VT_ERR_INVALID_ARG
+ * (NULL array), VT_ERR_SHAPE (n < 0), VT_ERR_PARAM (see the struct), VT_ERR_ALIGNMENT,
+ * VT_ERR_WORKSPACE, VT_ERR_DEVICE, VT_ERR_CUDA.  One cooperative launch (one CTA
+ * per SM) on `stream`; deterministic (fixed reduction order). */
+vt_status vtrace_rmsprop_step(int64_t n, float* params, float* mean_square, const float* grads,
+                              const vt_rmsprop_params* prm, double* global_norm_out,
+                              void* workspace, size_t workspace_bytes, vt_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

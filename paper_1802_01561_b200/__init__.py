@@ -7,8 +7,8 @@ fallback.
 """
 from . import workload  # noqa: F401
 from .vtrace import (  # noqa: F401
-    VtraceError, Workspace, from_logits, kernel_for, load_library, loss_and_grad,
-    loss_and_grad_from_host, read_device_status, status_string, tensors_from_workload, version,
-    workspace_bytes)
+    RmspropWorkspace, VtraceError, Workspace, from_logits, kernel_for, load_library, loss_and_grad,
+    loss_and_grad_from_host, read_device_status, rmsprop_step, status_string,
+    tensors_from_workload, version, workspace_bytes)
 
 __version__ = "0.1.0"

@@ -47,3 +47,17 @@ def gradient_norm(partials: torch.Tensor) -> float:
     """sqrt(sum dL/dz^2 + sum dL/dV^2) of the (reduced) partials (reading c17)."""
     p = partials.detach().to("cpu", torch.float64)
     return float(torch.sqrt(p[4] + p[5]))
+
+
+def allreduce_grads(grads: torch.Tensor, group=None, async_op: bool = False):
+    """SUM all-reduce, in place, of a learner's parameter gradient before the
+    update: the loss is summed over the batch, so the
+    whole batch's gradient is the sum of the learners' shard gradients (reading
+    r11); every learner then runs the same vtrace_rmsprop_step on its replica
+    (synchronous update).  NCCL on GPUs, gloo in the CPU tests."""
+    import torch.distributed as dist
+    if not grads.is_floating_point():
+        raise ValueError("grads must be a floating-point tensor")
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return None
+    return dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group, async_op=async_op)

@@ -34,7 +34,7 @@ DATA_ERRORS = {0: "ok", 1: "action", 2: "logits", 3: "reward", 4: "value", 5: "d
 EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_from_logits",
                     "vtrace_loss_and_grad", "vtrace_loss_and_grad_from_host",
                     "vtrace_read_device_status", "vtrace_status_string", "vtrace_version",
-                    "vtrace_kernel_for")
+                    "vtrace_kernel_for", "vtrace_rmsprop_workspace_bytes", "vtrace_rmsprop_step")
 
 
 class VtraceError(RuntimeError):
@@ -53,6 +53,11 @@ class _Params(ctypes.Structure):
 
 # vt_correction: Section 5.2.2 off-policy correction variants
 CORRECTION_VTRACE, CORRECTION_NONE, CORRECTION_EPSILON, CORRECTION_ONE_STEP_IS = 0, 1, 2, 3
+
+
+class _RmsParams(ctypes.Structure):  # vt_rmsprop_params
+    _fields_ = [("learning_rate", ctypes.c_float), ("decay", ctypes.c_float),
+                ("epsilon", ctypes.c_float), ("max_global_norm", ctypes.c_float)]
 
 
 class _Weights(ctypes.Structure):
@@ -95,6 +100,11 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_version.restype = ctypes.c_int32
     lib.vtrace_kernel_for.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
     lib.vtrace_kernel_for.restype = ctypes.c_char_p
+    lib.vtrace_rmsprop_workspace_bytes.argtypes = [i64]
+    lib.vtrace_rmsprop_workspace_bytes.restype = ctypes.c_size_t
+    lib.vtrace_rmsprop_step.argtypes = [i64, P, P, P, ctypes.POINTER(_RmsParams), P, P,
+                                        ctypes.c_size_t, P]
+    lib.vtrace_rmsprop_step.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -336,3 +346,44 @@ __all__ = ["workspace_bytes", "Workspace", "from_logits", "loss_and_grad",
            "loss_and_grad_from_host", "read_device_status", "status_string", "version",
            "tensors_from_workload", "VtraceError", "load_library"]
 
+
+# ---- the learner's parameter update (include/vtrace.h) ----
+
+class RmspropWorkspace(Workspace):
+    """Device workspace of vtrace_rmsprop_step: allocated once, initialised once."""
+
+    def __init__(self, n: int, device=None):  # noqa: D107 (same layout rules as Workspace)
+        nbytes = int(load_library().vtrace_rmsprop_workspace_bytes(int(n)))
+        if nbytes == 0:
+            raise ValueError("bad size for the rmsprop workspace")
+        self.device = torch.device(device if device is not None else "cuda")
+        self.nbytes = nbytes
+        self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        off = (-self.buf.data_ptr()) % 256
+        self.tensor = self.buf[off:off + nbytes]
+        _check(load_library().vtrace_workspace_init(_ptr(self.tensor), nbytes,
+                                                   _stream(self.device)),
+               "vtrace_workspace_init")
+
+
+def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
+                 epsilon: float, max_global_norm: float = 40.0, global_norm_out=None,
+                 workspace: RmspropWorkspace | None = None):
+    """Clipped RMSProp step (momentum 0) in place on fp32 CUDA tensors of equal size
+    (DESIGN.md r9-r11).  `global_norm_out`: optional float64 CUDA
+    tensor of 1 element receiving ||grads||_2 before clipping."""
+    for t in (params, mean_square, grads):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError("params, mean_square, grads must be contiguous fp32 CUDA tensors")
+    n = params.numel()
+    if mean_square.numel() != n or grads.numel() != n:
+        raise ValueError("params, mean_square and grads must have the same size")
+    if global_norm_out is not None and not (global_norm_out.is_cuda and
+                                            global_norm_out.dtype == torch.float64):
+        raise ValueError("global_norm_out must be a float64 CUDA tensor")
+    ws = workspace if workspace is not None else RmspropWorkspace(n, params.device)
+    prm = _RmsParams(float(learning_rate), float(decay), float(epsilon), float(max_global_norm))
+    _check(load_library().vtrace_rmsprop_step(n, _ptr(params), _ptr(mean_square), _ptr(grads),
+                                              ctypes.byref(prm), _ptr(global_norm_out), ws.ptr,
+                                              ws.nbytes, _stream(params.device)),
+           "vtrace_rmsprop_step")

@@ -162,3 +162,22 @@ def column_slice(inp: dict, b0: int, b1: int) -> dict:
             out[k] = np.ascontiguousarray(inp[k][:, b0:b1])
     out["bootstrap_value"] = np.ascontiguousarray(inp["bootstrap_value"][b0:b1])
     return out
+
+
+# ---- inputs of the learner's parameter update -------------
+# The paper's networks have 1.2 M (shallow) and 1.6 M (deep) parameters;
+# there is no network here, so the gradient is synthetic: per-parameter N(0, s^2)
+# with s chosen so the global norm is `norm` (default 80: above the clip of 40,
+# P:953), parameters N(0, 0.05^2), mean squares U(0.5, 1.5) (a run in progress).
+UPDATE_SIZES = {"shallow": 1_200_000, "deep": 1_600_000}
+
+
+def update_inputs(n: int, seed: int = 0, norm: float = 80.0, learners: int = 1) -> dict:
+    """fp32 numpy params [n], mean_square [n] and one gradient [n] per learner
+    (their sum has global norm ~`norm`)."""
+    rng = np.random.default_rng(seed)
+    params = rng.normal(0.0, 0.05, size=n).astype(np.float32)
+    ms = rng.uniform(0.5, 1.5, size=n).astype(np.float32)
+    s = norm / np.sqrt(max(n, 1) * learners)
+    grads = [rng.normal(0.0, s, size=n).astype(np.float32) for _ in range(learners)]
+    return {"n": n, "params": params, "mean_square": ms, "grads": grads}

@@ -140,3 +140,27 @@ def test_behaviour_log_prob_param_check(lib):
 
 def test_overlap_previous_param_check(lib):
     assert _call_loss(lib, params=vt.params(overlap_previous=2)) == 4
+
+
+def _rms(lib, n=10, p=16, m=32, g=48, prm=None, ws=None, wsb=0, norm=None):
+    prm = prm if prm is not None else vt._RmsParams(6e-4, 0.99, 0.01, 40.0)
+    c = (lambda x: None if x is None else ctypes.c_void_p(x))
+    return lib.vtrace_rmsprop_step(n, c(p), c(m), c(g), ctypes.byref(prm), c(norm), c(ws), wsb,
+                                   None)
+
+
+def test_rmsprop_host_checks(lib):
+    """vtrace_rmsprop_step (NEXT #4) rejects bad arguments before any launch."""
+    assert lib.vtrace_rmsprop_workspace_bytes(1_600_000) >= 256 + 16 * 148
+    assert lib.vtrace_rmsprop_workspace_bytes(-1) == 0
+    assert _rms(lib, p=None) == 1                                  # INVALID_ARG
+    assert _rms(lib, n=-1) == 2                                    # SHAPE
+    for bad in ((0.0, 0.99, 0.01, 40.0), (float("nan"), 0.99, 0.01, 40.0),
+                (6e-4, 1.0, 0.01, 40.0), (6e-4, -0.1, 0.01, 40.0), (6e-4, 0.99, 0.0, 40.0),
+                (6e-4, 0.99, 0.01, -1.0), (6e-4, 0.99, 0.01, float("inf"))):
+        assert _rms(lib, prm=vt._RmsParams(*bad)) == 4, bad          # PARAM
+    assert _rms(lib, p=18) == 5                                    # ALIGNMENT
+    assert _rms(lib, norm=20) == 5
+    assert _rms(lib) == 6                                          # WORKSPACE (NULL)
+    assert _rms(lib, ws=256, wsb=16) == 6                          # too small
+    assert _rms(lib, ws=300, wsb=1 << 20) == 6                     # not 256-aligned

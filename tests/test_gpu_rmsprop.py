@@ -1,0 +1,161 @@
+"""GPU parity of the learner update (vtrace_rmsprop_step)
+against the fp64 oracle (oracle/rmsprop_oracle.py), through the C ABI.
+
+Tolerance (learner update): the kernel computes in fp32 with IEEE sqrt
+and division, so the new mean square is within a few fp32 ulps (rtol 1e-6) and the
+new parameter within 1e-6 of the step size plus 2 ulps of the parameter.  The
+hyperparameters cross the ABI as fp32; the oracle gets those same fp32 values.
+The clip decision and the norm are fp64 on both sides (norm rtol 1e-12).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_1802_01561_b200 as pkg
+from oracle import rmsprop_oracle as ro
+from paper_1802_01561_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+LR, DECAY, EPS, CLIP = 6e-4, 0.99, 0.01, 40.0  # P:950-953 (decay: reading r9)
+
+
+def _f32(x):
+    return float(np.float32(x))
+
+
+def _check(theta_gpu, ms_gpu, theta0, theta_ref, ms_ref):
+    step = np.abs(theta_ref - np.asarray(theta0, np.float64))
+    err = np.abs(theta_gpu.astype(np.float64) - theta_ref)
+    bound = 1e-6 * step + 2.4e-7 * np.abs(theta_ref) + 1e-30
+    worst = float(np.max(err / bound)) if err.size else 0.0
+    assert worst <= 1.0, f"theta off by {worst:.3f} x tolerance"
+    np.testing.assert_allclose(ms_gpu.astype(np.float64), ms_ref, rtol=1e-6, atol=1e-30)
+
+
+def _run(inp, lr=LR, decay=DECAY, eps=EPS, clip=CLIP, offset=0, steps=1, ws=None):
+    dev = "cuda"
+    n = inp["n"]
+
+    def put(x):  # `offset` elements in: a 4-byte-aligned, not 16-byte-aligned view
+        buf = torch.zeros(n + offset, dtype=torch.float32, device=dev)
+        buf[offset:] = torch.from_numpy(np.ascontiguousarray(x))
+        return buf[offset:]
+
+    theta, ms = put(inp["params"]), put(inp["mean_square"])
+    norm = torch.zeros(1, dtype=torch.float64, device=dev)
+    ws = ws if ws is not None else pkg.RmspropWorkspace(n, dev)
+    norms = []
+    for k in range(steps):
+        g = put(inp["grads"][k % len(inp["grads"])])
+        pkg.rmsprop_step(theta, ms, g, lr, decay, eps, clip, global_norm_out=norm, workspace=ws)
+        norms.append(float(norm.item()))
+    torch.cuda.synchronize()
+    return theta.cpu().numpy(), ms.cpu().numpy(), norms
+
+
+def _oracle(inp, lr=LR, decay=DECAY, eps=EPS, clip=CLIP, steps=1):
+    theta, ms = inp["params"].astype(np.float64), inp["mean_square"].astype(np.float64)
+    norms = []
+    for k in range(steps):
+        theta, ms, nrm = ro.rmsprop_step(theta, ms, inp["grads"][k % len(inp["grads"])],
+                                         _f32(lr), _f32(decay), _f32(eps), _f32(clip))
+        norms.append(nrm)
+    return theta, ms, norms
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 7, 1000, 4099, 262147, 1_600_000])
+@pytest.mark.parametrize("norm", [80.0, 10.0])
+def test_rmsprop_matches_oracle(n, norm):
+    inp = wl.update_inputs(n, seed=n % 97, norm=norm)
+    th, ms, nr = _run(inp)
+    th_ref, ms_ref, nr_ref = _oracle(inp)
+    _check(th, ms, inp["params"], th_ref, ms_ref)
+    assert nr[0] == pytest.approx(nr_ref[0], rel=1e-12)
+    assert (nr_ref[0] > CLIP) == (norm > CLIP)
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_rmsprop_unaligned_views_take_the_scalar_path(offset):
+    inp = wl.update_inputs(5003, seed=offset, norm=80.0)
+    th, ms, nr = _run(inp, offset=offset)
+    th_ref, ms_ref, nr_ref = _oracle(inp)
+    _check(th, ms, inp["params"], th_ref, ms_ref)
+    assert nr[0] == pytest.approx(nr_ref[0], rel=1e-12)
+
+
+def test_rmsprop_successive_steps_share_a_workspace():
+    # the workspace's epoch tags separate the calls' partial-sum records
+    inp = wl.update_inputs(300_001, seed=2, norm=60.0, learners=3)  # 3 different gradients
+    th, ms, nr = _run(inp, steps=5)
+    th_ref, ms_ref, nr_ref = _oracle(inp, steps=5)
+    step = np.abs(th_ref - inp["params"])
+    err = np.abs(th.astype(np.float64) - th_ref)
+    assert np.max(err / (5e-6 * step + 1e-6 * np.abs(th_ref) + 1e-30)) <= 1.0
+    np.testing.assert_allclose(ms, ms_ref, rtol=5e-6)
+    np.testing.assert_allclose(nr, nr_ref, rtol=1e-12)
+
+
+def test_rmsprop_clip_disabled_and_lr_decay_extremes():
+    inp = wl.update_inputs(70_000, seed=8, norm=500.0)
+    for kw in ({"clip": 0.0}, {"decay": 0.0}, {"decay": 0.999, "eps": 1e-7}, {"eps": 0.1}):
+        th, ms, _ = _run(inp, **kw)
+        th_ref, ms_ref, _ = _oracle(inp, **kw)
+        _check(th, ms, inp["params"], th_ref, ms_ref)
+
+
+def test_rmsprop_zero_gradient_and_empty():
+    inp = wl.update_inputs(4096, seed=1)
+    inp["grads"] = [np.zeros(4096, np.float32)]
+    th, ms, nr = _run(inp)
+    assert nr[0] == 0.0
+    assert np.array_equal(th, inp["params"])
+    np.testing.assert_allclose(ms, _f32(DECAY) * inp["mean_square"].astype(np.float64), rtol=1e-6)
+    empty = torch.zeros(0, dtype=torch.float32, device="cuda")
+    norm = torch.full((1,), 7.0, dtype=torch.float64, device="cuda")
+    pkg.rmsprop_step(empty, empty.clone(), empty.clone(), LR, DECAY, EPS, CLIP,
+                     global_norm_out=norm)
+    assert float(norm.item()) == 0.0
+
+
+def test_rmsprop_is_deterministic():
+    inp = wl.update_inputs(1_200_000, seed=6, norm=45.0)
+    a = _run(inp)
+    b = _run(inp)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+def test_rmsprop_in_a_cuda_graph():
+    inp = wl.update_inputs(400_003, seed=3, norm=90.0, learners=2)
+    dev = "cuda"
+    theta = torch.from_numpy(inp["params"]).to(dev)
+    ms = torch.from_numpy(inp["mean_square"]).to(dev)
+    g = torch.from_numpy(inp["grads"][0]).to(dev)
+    ws = pkg.RmspropWorkspace(inp["n"], dev)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            pkg.rmsprop_step(theta, ms, g, LR, DECAY, EPS, CLIP, workspace=ws)
+    torch.cuda.synchronize()
+    # capture does not run the kernel: reset, then replay twice with two gradients
+    theta.copy_(torch.from_numpy(inp["params"]))
+    ms.copy_(torch.from_numpy(inp["mean_square"]))
+    for k in range(2):
+        g.copy_(torch.from_numpy(inp["grads"][k]))
+        graph.replay()
+    torch.cuda.synchronize()
+    th_ref, ms_ref, _ = _oracle(inp, steps=2)
+    step = np.abs(th_ref - inp["params"])
+    err = np.abs(theta.cpu().numpy().astype(np.float64) - th_ref)
+    assert np.max(err / (3e-6 * step + 1e-6 * np.abs(th_ref) + 1e-30)) <= 1.0
+    np.testing.assert_allclose(ms.cpu().numpy(), ms_ref, rtol=3e-6)
+
+
+def test_rmsprop_errors_raise():
+    t = torch.zeros(8, dtype=torch.float32, device="cuda")
+    with pytest.raises(pkg.VtraceError):
+        pkg.rmsprop_step(t, t.clone(), t.clone(), 0.0, DECAY, EPS, CLIP)
+    with pytest.raises(ValueError):
+        pkg.rmsprop_step(t, t.clone(), torch.zeros(9, device="cuda"), LR, DECAY, EPS, CLIP)

@@ -80,3 +80,49 @@ def test_shard_columns_cover():
 def test_gradient_norm():
     p = torch.tensor([0, 0, 0, 0, 9.0, 16.0, 0, 0], dtype=torch.float64)
     assert learner.gradient_norm(p) == 5.0
+
+
+def _grad_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import rmsprop_oracle as ro
+        from paper_1802_01561_b200 import workload as wl
+        inp = wl.update_inputs(1000, seed=4, learners=world)
+        g = torch.from_numpy(inp["grads"][rank].astype(np.float64))
+        learner.allreduce_grads(g)  # SUM over learners (reading r11)
+        theta, ms, norm = ro.rmsprop_step(inp["params"], inp["mean_square"], g.numpy(),
+                                          6e-4, 0.99, 0.01, 40.0)
+        q.put((rank, g.numpy().copy(), theta, ms, norm))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gradient_allreduce_gives_identical_replicas():
+    """NEXT #4 host logic: the learners' gradients are summed (NCCL on GPUs, gloo
+    here) and every learner applies the same clipped RMSProp step: the replicas
+    agree bitwise and equal one learner updating with the whole batch's gradient."""
+    from oracle import rmsprop_oracle as ro
+    from paper_1802_01561_b200 import workload as wl
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    inp = wl.update_inputs(1000, seed=4, learners=world)
+    total = ro.sum_learner_grads(inp["grads"])
+    theta, ms, norm = ro.rmsprop_step(inp["params"], inp["mean_square"], total, 6e-4, 0.99,
+                                      0.01, 40.0)
+    assert norm > 40.0  # the clip is active
+    (_, g0, t0, m0, n0), (_, g1, t1, m1, n1) = res
+    assert np.array_equal(g0, g1) and np.array_equal(t0, t1) and np.array_equal(m0, m1)
+    np.testing.assert_allclose(g0, total, rtol=1e-15)
+    np.testing.assert_allclose(t0, theta, rtol=1e-14)
+    assert n0 == pytest.approx(norm, rel=1e-14)
