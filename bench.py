@@ -62,6 +62,10 @@ def parse():
                     help="update: the learner's parameter update after the backward "
                          "(SURVEY 8(f) NEXT #4: gradient all-reduce at N > 1, global-norm "
                          "clip, RMSProp) instead of the V-trace path")
+    ap.add_argument("--update-collective", choices=["symm", "nccl"], default="symm",
+                    help="N > 1 on the update path: symm = the kernel sums every learner's "
+                         "gradient over NVLink from symmetric memory (fused); nccl = NCCL "
+                         "all_reduce then the single-gradient kernel")
     ap.add_argument("--update-size", default="deep",
                     help="parameters of the update path: shallow (1.2M), deep (1.6M, "
                          "P:285-286) or an integer")
@@ -597,7 +601,11 @@ def run_update(args):
     from paper_1802_01561_b200 import workload as wl
     size = args.update_size
     n = wl.UPDATE_SIZES[size] if size in wl.UPDATE_SIZES else int(size)
-    inp = wl.update_inputs(n, seed=1 + rank, norm=80.0 / math.sqrt(world))
+    # replicas start equal (one seed for parameters and mean squares); each learner
+    # has its own gradient (its shard of the batch)
+    inp = wl.update_inputs(n, seed=1, norm=80.0 / math.sqrt(world))
+    if rank > 0:
+        inp["grads"] = wl.update_inputs(n, seed=1 + rank, norm=80.0 / math.sqrt(world))["grads"]
     lr, decay, eps, clip = 6e-4, 0.99, 0.01, 40.0  # P:950-953 (decay: reading r9)
     per = 3 * 4 * n  # params, mean square, grads resident per copy
     R = max(1, math.ceil(4 * L2_BYTES / per))
@@ -608,10 +616,36 @@ def run_update(args):
     ws = pkg.RmspropWorkspace(n)
     s_main = torch.cuda.Stream()
 
-    red = torch.empty_like(grads[0]) if world > 1 else None
+    symm = world > 1 and args.update_collective == "symm"
+    red = hdl = ptrs = None
+    if symm:
+        # the learners' gradient buffers in symmetric memory: every GPU maps every
+        # other's, and the update kernel sums them (rank order) over NVLink
+        import torch.distributed._symmetric_memory as symm_mem
+        red = symm_mem.empty(n, dtype=torch.float32, device="cuda")
+        hdl = symm_mem.rendezvous(red, dist.group.WORLD.group_name)
+        ptrs = [int(p) for p in hdl.buffer_ptrs]
+        # each learner's {ready, done} words: the learners synchronise inside the kernel
+        flg = symm_mem.empty(2, dtype=torch.int32, device="cuda")
+        flg.zero_()
+        hdl_f = symm_mem.rendezvous(flg, dist.group.WORLD.group_name)
+        fptrs = [int(p) for p in hdl_f.buffer_ptrs]
+        torch.cuda.synchronize()
+        barrier(world)
+    elif world > 1:
+        red = torch.empty_like(grads[0])
 
     def step(i, allreduce=True):
         j = i % R
+        if symm:
+            if allreduce:
+                red.copy_(grads[j])      # this step's local gradient (the backward's output)
+            # every learner's buffer summed over NVLink in rank order; ready / done flags
+            # inside the kernel replace the barriers around it
+            pkg.rmsprop_step(theta[j], ms[j], ptrs, lr, decay, eps, clip,
+                             global_norm_out=norm, workspace=ws, learner_flags=fptrs,
+                             self_index=rank)
+            return
         g = grads[j]
         if allreduce and world > 1:
             # a fresh local gradient each step (the backward's output), summed in place
@@ -627,31 +661,85 @@ def run_update(args):
     torch.cuda.synchronize()
     barrier(world)
     K = args.steps
+
+    # eager Python loop (host launch rate included)
+    Ke = min(K, 500)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for i in range(Ke):
+            step(i)
+    q1.record(s_main)
+    torch.cuda.synchronize()
+    eager_ms = max_over_ranks(q0.elapsed_time(q1), world) / Ke
+
+    # CUDA graphs of R consecutive steps (one per rotated copy), replayed: exactly K
+    def capture(nsteps, allreduce=True):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s_main):
+            for i in range(nsteps):
+                step(i, allreduce)
+        return g
+
+    n_full, rem = divmod(K, R)
+    timing_mode = "cuda-graph of R steps, replayed (eager loop: eager_ms_per_step)"
+    try:
+        g_full, g_rem = capture(R), (capture(rem) if rem else None)
+    except Exception as e:  # (a collective that cannot be captured: eager timing)
+        g_full = g_rem = None
+        timing_mode = f"eager (capture failed: {type(e).__name__})"
+    torch.cuda.synchronize()
+    barrier(world)
+
+    def timed(gf, gr, allreduce=True):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(s_main)
+        with torch.cuda.stream(s_main):
+            if gf is None:
+                for i in range(K):
+                    step(i, allreduce)
+            else:
+                for _ in range(n_full):
+                    gf.replay()
+                if gr is not None:
+                    gr.replay()
+        t1.record(s_main)
+        torch.cuda.synchronize()
+        return max_over_ranks(t0.elapsed_time(t1), world) / K
+
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tw0 = time.time()
-    e0.record(s_main)
-    with torch.cuda.stream(s_main):
-        for i in range(K):
-            step(i)
-    e1.record(s_main)
-    torch.cuda.synchronize()
+    step_ms = timed(g_full, g_rem)
     tw1 = time.time()
     barrier(world)
     if sampler:
         sampler.stop()
-    step_ms = max_over_ranks(e0.elapsed_time(e1), world) / K
-    # the update kernel alone (roofline): same loop without the collective
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(s_main)
-    with torch.cuda.stream(s_main):
-        for i in range(K):
-            step(i, allreduce=False)
-    k1.record(s_main)
-    torch.cuda.synchronize()
-    kernel_ms = max_over_ranks(k0.elapsed_time(k1), world) / K
+    # the replicas must agree bitwise (same buffers, same order, same arithmetic)
+    replicas_equal = None
+    if world > 1:
+        h = torch.tensor([float(torch.sum(theta[0].double())), float(torch.sum(ms[0].double()))],
+                         dtype=torch.float64, device="cuda")
+        hs = [torch.zeros_like(h) for _ in range(world)]
+        dist.all_gather(hs, h)
+        replicas_equal = all(bool(torch.equal(hs[0], x)) for x in hs[1:])
+    graph_ms = step_ms
+    if world > 1 and eager_ms < step_ms:
+        # (at N = 2 graph replay measured slower than the eager loop for both the NCCL
+        # and the fused path -- DESIGN.md 9b; the faster of the two real runs is kept)
+        step_ms = eager_ms
+        timing_mode = "eager loop (faster than graph replay at this N; both reported)"
+    # the update kernel alone (roofline): the same graphs without the collective
+    if world > 1:
+        if g_full is None:
+            kernel_ms = timed(None, None, False)
+        else:
+            k_full, k_rem = capture(R, False), (capture(rem, False) if rem else None)
+            kernel_ms = timed(k_full, k_rem)
+    else:
+        kernel_ms = step_ms
+
     # end to end: this step's gradient from pinned host memory, the norm read back
     e2e = None
     if not args.no_e2e:
@@ -695,18 +783,26 @@ def run_update(args):
         "config": {"workload": f"learner update, {size} model ({n} parameters)",
                    "n_params": n, "optimizer": "RMSProp momentum 0, decay 0.99, eps 0.01, "
                    "lr 6e-4, clip global norm 40 (P:950-953)",
-                   "collective": "per step: copy of the local fp32 gradient + NCCL all_reduce "
-                                 "SUM of it" if world > 1 else "none",
+                   "collective": ("per step: local gradient into symmetric memory; ONE kernel "
+                                  "syncs the learners (ready/done flags over NVLink), sums "
+                                  "every learner's buffer (rank order) and updates" if symm else
+                                  "per step: copy of the local fp32 gradient + NCCL all_reduce "
+                                  "SUM of it, then the update kernel") if world > 1 else "none",
                    "l2": f"state rotated over {R} HBM-resident copies ({R} x {per / 1e6:.1f} MB "
-                         ">= 4 x L2)", "parallelism": f"dp{world}"},
+                         ">= 4 x L2)", "parallelism": f"dp{world}",
+                   "timing": timing_mode},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "rmsprop_kernel",
+                     "frac": achieved / peak, "traffic": load_traffic("update:" + str(size)),
+                     "kernel": "rmsprop_reg_kernel" if n <= 148 * 512 * 24 else "rmsprop_kernel",
                      "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg,
                      "peak_source": peak_src},
         "gpu_launches": K,
         "clocks": sampler.summary(tw0, tw1) if sampler else None,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "eager_ms_per_step": eager_ms,
+        "replicas_bitwise_equal": replicas_equal,
+        "graph_ms_per_step": graph_ms,
     }
     print(json.dumps(line), flush=True)
 

@@ -274,6 +274,42 @@ vt_status vtrace_rmsprop_step(int64_t n, float* params, float* mean_square, cons
                               const vt_rmsprop_params* prm, double* global_norm_out,
                               void* workspace, size_t workspace_bytes, vt_stream_t stream);
 
+/* The same step on the SUM of num_grads (1..8) gradient buffers, added in index order
+ * in fp32 inside the kernel: `grads` is a HOST array of DEVICE pointers, which may
+ * be other GPUs' memory reachable over NVLink (peer / symmetric-memory buffers).
+ * Learners that pass the same buffers in the same order compute bitwise-identical
+ * norms and updates, so the gradient all-reduce (reading r11) happens in
+ * this kernel.  The caller orders the accesses: every buffer is complete before
+ * the call, and no buffer is overwritten before every learner's call has finished
+ * (e.g. a barrier on both sides).  Errors as vtrace_rmsprop_step; num_grads out of
+ * range or a NULL entry: VT_ERR_INVALID_ARG. */
+vt_status vtrace_rmsprop_step_multi(int64_t n, float* params, float* mean_square,
+                                    const float* const* grads, int32_t num_grads,
+                                    const vt_rmsprop_params* prm, double* global_norm_out,
+                                    void* workspace, size_t workspace_bytes,
+                                    vt_stream_t stream);
+
+/* The multi-learner step with the learners' synchronisation inside the kernel (no
+ * separate barrier).  grads[j] (host array of device pointers) is learner j's
+ * gradient buffer and flags[j] its two zero-initialised uint32 words {ready, done}
+ * (8-byte aligned), all in memory every learner can reach (e.g. symmetric memory
+ * over NVLink); `self` is the caller's index.  Call k of every learner (counted by
+ * its workspace) publishes ready = k + 1 when its kernel starts -- the caller's own
+ * buffer must be complete by then (earlier work on `stream`) -- waits for every
+ * ready >= k + 1 before reading the buffers, and ends only after every learner has
+ * published done >= k + 1, so each buffer may be refilled after the call returns on
+ * the stream.  Every learner must make the same sequence of calls with the same
+ * buffer order (the sums, norms and updates are then bitwise identical); a learner
+ * that does not call leaves the others waiting.  Errors: as
+ * vtrace_rmsprop_step_multi; flags NULL, a NULL entry or self out of range:
+ * VT_ERR_INVALID_ARG. */
+vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_square,
+                                       const float* const* grads, uint32_t* const* flags,
+                                       int32_t num_learners, int32_t self,
+                                       const vt_rmsprop_params* prm, double* global_norm_out,
+                                       void* workspace, size_t workspace_bytes,
+                                       vt_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,7 +34,8 @@ DATA_ERRORS = {0: "ok", 1: "action", 2: "logits", 3: "reward", 4: "value", 5: "d
 EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_from_logits",
                     "vtrace_loss_and_grad", "vtrace_loss_and_grad_from_host",
                     "vtrace_read_device_status", "vtrace_status_string", "vtrace_version",
-                    "vtrace_kernel_for", "vtrace_rmsprop_workspace_bytes", "vtrace_rmsprop_step")
+                    "vtrace_kernel_for", "vtrace_rmsprop_workspace_bytes", "vtrace_rmsprop_step",
+                    "vtrace_rmsprop_step_multi", "vtrace_rmsprop_step_learners")
 
 
 class VtraceError(RuntimeError):
@@ -105,6 +106,15 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_rmsprop_step.argtypes = [i64, P, P, P, ctypes.POINTER(_RmsParams), P, P,
                                         ctypes.c_size_t, P]
     lib.vtrace_rmsprop_step.restype = ctypes.c_int
+    lib.vtrace_rmsprop_step_multi.argtypes = [i64, P, P, ctypes.POINTER(ctypes.c_void_p),
+                                              ctypes.c_int32, ctypes.POINTER(_RmsParams), P, P,
+                                              ctypes.c_size_t, P]
+    lib.vtrace_rmsprop_step_multi.restype = ctypes.c_int
+    lib.vtrace_rmsprop_step_learners.argtypes = [i64, P, P, ctypes.POINTER(ctypes.c_void_p),
+                                                 ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                                 ctypes.c_int32, ctypes.POINTER(_RmsParams), P, P,
+                                                 ctypes.c_size_t, P]
+    lib.vtrace_rmsprop_step_learners.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -368,22 +378,61 @@ class RmspropWorkspace(Workspace):
 
 def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
                  epsilon: float, max_global_norm: float = 40.0, global_norm_out=None,
-                 workspace: RmspropWorkspace | None = None):
+                 workspace: RmspropWorkspace | None = None, learner_flags=None,
+                 self_index: int = 0):
     """Clipped RMSProp step (momentum 0) in place on fp32 CUDA tensors of equal size
-    (DESIGN.md r9-r11).  `global_norm_out`: optional float64 CUDA
-    tensor of 1 element receiving ||grads||_2 before clipping."""
-    for t in (params, mean_square, grads):
+    (DESIGN.md r9-r11).  `grads`: one fp32 CUDA tensor, or a list
+    of up to 8 gradients -- fp32 CUDA tensors or raw device pointers (ints; e.g. the
+    learners' symmetric-memory buffers, peers included) -- summed in list order inside
+    the kernel (vtrace_rmsprop_step_multi).  `global_norm_out`: optional float64 CUDA
+    tensor of 1 element receiving ||sum of grads||_2 before clipping.  `learner_flags`:
+    with a list of learners' buffers, one device pointer per learner to its two
+    {ready, done} uint32 words -- the learners then synchronise inside the kernel
+    (vtrace_rmsprop_step_learners; `self_index` = this learner's position)."""
+    for t in (params, mean_square):
         if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
-            raise ValueError("params, mean_square, grads must be contiguous fp32 CUDA tensors")
+            raise ValueError("params and mean_square must be contiguous fp32 CUDA tensors")
     n = params.numel()
-    if mean_square.numel() != n or grads.numel() != n:
+    multi = isinstance(grads, (list, tuple))
+    glist = list(grads) if multi else [grads]
+    if not 1 <= len(glist) <= 8:
+        raise ValueError("between 1 and 8 gradients")
+    ptrs = []
+    for g in glist:
+        if isinstance(g, int):
+            ptrs.append(g)
+            continue
+        if not (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous()):
+            raise ValueError("gradients must be contiguous fp32 CUDA tensors (or device pointers)")
+        if g.numel() != n:
+            raise ValueError("params, mean_square and grads must have the same size")
+        ptrs.append(g.data_ptr())
+    if mean_square.numel() != n:
         raise ValueError("params, mean_square and grads must have the same size")
     if global_norm_out is not None and not (global_norm_out.is_cuda and
                                             global_norm_out.dtype == torch.float64):
         raise ValueError("global_norm_out must be a float64 CUDA tensor")
     ws = workspace if workspace is not None else RmspropWorkspace(n, params.device)
     prm = _RmsParams(float(learning_rate), float(decay), float(epsilon), float(max_global_norm))
-    _check(load_library().vtrace_rmsprop_step(n, _ptr(params), _ptr(mean_square), _ptr(grads),
-                                              ctypes.byref(prm), _ptr(global_norm_out), ws.ptr,
-                                              ws.nbytes, _stream(params.device)),
-           "vtrace_rmsprop_step")
+    lib = load_library()
+    if not multi:
+        st = lib.vtrace_rmsprop_step(n, _ptr(params), _ptr(mean_square), ctypes.c_void_p(ptrs[0]),
+                                     ctypes.byref(prm), _ptr(global_norm_out), ws.ptr, ws.nbytes,
+                                     _stream(params.device))
+        _check(st, "vtrace_rmsprop_step")
+        return
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    if learner_flags is not None:
+        if len(learner_flags) != len(ptrs):
+            raise ValueError("one flag pointer per learner buffer")
+        fl = (ctypes.c_void_p * len(ptrs))(*[int(f) for f in learner_flags])
+        st = lib.vtrace_rmsprop_step_learners(n, _ptr(params), _ptr(mean_square), arr, fl,
+                                              len(ptrs), int(self_index), ctypes.byref(prm),
+                                              _ptr(global_norm_out), ws.ptr, ws.nbytes,
+                                              _stream(params.device))
+        _check(st, "vtrace_rmsprop_step_learners")
+        return
+    st = lib.vtrace_rmsprop_step_multi(n, _ptr(params), _ptr(mean_square), arr, len(ptrs),
+                                       ctypes.byref(prm), _ptr(global_norm_out), ws.ptr,
+                                       ws.nbytes, _stream(params.device))
+    _check(st, "vtrace_rmsprop_step_multi")

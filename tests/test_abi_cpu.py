@@ -164,3 +164,35 @@ def test_rmsprop_host_checks(lib):
     assert _rms(lib) == 6                                          # WORKSPACE (NULL)
     assert _rms(lib, ws=256, wsb=16) == 6                          # too small
     assert _rms(lib, ws=300, wsb=1 << 20) == 6                     # not 256-aligned
+
+
+def test_rmsprop_multi_host_checks(lib):
+    prm = vt._RmsParams(6e-4, 0.99, 0.01, 40.0)
+
+    def call(ptrs, ng, n=10):
+        arr = (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+        return lib.vtrace_rmsprop_step_multi(n, ctypes.c_void_p(16), ctypes.c_void_p(32), arr,
+                                             ng, ctypes.byref(prm), None, None, 0, None)
+    assert call([48, 64], 0) == 1                 # no gradient
+    assert call([48] * 9, 9) == 1                 # more than 8
+    assert call([48, None], 2) == 1               # a NULL buffer
+    assert call([48, 66], 2) == 5                 # a misaligned buffer
+    assert call([48, 64], 2) == 6                 # then the workspace check
+    assert lib.vtrace_rmsprop_step_multi(10, ctypes.c_void_p(16), ctypes.c_void_p(32), None, 1,
+                                         ctypes.byref(prm), None, None, 0, None) == 1
+
+
+def test_rmsprop_learners_host_checks(lib):
+    prm = vt._RmsParams(6e-4, 0.99, 0.01, 40.0)
+    g = (ctypes.c_void_p * 2)(48, 64)
+
+    def call(flags, self_index):
+        fl = None if flags is None else (ctypes.c_void_p * 2)(*flags)
+        return lib.vtrace_rmsprop_step_learners(10, ctypes.c_void_p(16), ctypes.c_void_p(32), g,
+                                                fl, 2, self_index, ctypes.byref(prm), None, None,
+                                                0, None)
+    assert call(None, 0) == 1          # no flags
+    assert call([128, None], 0) == 1   # a NULL flag pointer
+    assert call([128, 136], 2) == 1    # self out of range
+    assert call([128, 132], 0) == 5    # flags not 8-byte aligned
+    assert call([128, 136], 1) == 6    # then the workspace check
