@@ -359,6 +359,21 @@ __all__ = ["workspace_bytes", "Workspace", "from_logits", "loss_and_grad",
 
 # ---- the learner's parameter update (include/vtrace.h) ----
 
+_RMS_PRM_CACHE: dict = {}
+_PTR_ARRAYS: dict = {}
+
+
+def _ptr_array(ptrs):
+    """ctypes array of device pointers, cached by value (same buffers every step)."""
+    key = tuple(ptrs)
+    arr = _PTR_ARRAYS.get(key)
+    if arr is None:
+        if len(_PTR_ARRAYS) > 256:
+            _PTR_ARRAYS.clear()
+        arr = _PTR_ARRAYS.setdefault(key, (ctypes.c_void_p * len(ptrs))(*ptrs))
+    return arr
+
+
 class RmspropWorkspace(Workspace):
     """Device workspace of vtrace_rmsprop_step: allocated once, initialised once."""
 
@@ -413,7 +428,10 @@ def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
                                             global_norm_out.dtype == torch.float64):
         raise ValueError("global_norm_out must be a float64 CUDA tensor")
     ws = workspace if workspace is not None else RmspropWorkspace(n, params.device)
-    prm = _RmsParams(float(learning_rate), float(decay), float(epsilon), float(max_global_norm))
+    key = (float(learning_rate), float(decay), float(epsilon), float(max_global_norm))
+    prm = _RMS_PRM_CACHE.get(key)
+    if prm is None:  # (argument marshalling is cached: a learner calls this every step)
+        prm = _RMS_PRM_CACHE.setdefault(key, _RmsParams(*key))
     lib = load_library()
     if not multi:
         st = lib.vtrace_rmsprop_step(n, _ptr(params), _ptr(mean_square), ctypes.c_void_p(ptrs[0]),
@@ -421,11 +439,11 @@ def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
                                      _stream(params.device))
         _check(st, "vtrace_rmsprop_step")
         return
-    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    arr = _ptr_array(ptrs)
     if learner_flags is not None:
         if len(learner_flags) != len(ptrs):
             raise ValueError("one flag pointer per learner buffer")
-        fl = (ctypes.c_void_p * len(ptrs))(*[int(f) for f in learner_flags])
+        fl = _ptr_array([int(f) for f in learner_flags])
         st = lib.vtrace_rmsprop_step_learners(n, _ptr(params), _ptr(mean_square), arr, fl,
                                               len(ptrs), int(self_index), ctypes.byref(prm),
                                               _ptr(global_norm_out), ws.ptr, ws.nbytes,
