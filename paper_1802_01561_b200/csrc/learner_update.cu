@@ -39,6 +39,7 @@ struct RmsHeader {  // workspace bytes [0, 8); vtrace_workspace_init zeroes it
   unsigned int epoch;   // calls completed (tags this call's records with epoch + 1)
   unsigned int ticket;  // CTAs done with phase 1 (the last one bumps the epoch)
   unsigned int done_ticket;  // CTAs done reading (learner sync: the last one signals)
+  unsigned int go;           // learner sync: every learner ready for epoch go - 1 (CTA 0)
 };
 
 struct RmsArgs {
@@ -108,14 +109,22 @@ __device__ __forceinline__ unsigned int rms_epoch(const RmsArgs& a) {
 // and every CTA waits for all learners' ready >= e + 1 before reading their buffers.
 __device__ __forceinline__ void peers_ready(const RmsArgs& a, unsigned int e) {
   if (a.flags[0] == nullptr) return;
+  // (CTA 0 alone polls the other learners' flags over NVLink, then releases a local
+  // "go" word that the other CTAs poll in L2: 148 remote pollers per GPU slowed the
+  // gradient reads)
+  RmsHeader* hdr = reinterpret_cast<RmsHeader*>(a.ws);
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
       __threadfence_system();
       st_release_sys(a.flags[a.self], e + 1u);
-    }
-    for (int j = 0; j < a.ng; ++j) {
-      if (j == a.self) continue;
-      while ((int)(ld_acquire_sys(a.flags[j]) - (e + 1u)) < 0) {
+      for (int j = 0; j < a.ng; ++j) {
+        if (j == a.self) continue;
+        while ((int)(ld_acquire_sys(a.flags[j]) - (e + 1u)) < 0) {
+        }
+      }
+      st_release_u32(&hdr->go, e + 1u);
+    } else {
+      while ((int)(ld_acquire_u32(&hdr->go) - (e + 1u)) < 0) {
       }
     }
   }
