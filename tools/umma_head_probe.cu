@@ -1,0 +1,186 @@
+// De-risking probe for NEXT #3: the output-layer GEMM of P:173-174,
+// [z | V] = h W, on the 5th-gen tensor cores.  One CTA per 128 rows of h: h tile
+// [128 x K] and W^T [N x K] (bf16, K-major) staged in shared memory in the canonical
+// no-swizzle core-matrix layout (8 rows x 16 bytes per core matrix), K/16 tcgen05.mma
+// (M=128, N=32, kind::f16, fp32 accumulate) issued by one thread into 32 TMEM columns,
+// completion via tcgen05.commit -> mbarrier, epilogue tcgen05.ld 32x32b (thread = row).
+// Not product code: it checks the descriptor encodings (LBO/SBO order) against a CPU
+// fp64 GEMM and times the kernel.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
+// -O3 -o umma_head_probe tools/umma_head_probe.cu
+#include <cuda_bf16.h>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+
+constexpr int BM = 128, BN = 32, BK = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// tcgen05 shared-memory matrix descriptor, no swizzle (layout type 0), version 1.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;
+}
+
+// offset (elements) of (row, k) in the canonical layout: core matrix (row/8, k/8) at
+// ((row/8) * (K/8) + k/8) * 64 elements, inside it row%8 * 8 + k%8.
+__device__ __forceinline__ int canon(int row, int k, int K) {
+  return ((row >> 3) * (K >> 3) + (k >> 3)) * 64 + (row & 7) * 8 + (k & 7);
+}
+
+template <bool SWAP>
+__global__ void __launch_bounds__(128) head_kernel(const __nv_bfloat16* __restrict__ h,
+                                                   const __nv_bfloat16* __restrict__ wt,
+                                                   float* __restrict__ out, int M, int n_out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* sb = sa + BM * BK;
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row0 = blockIdx.x * BM;
+
+  // stage h tile and W^T (16-byte chunks = 8 bf16 along k)
+  for (int c = tid; c < BM * BK / 8; c += blockDim.x) {
+    int r = c / (BK / 8), k = (c % (BK / 8)) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row0 + r < M) v = *reinterpret_cast<const uint4*>(h + (size_t)(row0 + r) * BK + k);
+    *reinterpret_cast<uint4*>(sa + canon(r, k, BK)) = v;
+  }
+  for (int c = tid; c < BN * BK / 8; c += blockDim.x) {
+    int r = c / (BK / 8), k = (c % (BK / 8)) * 8;
+    *reinterpret_cast<uint4*>(sb + canon(r, k, BK)) =
+        *reinterpret_cast<const uint4*>(wt + (size_t)r * BK + k);
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&tmem_base)), "n"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (tid == 0) {
+    // idesc: D f32 (bits 4-5 = 1), A bf16 (7-9 = 1), B bf16 (10-12 = 1), K-major both,
+    // N >> 3 at bit 17, M >> 4 at bit 24
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    const uint32_t kcore = 128;                 // bytes between core matrices along K
+    const uint32_t a_mn = (BK / 8) * 128;       // bytes between 8-row groups of A
+    const uint32_t b_mn = (BK / 8) * 128;
+    for (int k = 0; k < BK / 16; ++k) {
+      uint32_t off = k * 2 * 128;               // two core matrices of K per MMA (K = 16)
+      uint64_t da = SWAP ? make_desc(smem_u32(sa) + off, a_mn, kcore)
+                         : make_desc(smem_u32(sa) + off, kcore, a_mn);
+      uint64_t db = SWAP ? make_desc(smem_u32(sb) + off, b_mn, kcore)
+                         : make_desc(smem_u32(sb) + off, kcore, b_mn);
+      uint32_t acc = k > 0;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                   "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                   ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(&mbar)));
+  }
+  // wait for the accumulator (phase 0)
+  asm volatile("{\n\t.reg .pred done;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n\t"
+               "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(&mbar)));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t v[32];
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+  const int row = row0 + warp * 32 + lane;
+  if (row < M) {
+#pragma unroll
+    for (int n = 0; n < BN; ++n)
+      if (n < n_out) out[(size_t)row * n_out + n] = __uint_as_float(v[n]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
+}
+
+static float bf(uint16_t x) { uint32_t u = (uint32_t)x << 16; float f; memcpy(&f, &u, 4); return f; }
+
+int main(int argc, char** argv) {
+  const int M = argc > 1 ? atoi(argv[1]) : 819200, n_out = 19;
+  std::vector<uint16_t> hh((size_t)M * BK), hw((size_t)BN * BK, 0);
+  uint32_t s = 12345u;
+  auto rnd = [&]() { s = s * 1664525u + 1013904223u; return (int)((s >> 9) % 17) - 8; };
+  for (auto& x : hh) { float f = rnd() / 16.0f; uint32_t u; memcpy(&u, &f, 4); x = u >> 16; }
+  for (int n = 0; n < n_out; ++n)
+    for (int k = 0; k < BK; ++k) { float f = rnd() / 8.0f; uint32_t u; memcpy(&u, &f, 4); hw[n * BK + k] = u >> 16; }
+  __nv_bfloat16 *dh, *dw; float* dout;
+  cudaMalloc(&dh, hh.size() * 2); cudaMalloc(&dw, hw.size() * 2);
+  cudaMalloc(&dout, (size_t)M * n_out * 4);
+  cudaMemcpy(dh, hh.data(), hh.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice);
+  const int smem = (BM + BN) * BK * 2;
+  cudaFuncSetAttribute(head_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(head_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = (M + BM - 1) / BM;
+  std::vector<float> got((size_t)M * n_out);
+  for (int swap = 0; swap < 2; ++swap) {
+    cudaMemset(dout, 0, (size_t)M * n_out * 4);
+    if (swap) head_kernel<true><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+    else head_kernel<false><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("swap=%d error %s\n", swap, cudaGetErrorString(e)); return 1; }
+    cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
+    // exact check (dyadic inputs: every partial sum is exact in fp32) on sampled rows
+    long bad = 0, checked = 0;
+    for (int r = 0; r < M; r += (M > 4096 ? 97 : 1)) {
+      for (int n = 0; n < n_out; ++n) {
+        double ref = 0;
+        for (int k = 0; k < BK; ++k) ref += (double)bf(hh[(size_t)r * BK + k]) * bf(hw[n * BK + k]);
+        ++checked;
+        if (ref != got[(size_t)r * n_out + n]) {
+          if (bad < 3) printf("  swap=%d r=%d n=%d got %g ref %g\n", swap, r, n, got[(size_t)r * n_out + n], ref);
+          ++bad;
+        }
+      }
+    }
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int i = 0; i < 3; ++i)
+      swap ? head_kernel<true><<<grid, 128, smem>>>(dh, dw, dout, M, n_out)
+           : head_kernel<false><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+    cudaEventRecord(a);
+    const int it = 20;
+    for (int i = 0; i < it; ++i)
+      swap ? head_kernel<true><<<grid, 128, smem>>>(dh, dw, dout, M, n_out)
+           : head_kernel<false><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b); ms /= it;
+    double bytes = (double)M * BK * 2 + (double)M * n_out * 4;
+    printf("{\"probe\": \"umma_head\", \"swap_lbo_sbo\": %d, \"M\": %d, \"K\": %d, \"N\": %d, "
+           "\"checked\": %ld, \"bad\": %ld, \"us\": %.2f, \"GBps\": %.1f}\n",
+           swap, M, BK, n_out, checked, bad, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+  }
+  return 0;
+}
