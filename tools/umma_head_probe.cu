@@ -4,7 +4,9 @@
 // no-swizzle core-matrix layout (8 rows x 16 bytes per core matrix), K/16 tcgen05.mma
 // (M=128, N=32, kind::f16, fp32 accumulate) issued by one thread into 32 TMEM columns,
 // completion via tcgen05.commit -> mbarrier, epilogue tcgen05.ld 32x32b (thread = row).
-// Not product code: it checks the descriptor encodings (LBO/SBO order) against a CPU
+// Not product code: it checks the descriptor encoding (LBO = K core stride, verified
+// against the swapped order in v1) and two staging variants (v1 plain loads, v2 cp.async +
+// coalesced epilogue) against a CPU
 // fp64 GEMM and times the kernel.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
 // -O3 -o umma_head_probe tools/umma_head_probe.cu
 #include <cuda_bf16.h>
@@ -13,6 +15,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <vector>
+#include <algorithm>
+#include <cstring>
 
 constexpr int BM = 128, BN = 32, BK = 256;
 
@@ -36,8 +40,8 @@ __device__ __forceinline__ int canon(int row, int k, int K) {
   return ((row >> 3) * (K >> 3) + (k >> 3)) * 64 + (row & 7) * 8 + (k & 7);
 }
 
-template <bool SWAP>
-__global__ void __launch_bounds__(128) head_kernel(const __nv_bfloat16* __restrict__ h,
+template <bool SWAP, bool V2>
+__global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restrict__ h,
                                                    const __nv_bfloat16* __restrict__ wt,
                                                    float* __restrict__ out, int M, int n_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -48,18 +52,27 @@ __global__ void __launch_bounds__(128) head_kernel(const __nv_bfloat16* __restri
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row0 = blockIdx.x * BM;
 
-  // stage h tile and W^T (16-byte chunks = 8 bf16 along k)
+  // stage h tile and W^T (16-byte chunks = 8 bf16 along k); V2: cp.async so every
+  // thread has all its 16-byte loads in flight at once (rows past M zero-filled)
   for (int c = tid; c < BM * BK / 8; c += blockDim.x) {
     int r = c / (BK / 8), k = (c % (BK / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row0 + r < M) v = *reinterpret_cast<const uint4*>(h + (size_t)(row0 + r) * BK + k);
-    *reinterpret_cast<uint4*>(sa + canon(r, k, BK)) = v;
+    if (V2) {
+      const bool ok = row0 + r < M;
+      const __nv_bfloat16* src = h + (size_t)(ok ? row0 + r : 0) * BK + k;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                   ::"r"(smem_u32(sa + canon(r, k, BK))), "l"(src), "r"(ok ? 16 : 0));
+    } else {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (row0 + r < M) v = *reinterpret_cast<const uint4*>(h + (size_t)(row0 + r) * BK + k);
+      *reinterpret_cast<uint4*>(sa + canon(r, k, BK)) = v;
+    }
   }
   for (int c = tid; c < BN * BK / 8; c += blockDim.x) {
     int r = c / (BK / 8), k = (c % (BK / 8)) * 8;
     *reinterpret_cast<uint4*>(sb + canon(r, k, BK)) =
         *reinterpret_cast<const uint4*>(wt + (size_t)r * BK + k);
   }
+  if (V2) asm volatile("cp.async.wait_all;" ::: "memory");
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -103,6 +116,7 @@ __global__ void __launch_bounds__(128) head_kernel(const __nv_bfloat16* __restri
                "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(&mbar)));
   asm volatile("tcgen05.fence::after_thread_sync;");
   uint32_t v[32];
+  if (warp < 4) {  // TMEM lanes 32w..32w+31 belong to warp w % 4; warps 4-7 only stage/store
   const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -114,13 +128,136 @@ __global__ void __launch_bounds__(128) head_kernel(const __nv_bfloat16* __restri
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;");
-  const int row = row0 + warp * 32 + lane;
-  if (row < M) {
+  }
+  if (V2) {
+    // coalesced store: rows [row0, row0+128) of out are one contiguous 128*n_out block
+    float* so = reinterpret_cast<float*>(smem);  // A tile is dead once the MMAs completed
+    const int r = warp * 32 + lane;
+    if (warp < 4) {
 #pragma unroll
-    for (int n = 0; n < BN; ++n)
-      if (n < n_out) out[(size_t)row * n_out + n] = __uint_as_float(v[n]);
+      for (int n = 0; n < BN; ++n)
+        if (n < n_out) so[r * n_out + n] = __uint_as_float(v[n]);
+    }
+    __syncthreads();
+    const int rows = min(BM, M - row0);
+    for (int i = tid; i < rows * n_out; i += blockDim.x) out[(size_t)row0 * n_out + i] = so[i];
+  } else {
+    const int row = row0 + warp * 32 + lane;
+    if (warp < 4 && row < M) {
+#pragma unroll
+      for (int n = 0; n < BN; ++n)
+        if (n < n_out) out[(size_t)row * n_out + n] = __uint_as_float(v[n]);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
+}
+
+// V3: persistent, one CTA per SM, NBUF-deep cp.async ring of h tiles so the loads of the
+// next NBUF-1 tiles are in flight while tile j is multiplied and stored.
+template <int NBUF>
+__global__ void __launch_bounds__(256) head_kernel_pipe(const __nv_bfloat16* __restrict__ h,
+                                                        const __nv_bfloat16* __restrict__ wt,
+                                                        float* __restrict__ out, int M, int n_out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(smem);            // W^T, 16 KB
+  __nv_bfloat16* sa0 = sb + BN * BK;                                    // NBUF x 64 KB
+  float* so = reinterpret_cast<float*>(sa0 + NBUF * BM * BK);           // 128 x n_out
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tiles = (M + BM - 1) / BM;
+
+  for (int c = tid; c < BN * BK / 8; c += blockDim.x) {
+    int r = c / (BK / 8), k = (c % (BK / 8)) * 8;
+    *reinterpret_cast<uint4*>(sb + canon(r, k, BK)) =
+        *reinterpret_cast<const uint4*>(wt + (size_t)r * BK + k);
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&tmem_base)), "n"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  auto issue = [&](int j) {  // loads of this CTA's j-th tile (a group even when empty)
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile < tiles) {
+      __nv_bfloat16* sa = sa0 + (j % NBUF) * BM * BK;
+      const int row0 = tile * BM;
+      for (int c = tid; c < BM * BK / 8; c += blockDim.x) {
+        int r = c / (BK / 8), k = (c % (BK / 8)) * 8;
+        const bool ok = row0 + r < M;
+        const __nv_bfloat16* src = h + (size_t)(ok ? row0 + r : 0) * BK + k;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                     ::"r"(smem_u32(sa + canon(r, k, BK))), "l"(src), "r"(ok ? 16 : 0));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int j = 0; j < NBUF - 1; ++j) issue(j);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)(BM >> 4) << 24);
+  for (int j = 0;; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= tiles) break;
+    issue(j + NBUF - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(NBUF - 1) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a_base = smem_u32(sa0 + (j % NBUF) * BM * BK), b_base = smem_u32(sb);
+      for (int k = 0; k < BK / 16; ++k) {
+        const uint32_t off = k * 256;
+        uint64_t da = make_desc(a_base + off, 128, (BK / 8) * 128);
+        uint64_t db = make_desc(b_base + off, 128, (BK / 8) * 128);
+        uint32_t acc = k > 0;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                     ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   ::"r"(smem_u32(&mbar)));
+    }
+    asm volatile("{\n\t.reg .pred done;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+                 "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(&mbar)), "r"(j & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp < 4) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+            "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      const int r = warp * 32 + lane;
+#pragma unroll
+      for (int n = 0; n < BN; ++n)
+        if (n < n_out) so[r * n_out + n] = __uint_as_float(v[n]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    const int row0 = tile * BM, rows = min(BM, M - row0);
+    for (int i = tid; i < rows * n_out; i += blockDim.x) out[(size_t)row0 * n_out + i] = so[i];
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
@@ -130,6 +267,7 @@ static float bf(uint16_t x) { uint32_t u = (uint32_t)x << 16; float f; memcpy(&f
 
 int main(int argc, char** argv) {
   const int M = argc > 1 ? atoi(argv[1]) : 819200, n_out = 19;
+  const int nt = argc > 2 ? atoi(argv[2]) : 128;
   std::vector<uint16_t> hh((size_t)M * BK), hw((size_t)BN * BK, 0);
   uint32_t s = 12345u;
   auto rnd = [&]() { s = s * 1664525u + 1013904223u; return (int)((s >> 9) % 17) - 8; };
@@ -142,14 +280,14 @@ int main(int argc, char** argv) {
   cudaMemcpy(dh, hh.data(), hh.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice);
   const int smem = (BM + BN) * BK * 2;
-  cudaFuncSetAttribute(head_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(head_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(head_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(head_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int grid = (M + BM - 1) / BM;
   std::vector<float> got((size_t)M * n_out);
   for (int swap = 0; swap < 2; ++swap) {
     cudaMemset(dout, 0, (size_t)M * n_out * 4);
-    if (swap) head_kernel<true><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
-    else head_kernel<false><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+    if (swap) head_kernel<false, true><<<grid, nt, smem>>>(dh, dw, dout, M, n_out);
+    else head_kernel<false, false><<<grid, nt, smem>>>(dh, dw, dout, M, n_out);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("swap=%d error %s\n", swap, cudaGetErrorString(e)); return 1; }
     cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
@@ -168,19 +306,50 @@ int main(int argc, char** argv) {
     }
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     for (int i = 0; i < 3; ++i)
-      swap ? head_kernel<true><<<grid, 128, smem>>>(dh, dw, dout, M, n_out)
-           : head_kernel<false><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+      swap ? head_kernel<false, true><<<grid, nt, smem>>>(dh, dw, dout, M, n_out)
+           : head_kernel<false, false><<<grid, nt, smem>>>(dh, dw, dout, M, n_out);
     cudaEventRecord(a);
     const int it = 20;
     for (int i = 0; i < it; ++i)
-      swap ? head_kernel<true><<<grid, 128, smem>>>(dh, dw, dout, M, n_out)
-           : head_kernel<false><<<grid, 128, smem>>>(dh, dw, dout, M, n_out);
+      swap ? head_kernel<false, true><<<grid, nt, smem>>>(dh, dw, dout, M, n_out)
+           : head_kernel<false, false><<<grid, nt, smem>>>(dh, dw, dout, M, n_out);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b); ms /= it;
     double bytes = (double)M * BK * 2 + (double)M * n_out * 4;
-    printf("{\"probe\": \"umma_head\", \"swap_lbo_sbo\": %d, \"M\": %d, \"K\": %d, \"N\": %d, "
+    printf("{\"probe\": \"umma_head\", \"v2_cpasync_coalesced\": %d, \"threads\": %d, \"M\": %d, \"K\": %d, \"N\": %d, "
            "\"checked\": %ld, \"bad\": %ld, \"us\": %.2f, \"GBps\": %.1f}\n",
-           swap, M, BK, n_out, checked, bad, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+           swap, nt, M, BK, n_out, checked, bad, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+  }
+  {  // V3 persistent pipelined kernel
+    int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    constexpr int NB = 3;
+    const int smem3 = (BN * BK + NB * BM * BK) * 2 + BM * n_out * 4;
+    cudaFuncSetAttribute(head_kernel_pipe<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    const int g3 = std::min(sms, grid);
+    cudaMemset(dout, 0, (size_t)M * n_out * 4);
+    head_kernel_pipe<NB><<<g3, 256, smem3>>>(dh, dw, dout, M, n_out);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("v3 error %s\n", cudaGetErrorString(e)); return 1; }
+    cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
+    long bad = 0, checked = 0;
+    for (int r = 0; r < M; r += (M > 4096 ? 97 : 1))
+      for (int n = 0; n < n_out; ++n) {
+        double ref = 0;
+        for (int k = 0; k < BK; ++k) ref += (double)bf(hh[(size_t)r * BK + k]) * bf(hw[n * BK + k]);
+        ++checked;
+        if (ref != got[(size_t)r * n_out + n]) ++bad;
+      }
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int i = 0; i < 3; ++i) head_kernel_pipe<NB><<<g3, 256, smem3>>>(dh, dw, dout, M, n_out);
+    cudaEventRecord(a);
+    const int it = 20;
+    for (int i = 0; i < it; ++i) head_kernel_pipe<NB><<<g3, 256, smem3>>>(dh, dw, dout, M, n_out);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b); ms /= it;
+    double bytes = (double)M * BK * 2 + (double)M * n_out * 4;
+    printf("{\"probe\": \"umma_head\", \"variant\": \"v3_persistent_ring%d\", \"grid\": %d, \"M\": %d, "
+           "\"checked\": %ld, \"bad\": %ld, \"us\": %.2f, \"GBps\": %.1f}\n",
+           NB, g3, M, checked, bad, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
   }
   return 0;
 }
