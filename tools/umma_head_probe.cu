@@ -9,6 +9,8 @@
 // coalesced epilogue) against a CPU
 // fp64 GEMM and times the kernel.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
 // -O3 -o umma_head_probe tools/umma_head_probe.cu
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cstdio>
 #include <cstdint>
@@ -263,6 +265,125 @@ __global__ void __launch_bounds__(256) head_kernel_pipe(const __nv_bfloat16* __r
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
 }
 
+// V4: as V3, but each h tile arrives by TMA (4 boxes of 64 k x 128 rows, SWIZZLE_128B,
+// one thread issues, completion by mbarrier transaction count) and the MMA descriptors use
+// the 128-byte-swizzled K-major layout (SBO = 1024 B, k step = +32 B inside the atom).
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile("{\n\t.reg .pred done;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+               "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int NBUF>
+__global__ void __launch_bounds__(256) head_kernel_tma(const __grid_constant__ CUtensorMap hmap,
+                                                       const __grid_constant__ CUtensorMap wmap,
+                                                       float* __restrict__ out, int M, int n_out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);                    // W^T: 4 atoms x 4 KB
+  const uint32_t sa0 = sb + 16384;                       // NBUF x (4 atoms x 16 KB)
+  float* so = reinterpret_cast<float*>(smem + 16384 + NBUF * 65536);
+  __shared__ uint64_t full[NBUF], wbar, mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tiles = (M + BM - 1) / BM;
+  if (tid == 0) {
+    for (int i = 0; i < NBUF; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&tmem_base)), "n"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  auto issue = [&](int j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= tiles) return;
+    uint64_t* bar = &full[j % NBUF];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(65536));
+    for (int kb = 0; kb < 4; ++kb)
+      tma2d(sa0 + (j % NBUF) * 65536 + kb * 16384, &hmap, kb * 64, tile * BM, bar);
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&wbar)), "r"(16384));
+    for (int kb = 0; kb < 4; ++kb) tma2d(sb + kb * 4096, &wmap, kb * 64, 0, &wbar);
+    for (int j = 0; j < NBUF - 1; ++j) issue(j);
+    mbar_wait(&wbar, 0);
+  }
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)(BM >> 4) << 24);
+  for (int j = 0;; ++j) {
+    const int tile = blockIdx.x + j * gridDim.x;
+    if (tile >= tiles) break;
+    if (tid == 0) {
+      issue(j + NBUF - 1);
+      mbar_wait(&full[j % NBUF], (j / NBUF) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a_base = sa0 + (j % NBUF) * 65536;
+      for (int k = 0; k < BK / 16; ++k) {
+        const int kb = k >> 2, kk = k & 3;
+        uint64_t da = make_desc_sw128(a_base + kb * 16384 + kk * 32);
+        uint64_t db = make_desc_sw128(sb + kb * 4096 + kk * 32);
+        uint32_t acc = k > 0;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                     ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   ::"r"(smem_u32(&mbar)));
+    }
+    mbar_wait(&mbar, j & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp < 4) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+            "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      const int r = warp * 32 + lane;
+#pragma unroll
+      for (int n = 0; n < BN; ++n)
+        if (n < n_out) so[r * n_out + n] = __uint_as_float(v[n]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    const int row0 = tile * BM, rows = min(BM, M - row0);
+    for (int i = tid; i < rows * n_out; i += blockDim.x) out[(size_t)row0 * n_out + i] = so[i];
+    __syncthreads();
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
+}
+
 static float bf(uint16_t x) { uint32_t u = (uint32_t)x << 16; float f; memcpy(&f, &u, 4); return f; }
 
 int main(int argc, char** argv) {
@@ -350,6 +471,49 @@ int main(int argc, char** argv) {
     printf("{\"probe\": \"umma_head\", \"variant\": \"v3_persistent_ring%d\", \"grid\": %d, \"M\": %d, "
            "\"checked\": %ld, \"bad\": %ld, \"us\": %.2f, \"GBps\": %.1f}\n",
            NB, g3, M, checked, bad, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+  }
+  {  // V4 TMA + SWIZZLE_128B
+    void* fn = nullptr; cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    CUtensorMap hm, wm;
+    cuuint64_t hd[2] = {(cuuint64_t)BK, (cuuint64_t)M}, hs[1] = {(cuuint64_t)BK * 2};
+    cuuint64_t wd[2] = {(cuuint64_t)BK, (cuuint64_t)BN}, ws[1] = {(cuuint64_t)BK * 2};
+    cuuint32_t hb[2] = {64, 128}, wb[2] = {64, 32}, es[2] = {1, 1};
+    CUresult r1 = enc(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dh, hd, hs, hb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r2 = enc(&wm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dw, wd, ws, wb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) { printf("encode failed %d %d\n", (int)r1, (int)r2); return 1; }
+    int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    constexpr int NB = 3;
+    const int smem4 = 1024 + 16384 + NB * 65536 + BM * n_out * 4;
+    cudaFuncSetAttribute(head_kernel_tma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4);
+    const int g4 = std::min(sms, grid);
+    cudaMemset(dout, 0, (size_t)M * n_out * 4);
+    head_kernel_tma<NB><<<g4, 256, smem4>>>(hm, wm, dout, M, n_out);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("v4 error %s\n", cudaGetErrorString(e)); return 1; }
+    cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
+    long bad = 0, checked = 0;
+    for (int r = 0; r < M; r += (M > 4096 ? 97 : 1))
+      for (int n = 0; n < n_out; ++n) {
+        double ref = 0;
+        for (int k = 0; k < BK; ++k) ref += (double)bf(hh[(size_t)r * BK + k]) * bf(hw[n * BK + k]);
+        ++checked;
+        if (ref != got[(size_t)r * n_out + n]) { if (bad < 3) printf("  v4 r=%d n=%d got %g ref %g\n", r, n, got[(size_t)r * n_out + n], ref); ++bad; }
+      }
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int i = 0; i < 3; ++i) head_kernel_tma<NB><<<g4, 256, smem4>>>(hm, wm, dout, M, n_out);
+    cudaEventRecord(a);
+    const int it = 20;
+    for (int i = 0; i < it; ++i) head_kernel_tma<NB><<<g4, 256, smem4>>>(hm, wm, dout, M, n_out);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b); ms /= it;
+    double bytes = (double)M * BK * 2 + (double)M * n_out * 4;
+    printf("{\"probe\": \"umma_head\", \"variant\": \"v4_tma_sw128_ring%d\", \"grid\": %d, \"M\": %d, "
+           "\"checked\": %ld, \"bad\": %ld, \"us\": %.2f, \"GBps\": %.1f}\n",
+           NB, g4, M, checked, bad, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
   }
   return 0;
 }
