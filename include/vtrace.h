@@ -310,6 +310,27 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
                                        void* workspace, size_t workspace_bytes,
                                        vt_stream_t stream);
 
+/* ---- NEXT #3, first half: the output layer in front of the path ----
+ * [z^pi | V] = h W + b over all M = T*B time-folded steps (time folded into the
+ * batch; Fig. 3: linear policy and baseline heads on the LSTM output; DESIGN.md
+ * reading r12), on the tcgen05 tensor cores (bf16 in, fp32 accumulate, fp32 out).
+ *   M           rows = T*B (time-major, row t*B + b); M = 0 is a no-op
+ *   H           hidden width: 64, 128, 192 or 256
+ *   A           actions, 1 <= A <= 31 (A + 1 <= 32 head columns)
+ *   hidden      h   [M, H]   bf16 device, row-major, 16-byte aligned
+ *   w_t         W^T [A+1, H] bf16 device, row j = column j of W (rows 0..A-1 the policy
+ *               logits, row A the baseline), 16-byte aligned
+ *   bias        b   [A+1]    fp32 device, or NULL (no bias)
+ *   logits_out  z^pi [M, A]  fp32 device (the layout vtrace_loss_and_grad reads)
+ *   values_out  V    [M]     fp32 device
+ * Outputs must not overlap the inputs.  Caller owns every buffer.  Errors: VT_ERR_SHAPE
+ * (M, H or A out of range), VT_ERR_INVALID_ARG (NULL array), VT_ERR_ALIGNMENT,
+ * VT_ERR_DEVICE, VT_ERR_CUDA.  One persistent launch on `stream`; deterministic (fixed
+ * accumulation order); capturable in a CUDA graph. */
+vt_status vtrace_output_layer(int64_t M, int32_t H, int32_t A, const void* hidden,
+                              const void* w_t, const float* bias, float* logits_out,
+                              float* values_out, vt_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

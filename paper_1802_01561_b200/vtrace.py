@@ -35,7 +35,8 @@ EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_f
                     "vtrace_loss_and_grad", "vtrace_loss_and_grad_from_host",
                     "vtrace_read_device_status", "vtrace_status_string", "vtrace_version",
                     "vtrace_kernel_for", "vtrace_rmsprop_workspace_bytes", "vtrace_rmsprop_step",
-                    "vtrace_rmsprop_step_multi", "vtrace_rmsprop_step_learners")
+                    "vtrace_rmsprop_step_multi", "vtrace_rmsprop_step_learners",
+                    "vtrace_output_layer")
 
 
 class VtraceError(RuntimeError):
@@ -115,6 +116,8 @@ def load_library(path: str = LIB_PATH):
                                                  ctypes.c_int32, ctypes.POINTER(_RmsParams), P, P,
                                                  ctypes.c_size_t, P]
     lib.vtrace_rmsprop_step_learners.restype = ctypes.c_int
+    lib.vtrace_output_layer.argtypes = [i64, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P]
+    lib.vtrace_output_layer.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -454,3 +457,33 @@ def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
                                        ctypes.byref(prm), _ptr(global_norm_out), ws.ptr,
                                        ws.nbytes, _stream(params.device))
     _check(st, "vtrace_rmsprop_step_multi")
+
+
+def output_layer(hidden: torch.Tensor, w_t: torch.Tensor, bias: torch.Tensor | None = None,
+                 logits_out: torch.Tensor | None = None, values_out: torch.Tensor | None = None):
+    """NEXT #3 (reading r12): ``[z^pi | V] = h W + b`` on the tensor cores.
+    ``hidden`` [T, B, H] (or [M, H]) bf16, ``w_t`` = W^T [A+1, H] bf16, ``bias`` [A+1] fp32
+    or None.  Returns (logits [.., A] fp32, values [..] fp32) -- the layouts
+    :func:`loss_and_grad` reads.  Marshalling only: vtrace_output_layer does the work."""
+    if hidden.dtype != torch.bfloat16 or w_t.dtype != torch.bfloat16:
+        raise TypeError("output_layer: hidden and w_t must be bfloat16")
+    lead = tuple(hidden.shape[:-1])
+    H = int(hidden.shape[-1])
+    A = int(w_t.shape[0]) - 1
+    if w_t.dim() != 2 or int(w_t.shape[1]) != H:
+        raise ValueError("output_layer: w_t must be [A+1, H]")
+    M = 1
+    for d in lead:
+        M *= int(d)
+    _contig(hidden, w_t)
+    if bias is not None:
+        bias = bias.to(device=hidden.device, dtype=torch.float32).contiguous()
+    dev = hidden.device
+    if logits_out is None:
+        logits_out = torch.empty(lead + (A,), dtype=torch.float32, device=dev)
+    if values_out is None:
+        values_out = torch.empty(lead, dtype=torch.float32, device=dev)
+    st = load_library().vtrace_output_layer(M, H, A, _ptr(hidden), _ptr(w_t), _ptr(bias),
+                                            _ptr(logits_out), _ptr(values_out), _stream(dev))
+    _check(st, "vtrace_output_layer")
+    return logits_out, values_out
