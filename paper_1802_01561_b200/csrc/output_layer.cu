@@ -55,7 +55,11 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int 
 
 // KB = H / 64 swizzle atoms per row; NBUF ring depth
 template <int KB, int NBUF>
+#ifdef OL_NO_MINBLOCKS  // A/B only
+__global__ void __launch_bounds__(THREADS)
+#else
 __global__ void __launch_bounds__(THREADS, 1)
+#endif
 output_layer_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap wmap,
                     const float* __restrict__ bias, float* __restrict__ z_out,
                     float* __restrict__ v_out, int M, int A) {

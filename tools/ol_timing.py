@@ -18,7 +18,7 @@ if os.environ.get("OL_DATA") == "dyadic":  # A/B: value pattern of the h stream
 else:
     h = torch.randn((M, H), generator=g, device="cuda:0").to(torch.bfloat16)
 w = (torch.randn((A + 1, H), generator=g, device="cuda:0") * 0.1).to(torch.bfloat16)
-b = torch.randn(A + 1, generator=g, device="cuda:0")
+b = None if os.environ.get("OL_NOBIAS") else torch.randn(A + 1, generator=g, device="cuda:0")
 z = torch.empty((M, A), device="cuda:0")
 v = torch.empty(M, device="cuda:0")
 for _ in range(5):
@@ -34,6 +34,6 @@ e1.record(s)
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / n
 nbytes = M * H * 2 + (A + 1) * H * 2 + M * (A + 1) * 4 + (A + 1) * 4
-print(json.dumps({"kernel": "vtrace_output_layer", "data": os.environ.get("OL_DATA", "normal"), "M": M, "H": H, "A": A, "us": round(us, 2),
+print(json.dumps({"kernel": "vtrace_output_layer", "data": os.environ.get("OL_DATA", "normal"), "bias": b is not None, "defines": os.environ.get("VTRACE_DEFINES", ""), "M": M, "H": H, "A": A, "us": round(us, 2),
                   "algorithmic_bytes": nbytes, "GBps": round(nbytes / us / 1e3, 1),
                   "frac_of_measured_hbm": round(nbytes / us / 1e3 / 6544.7, 3)}))
