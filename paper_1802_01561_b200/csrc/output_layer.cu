@@ -28,6 +28,7 @@ constexpr int BM = 128;        // rows per tile (MMA M)
 constexpr int BN = 32;         // output columns per MMA (A + 1 <= 32)
 constexpr int THREADS = 256;
 constexpr int SMEM_LIMIT = 232448;
+constexpr int SO_LD = BN + 1;   // row stride (floats) of the epilogue staging tile
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -65,12 +66,12 @@ output_layer_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_const
                     float* __restrict__ v_out, int M, int A) {
   constexpr uint32_t STAGE = KB * 16384;  // 128 rows x 64 k x 2 B per atom
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-byte alignment for the swizzled atoms, derived from smem_raw so the compiler
+  // keeps the shared state space (STS/LDS, not generic stores) for the staging below
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sw = smem_u32(smem);               // W^T: KB atoms of 32 rows x 128 B
   const uint32_t sa0 = sw + KB * 4096;              // NBUF stages
-  float* sz = reinterpret_cast<float*>(smem + KB * 4096 + NBUF * STAGE);  // [128][A]
-  float* sv = sz + BM * (BN - 1);                                          // [128]
+  float* so = reinterpret_cast<float*>(smem + KB * 4096 + NBUF * STAGE);  // [128][SO_LD]
   __shared__ uint64_t full[NBUF], wbar, mbar;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -151,21 +152,22 @@ output_layer_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_const
             "=r"(v[31])
           : "r"(tmem + ((uint32_t)(warp * 32) << 16)));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
+      // all 32 accumulator columns, unconditionally (no per-column branches); the row
+      // stride SO_LD = 33 keeps the 32 lanes' stores on distinct banks
       const int r = warp * 32 + lane;
 #pragma unroll
-      for (int n = 0; n < BN; ++n) {
-        const float bn = __shfl_sync(0xffffffffu, b_lane, n);
-        const float x = __uint_as_float(v[n]) + bn;
-        if (n < A) sz[r * A + n] = x;
-        else if (n == A) sv[r] = x;
-      }
+      for (int n = 0; n < BN; ++n)
+        so[r * SO_LD + n] = __uint_as_float(v[n]) + __shfl_sync(0xffffffffu, b_lane, n);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     const int row0 = tile * BM, rows = min(BM, M - row0);
     float* zdst = z_out + (size_t)row0 * A;
-    for (int i = tid; i < rows * A; i += THREADS) zdst[i] = sz[i];
-    for (int i = tid; i < rows; i += THREADS) v_out[row0 + i] = sv[i];
+    for (int i = tid; i < rows * A; i += THREADS) {
+      const int r = i / A;
+      zdst[i] = so[r * SO_LD + (i - r * A)];
+    }
+    for (int i = tid; i < rows; i += THREADS) v_out[row0 + i] = so[i * SO_LD + A];
     __syncthreads();
   }
   if (warp == 0)
@@ -210,9 +212,9 @@ vt_status device_sms(int* sms) {
 template <int KB>
 vt_status launch(const CUtensorMap& hm, const CUtensorMap& wm, const float* bias, float* z,
                  float* v, int M, int A, int sms, cudaStream_t st) {
-  constexpr int NBUF = std::min(4, (SMEM_LIMIT - 1024 - KB * 4096 - BM * BN * 4) / (KB * 16384));
+  constexpr int NBUF = std::min(4, (SMEM_LIMIT - 1024 - KB * 4096 - BM * SO_LD * 4) / (KB * 16384));
   static_assert(NBUF >= 2, "ring too shallow");
-  constexpr int SMEM = 1024 + KB * 4096 + NBUF * KB * 16384 + BM * BN * 4;
+  constexpr int SMEM = 1024 + KB * 4096 + NBUF * KB * 16384 + BM * SO_LD * 4;
   auto kern = output_layer_kernel<KB, NBUF>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
     return VT_ERR_CUDA;
