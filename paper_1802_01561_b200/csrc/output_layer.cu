@@ -116,6 +116,10 @@ output_layer_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_const
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)(BM >> 4) << 24);
   const float b_lane = (lane <= A && bias != nullptr) ? bias[lane] : 0.f;
+  // ceil(2^32 / A): floor(i * a_magic / 2^32) = floor(i / A) while i * (a_magic - 2^32/A)
+  // < 2^32 / A, i.e. for every i < 128 * 31 (error < 4e3 / 2^32 < 1 / A); A = 1 wraps to 0
+  // and takes r = i (checked exhaustively on the host for A = 2..31)
+  const uint32_t a_magic = (uint32_t)((0x100000000ull + (uint32_t)A - 1) / (uint32_t)A);
 
   for (int j = 0;; ++j) {
     const int tile = blockIdx.x + j * gridDim.x;
@@ -164,7 +168,7 @@ output_layer_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_const
     const int row0 = tile * BM, rows = min(BM, M - row0);
     float* zdst = z_out + (size_t)row0 * A;
     for (int i = tid; i < rows * A; i += THREADS) {
-      const int r = i / A;
+      const int r = A == 1 ? i : (int)__umulhi((uint32_t)i, a_magic);  // == i / A
       zdst[i] = so[r * SO_LD + (i - r * A)];
     }
     for (int i = tid; i < rows; i += THREADS) v_out[row0 + i] = so[i * SO_LD + A];
