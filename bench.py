@@ -58,10 +58,11 @@ def parse():
                          "steps can overlap (0: no overlap at N > 1)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
-    ap.add_argument("--path", choices=["vtrace", "update"], default="vtrace",
+    ap.add_argument("--path", choices=["vtrace", "update", "head"], default="vtrace",
                     help="update: the learner's parameter update after the backward "
                          "(SURVEY 8(f) NEXT #4: gradient all-reduce at N > 1, global-norm "
-                         "clip, RMSProp) instead of the V-trace path")
+                         "clip, RMSProp) instead of the V-trace path; head: the tcgen05 output "
+                         "layer [z|V] = hW + b in front of the path (NEXT #3)")
     ap.add_argument("--update-collective", choices=["symm", "nccl"], default="symm",
                     help="N > 1 on the update path: symm = the kernel sums every learner's "
                          "gradient over NVLink from symmetric memory (fused); nccl = NCCL "
@@ -809,10 +810,117 @@ def run_update(args):
     print(json.dumps(line), flush=True)
 
 
+# --path head: the output layer in front of the path
+
+
+def run_head(args):
+    """K launches of vtrace_output_layer at the `large` config's T*B rows (H = 256, A = 18).
+    Each rank computes its own T*B rows (weak scaling, no collective).  h (419 MB) is
+    larger than L2, and two copies are alternated, so no flush is needed."""
+    world, rank, local = dist_env()
+    init_dist(world, local)
+    torch.cuda.set_device(local)
+    import paper_1802_01561_b200 as pkg
+    T, B, H, A = 100, 8192, 256, 18
+    M = T * B
+    g = torch.Generator(device="cuda").manual_seed(100 + rank)
+    hs = [torch.randn((M, H), generator=g, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    w = (torch.randn((A + 1, H), generator=g, device="cuda") * 0.1).to(torch.bfloat16)
+    b = torch.randn(A + 1, generator=g, device="cuda")
+    z = torch.empty((M, A), device="cuda")
+    v = torch.empty(M, device="cuda")
+    s_main = torch.cuda.Stream()
+    K, W = args.steps, max(args.warmup, 3)
+    with torch.cuda.stream(s_main):
+        for i in range(W):
+            pkg.output_layer(hs[i % 2], w, b, z, v)
+    torch.cuda.synchronize()
+    barrier(world)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    tw0 = time.time()
+    e0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for i in range(K):
+            pkg.output_layer(hs[i % 2], w, b, z, v)
+    e1.record(s_main)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if sampler:
+        sampler.stop()
+    barrier(world)
+    step_ms = max_over_ranks(e0.elapsed_time(e1), world) / K
+    e2e = None
+    if not args.no_e2e:  # h from pinned host memory, V read back, every step
+        h_host = hs[0].cpu().pin_memory()
+        v_host = torch.empty(M, dtype=torch.float32).pin_memory()
+        Ke = min(K, 10)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s_main)
+        with torch.cuda.stream(s_main):
+            for i in range(Ke):
+                hs[0].copy_(h_host, non_blocking=True)
+                pkg.output_layer(hs[0], w, b, z, v)
+                v_host.copy_(v, non_blocking=True)
+        a1.record(s_main)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(a0.elapsed_time(a1), world) / Ke
+        e2e = {"value": world * M / (e2e_ms * 1e-3), "unit": "rows/s",
+               "h2d_bytes_per_step": M * H * 2, "d2h_bytes_per_step": M * 4, "ms_per_step": e2e_ms}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import output_layer_oracle as ol
+        rows = 16384
+        hh = hs[0][:rows].float().cpu().numpy().astype("float64").reshape(rows, 1, H)
+        Wn = w.float().cpu().numpy().astype("float64").T
+        bn = b.cpu().numpy().astype("float64")
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < min(args.cpu_seconds, 5.0) or reps == 0:
+            ol.output_layer(hh, Wn, bn)
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        cpu = {"value": rows / dt, "unit": "rows/s", "cores": torch.get_num_threads(),
+               "kind": "oracle", "sample": f"{reps} x oracle.output_layer_oracle.output_layer on "
+               f"rows [0, {rows}) (numpy fp64 matmul, BLAS threads)"}
+    if rank != 0:
+        return
+    peak, peak_src = load_peak()
+    alg = M * H * 2 + (A + 1) * H * 2 + M * (A + 1) * 4 + (A + 1) * 4
+    achieved = alg / (step_ms * 1e-3) / 1e9
+    line = {
+        "metric": "output_layer_rows_per_s", "value": world * M / (step_ms * 1e-3),
+        "unit": "rows/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 in, f32 accumulate (tcgen05), f32 out", "path": "head",
+        "data": "synthetic (seeded N(0,1) hidden, N(0,0.01) weights)",
+        "config": {"workload": "output layer at large: T=100 B=8192 H=256 A=18",
+                   "parallelism": f"dp{world}", "collective": "none",
+                   "l2": "h (419 MB per copy, 2 copies alternated) exceeds L2", "timing": "eager"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "output_layer_kernel",
+                     "kernel_ms": step_ms, "algorithmic_bytes_per_launch": alg,
+                     "peak_source": peak_src},
+        "gpu_launches": K,
+        "clocks": sampler.summary(tw0, tw1) if sampler else None,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 if __name__ == "__main__":
     a = parse()
     try:
-        if a.path == "update":
+        if a.path == "head":
+            if a.impl == "reference":
+                print(json.dumps({"impl": "reference", "path": "head", "unavailable":
+                                  "the head path's CPU baseline is in the ours line"}))
+            else:
+                run_head(a)
+        elif a.path == "update":
             if a.impl == "reference":
                 print(json.dumps({"impl": "reference", "path": "update", "unavailable":
                                   "the update path's CPU baseline is in the ours line"}))
