@@ -196,3 +196,23 @@ def test_rmsprop_learners_host_checks(lib):
     assert call([128, 136], 2) == 1    # self out of range
     assert call([128, 132], 0) == 5    # flags not 8-byte aligned
     assert call([128, 136], 1) == 6    # then the workspace check
+
+
+def test_output_layer_host_checks(lib):
+    """vtrace_output_layer (NEXT #3) validates shapes, pointers and alignment on the host,
+    before touching a device: H not a multiple of 64 or > 256, A + 1 > 32, M < 0 ->
+    VT_ERR_SHAPE; M = 0 -> no-op; NULL -> VT_ERR_INVALID_ARG; misaligned h -> VT_ERR_ALIGNMENT."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    base = (ctypes.addressof(buf) + 255) & ~255
+    p = ctypes.c_void_p(base)
+    f = lib.vtrace_output_layer
+    assert f(128, 100, 9, p, p, None, p, p, None) == 2
+    assert f(128, 320, 9, p, p, None, p, p, None) == 2
+    assert f(128, 256, 32, p, p, None, p, p, None) == 2
+    assert f(128, 256, 0, p, p, None, p, p, None) == 2
+    assert f(-1, 256, 9, p, p, None, p, p, None) == 2
+    assert f(0, 256, 9, None, None, None, None, None, None) == 0
+    assert f(128, 256, 9, None, p, None, p, p, None) == 1
+    assert f(128, 256, 9, p, p, None, p, None, None) == 1
+    assert f(128, 256, 9, ctypes.c_void_p(base + 8), p, None, p, p, None) == 5
+    assert f(128, 256, 9, p, ctypes.c_void_p(base + 4), None, p, p, None) == 5
