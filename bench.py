@@ -900,7 +900,8 @@ def run_head(args):
                    "parallelism": f"dp{world}", "collective": "none",
                    "l2": "h (419 MB per copy, 2 copies alternated) exceeds L2", "timing": "eager"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "output_layer_kernel",
+                     "frac": achieved / peak, "traffic": load_traffic("head:large"),
+                     "kernel": "output_layer_kernel",
                      "kernel_ms": step_ms, "algorithmic_bytes_per_launch": alg,
                      "peak_source": peak_src},
         "gpu_launches": K,
