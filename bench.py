@@ -5,11 +5,14 @@ Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` (torchrun f
 N > 1, one rank per GPU, NCCL) prints ONE JSON line on rank 0.
 
 A "step" is one learner update's hot path over one batch: the fused
-vtrace_loss_and_grad kernel on this rank's [T, B, A] trajectories (all SURVEY
+vtrace_loss_and_grad kernel on this rank's [T, B/N, A] trajectories (all SURVEY
 8(a) rows a1-a12), plus, for N > 1, the NCCL all-reduce of the 8 fp64 partial
-sums (row a13, issued on a side stream so it overlaps the next step's kernel).
-Weak scaling: every rank owns its own B = 8192 trajectories (the paper's
-synchronous learners each consume their own batch).
+sums (row a13, issued on a side stream so it overlaps the next step's kernel) --
+the product's learner.LearnerStep.  Default at N > 1: strong scaling, the
+BASELINE config's B = 8192 trajectories column-sharded over the N synchronous
+learners; --weak gives every rank its own B = 8192.
+Without WORLD_SIZE in the environment, ``--gpus N`` (N > 1) launches the N ranks
+itself (torch.distributed.run, 127.0.0.1) and exits with their status.
 
 Workload (default): BASELINE.json configs[3], "large": T=100, B=8192, A=18,
 bf16 logits, clip[-1,1] rewards; inputs resident in HBM, rotated over R copies
@@ -47,8 +50,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="large")
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: the config's B is the GLOBAL batch")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank gets the config's B (default at N > 1: "
+                         "strong scaling, the config's B is the GLOBAL batch)")
+    ap.add_argument("--strong", action="store_true", help=argparse.SUPPRESS)  # (the default)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=100)
@@ -223,11 +228,14 @@ def algorithmic_bytes(T, B, A, elem, mu_lp=False):
 
 
 def make_rank_inputs(cfg, rank, world, strong):
+    """Strong scaling: this rank's column shard of the config's global batch (shards of
+    8-column units, so every shard keeps 16-byte TMA segments); weak: its own batch."""
+    from paper_1802_01561_b200 import learner
     from paper_1802_01561_b200 import workload as wl
-    if strong:
+    if strong and world > 1:
         full = wl.make_inputs(cfg.name)
-        per = cfg.B // world
-        return wl.column_slice(full, rank * per, (rank + 1) * per)
+        b0, b1 = learner.shard_columns(cfg.B, world, rank, align=8 if cfg.B % 8 == 0 else 1)
+        return wl.column_slice(full, b0, b1)
     return wl.make_inputs(cfg.name, seed=cfg.seed + 7919 * rank)
 
 
@@ -237,20 +245,21 @@ def make_rank_inputs(cfg, rank, world, strong):
 
 def run_ours(args):
     world, rank, local = dist_env()
-    if world != args.gpus and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     dist = init_dist(world, local)
     torch.cuda.set_device(local)
     import paper_1802_01561_b200 as pkg
+    from paper_1802_01561_b200 import learner
     from paper_1802_01561_b200 import vtrace as vt
     from paper_1802_01561_b200 import workload as wl
 
     cfg = wl.CONFIGS[args.config]
-    inp = make_rank_inputs(cfg, rank, world, args.strong)
+    strong = not args.weak
+    inp = make_rank_inputs(cfg, rank, world, strong)
     mu_lp = args.behaviour == "log_probs"
     if mu_lp:
         inp = with_behaviour_log_probs(inp)
     T, B, A = inp["T"], inp["B"], inp["A"]
+    B_global = B * world if not strong else cfg.B
     elem = 2 if inp["dtype"] == wl.DTYPE_BF16 else 4
     host = pkg.tensors_from_workload(inp, "cpu", pin=True)
     base = {k: v.to("cuda", non_blocking=True) for k, v in host.items()}
@@ -263,40 +272,25 @@ def run_ours(args):
                                                device="cuda"),
              "grad_values": torch.empty(T, B, dtype=torch.float32, device="cuda"),
              "partials": torch.zeros(8, dtype=torch.float64, device="cuda")} for _ in range(R)]
-    ws = pkg.Workspace(T, B, A, inp["dtype"])
     kw = dict(reward_mode=inp["reward_mode"], baseline_cost=wl.BASELINE_COST,
               entropy_cost=wl.ENTROPY_COST, rho_bar=wl.RHO_BAR, c_bar=wl.C_BAR)
-    # consecutive learner steps: each step's inputs are a fresh (rotated) trajectory
-    # batch, never the previous step's outputs, so the step may overlap the previous
-    # kernel's tail (programmatic dependent launch; --no-overlap: plain stream order)
-    # (N > 1: the side-stream NCCL collective of step k needs an SM while step k+1's
-    # CTAs take every SM the previous step releases; with no SM left to it the collective
-    # waited behind the next step (40.3 vs 37.9 us at N=2), so the kernel leaves
-    # --reserve-sms (1) SM free: 34.3 us at N=2)
-    # (only the balanced kernel can leave SMs free; with one-warp CTAs the collective
-    # still waits -- strong scaling at N=2: 31.1 vs 25.7 us -- so those keep stream order)
-    overlap = not args.no_overlap and (
-        world == 1 or (args.reserve_sms > 0 and vt.kernel_for(T, B, A, inp["dtype"])
-                       == "vtrace_ctb_kernel"))
-    if world > 1 and args.reserve_sms > 0:  # SMs left free for the NCCL collective
-        os.environ["VTRACE_RESERVE_SMS"] = str(args.reserve_sms)
-    kw_step = dict(kw, overlap_previous=overlap)
-    s_main = torch.cuda.Stream()
-    s_comm = torch.cuda.Stream()
+    # the product's learner step: kernel on the main stream, step k's partials
+    # all-reduce on a side stream under step k+1's kernel, consecutive steps overlapped
+    # (programmatic dependent launch: every step reads a fresh rotated batch), one SM
+    # left to the collective at N > 1
+    overlap = not args.no_overlap
+    step_obj = learner.LearnerStep(T, B, A, inp["dtype"], overlap=overlap,
+                                   reserve_sms=(args.reserve_sms if world > 1 else 0), **kw)
+    ws = step_obj.workspace
+    s_main = step_obj.stream
 
     def step(i):
-        o = outs[i % R]
-        x = sets[i % R]
-        pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw_step)
-        if world > 1:
-            s_comm.wait_stream(s_main)
-            with torch.cuda.stream(s_comm):
-                dist.all_reduce(o["partials"])
+        step_obj(sets[i % R], outs[i % R])
 
     # eager warm-up (also creates the NCCL communicator before any capture)
-    with torch.cuda.stream(s_main):
-        for i in range(max(args.warmup, 1)):
-            step(i)
+    for i in range(max(args.warmup, 1)):
+        step(i)
+    step_obj.join()
     torch.cuda.synchronize()
     barrier(world)
 
@@ -307,13 +301,7 @@ def run_ours(args):
     graph_mode = "cuda-graph"
 
     def capture(nsteps):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s_main):
-            for i in range(nsteps):
-                step(i)
-            if world > 1:
-                s_main.wait_stream(s_comm)
-        return g
+        return step_obj.capture([(sets[i % R], outs[i % R]) for i in range(nsteps)])
 
     try:
         g_full = capture(C) if n_full else None
@@ -325,11 +313,9 @@ def run_ours(args):
 
     def run_timed_body():
         if g_full is None and g_rem is None:
-            with torch.cuda.stream(s_main):
-                for i in range(K):
-                    step(i)
-                if world > 1:
-                    s_main.wait_stream(s_comm)
+            for i in range(K):
+                step(i)
+            step_obj.join()
         else:
             with torch.cuda.stream(s_main):
                 for _ in range(n_full):
@@ -337,7 +323,7 @@ def run_ours(args):
                 if g_rem is not None:
                     g_rem.replay()
 
-    # warm the graphs (untimed) with W more steps' worth of replays
+    # warm the graphs (untimed) with one more replay
     if g_full is not None or g_rem is not None:
         with torch.cuda.stream(s_main):
             (g_rem or g_full).replay()
@@ -362,6 +348,7 @@ def run_ours(args):
         sampler.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
     elapsed_max = max_over_ranks(elapsed_ms, world)
+    kw_step = dict(kw, workspace=ws, overlap_previous=overlap, sm_budget=step_obj.kw["sm_budget"])
 
     # kernel-only timing for the roofline: the same kernels, no collective
     Kk = min(K, 2000)
@@ -389,17 +376,15 @@ def run_ours(args):
 
     # eager launches (no graph): the latency-bound configs' per-call time
     Ke = min(K, 500)
-    with torch.cuda.stream(s_main):
-        for i in range(5):
-            step(i)
+    for i in range(5):
+        step(i)
+    step_obj.join()
     torch.cuda.synchronize()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ee0.record(s_main)
-    with torch.cuda.stream(s_main):
-        for i in range(Ke):
-            step(i)
-        if world > 1:
-            s_main.wait_stream(s_comm)
+    for i in range(Ke):
+        step(i)
+    step_obj.join()
     ee1.record(s_main)
     torch.cuda.synchronize()
     eager_ms = max_over_ranks(ee0.elapsed_time(ee1), world) / Ke
@@ -424,7 +409,7 @@ def run_ours(args):
         eb.record(s_main)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(ea.elapsed_time(eb), world) / Ke
-        e2e = {"value": T * B * world / (e2e_ms * 1e-3), "unit": UNIT,
+        e2e = {"value": T * B_global / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 64,
                "ms_per_step": e2e_ms}
 
@@ -441,7 +426,7 @@ def run_ours(args):
     if rank != 0:
         return
     ms_per_step = elapsed_max / K
-    value = T * B * world / (ms_per_step * 1e-3)
+    value = T * B_global / (ms_per_step * 1e-3)
     peak, peak_src = load_peak()
     alg = algorithmic_bytes(T, B, A, elem, mu_lp)
     achieved = alg / (kernel_ms * 1e-3) / 1e9
@@ -450,22 +435,23 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+        "scaling": "strong" if strong and world > 1 else "weak", "vs_baseline": None,
         "dtype": ("bf16" if elem == 2 else "f32") + " logits; f32 exps with compensated "
                  "(exact-order) sums, f64 ratio and scan, f32 gradient epilogue",
         "data": "synthetic (seeded, DMLab/Atari-shaped; DESIGN.md input recipe)",
         "config": {"workload": cfg.name + ("+behaviour_log_probs" if mu_lp else ""),
                    "T": T, "B_per_gpu": B, "A": A, "behaviour": args.behaviour,
                    "logits_dtype": "bf16" if elem == 2 else "fp32",
-                   "global_batch": B * world, "seq_len": T, "parallelism": f"dp{world}",
+                   "global_batch": B_global, "seq_len": T, "parallelism": f"dp{world}",
                    "l2": f"inputs rotated over {R} HBM-resident copies "
                          f"({R} x {working / 1e6:.1f} MB >= 4 x L2)",
                    "timing": graph_mode,
                    "step_overlap": "programmatic dependent launch (overlap_previous: inputs are "
                                    "fresh batches)" if overlap else "none",
                    "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream"
-                                 + (f", {args.reserve_sms} SM reserved)" if overlap else ")")
-                   if world > 1 else "none"},
+                                 + (f", {args.reserve_sms} SM reserved)" if args.reserve_sms else ")")
+                   if world > 1 else "none",
+                   "step": "paper_1802_01561_b200.learner.LearnerStep"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": vt.kernel_for(T, B, A, inp["dtype"]), "kernel_ms": kernel_ms,
@@ -912,8 +898,32 @@ def run_head(args):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """--gpus N without a launcher: start the N ranks with torch.distributed.run on
+    127.0.0.1 (one process per GPU) and return their exit status."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse()
+    _world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        if torch.cuda.device_count() < a.gpus:
+            print(f"bench.py: --gpus {a.gpus} but only {torch.cuda.device_count()} CUDA devices",
+                  file=sys.stderr)
+            sys.exit(2)
+        sys.exit(spawn_ranks(a))
+    if _world != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={_world}", file=sys.stderr)
+        sys.exit(2)
     try:
         if a.path == "head":
             if a.impl == "reference":

@@ -127,7 +127,23 @@ typedef struct {
                                   the previous kernel's tail, and it waits for that
                                   kernel before its first global write.  0 = plain
                                   stream order (always safe)                         */
+  int32_t kernel;              /* vt_kernel: which kernel runs the call; 0 = automatic
+                                  (a pure function of the shape and pointer alignment,
+                                  vtrace_kernel_for).  A forced kernel that cannot take
+                                  the shape returns VT_ERR_SHAPE.  Tests / A-B only    */
+  int32_t sm_budget;           /* > 0: the column-block kernel plans for at most this
+                                  many SMs (e.g. leave SMs to a concurrent per-step
+                                  collective); 0 = every SM        */
 } vt_vtrace_params;
+
+/* Kernel choice (vt_vtrace_params.kernel). */
+typedef enum {
+  VT_KERNEL_AUTO = 0,
+  VT_KERNEL_COLUMN_BLOCK = 1, /* vtrace_cb_kernel: one CTA per SM owns a block of
+                                 trajectories over the whole unroll (TMA ring)       */
+  VT_KERNEL_LOOKBACK = 2      /* vtrace_fused_kernel: (8 trajectories x Tc steps)
+                                 units, decoupled look-back across time chunks       */
+} vt_kernel;
 
 typedef struct {
   float baseline_cost; /* c_v: "baseline loss scaling" 0.5 */

@@ -1,6 +1,6 @@
 """Builds libvtrace.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-Five objects (the look-back kernel + the C ABI; the column-task kernels for bf16
+Five objects (the look-back kernel + the C ABI; the column-block kernels for bf16
 and for fp32 logits; the learner update; the tcgen05 output layer) are compiled in parallel and linked into
 one shared library.
 """
@@ -15,12 +15,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libvtrace.so")
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, "vtrace_api.cu"), os.path.join(CSRC, "vtrace_ct_launch.cu"),
+SOURCES = [os.path.join(CSRC, "vtrace_api.cu"), os.path.join(CSRC, "vtrace_cb_launch.cu"),
            os.path.join(CSRC, "learner_update.cu"), os.path.join(CSRC, "output_layer.cu")]
-# (source, object, defines): the column-task unit is compiled once per logits dtype
+# (source, object, defines): the column-block unit is compiled once per logits dtype
 UNITS = [(SOURCES[0], "vtrace_api.o", []),
-         (SOURCES[1], "vtrace_ct_bf16.o", ["-DVT_CT_PART=0"]),
-         (SOURCES[1], "vtrace_ct_f32.o", ["-DVT_CT_PART=1"]),
+         (SOURCES[1], "vtrace_cb_bf16.o", ["-DVT_CB_PART=0"]),
+         (SOURCES[1], "vtrace_cb_f32.o", ["-DVT_CB_PART=1"]),
          (SOURCES[2], "learner_update.o", []),
          (SOURCES[3], "output_layer.o", [])]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

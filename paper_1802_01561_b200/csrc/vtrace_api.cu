@@ -9,13 +9,14 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <type_traits>
 
 #include "../../include/vtrace.h"
 #include "vtrace_kernels.cuh"
 #include "vtrace_rows.cuh"
-#include "vtrace_ct_host.h"
+#include "vtrace_cb_host.h"
 
 namespace vtb200 {
 
@@ -676,19 +677,18 @@ static Plan make_plan(long long T, long long B, int A, int elem) {
 }
 
 struct WsLayout {
-  size_t recs, cta, ct_task, ct_group, ct_count, total;
+  size_t recs, cta, cb_recs, cb_count, total;
 };
 
 static WsLayout ws_layout(const Plan& p) {
   WsLayout w;
   w.recs = 256;
   w.cta = a128(w.recs + (size_t)p.units * BC * RECS_PER_COL * sizeof(TagRec));
-  w.ct_task = a128(w.cta + (size_t)kMaxCtas * NPART * sizeof(double));
-  const size_t tasks = (size_t)(p.G * BC + CT_COLS - 1) / CT_COLS;  // >= ceil(B / 4)
-  const size_t groups = (tasks + CT_GROUP - 1) / CT_GROUP;
-  w.ct_group = a128(w.ct_task + tasks * NPART * sizeof(TagRec));
-  w.ct_count = a128(w.ct_group + groups * NPART * sizeof(TagRec));
-  w.total = a128(w.ct_count + (groups + 1) * sizeof(unsigned int));
+  // column-block kernel: one record set per CTA (at most ceil(B / 4) CTAs) + a ticket
+  w.cb_recs = a128(w.cta + (size_t)kMaxCtas * NPART * sizeof(double));
+  const size_t ctas = ((size_t)p.G * BC + 3) / 4;  // >= ceil(B / 4)
+  w.cb_count = a128(w.cb_recs + ctas * NPART * sizeof(TagRec));
+  w.total = a128(w.cb_count + sizeof(unsigned int));
   return w;
 }
 
@@ -698,9 +698,6 @@ static size_t ws_bytes_for(const Plan& p) { return ws_layout(p).total; }
 static std::mutex g_mu;
 static int g_dev_ok[64];  // 0 unknown, 1 ok, 2 bad
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-// debug hook (not part of the ABI): per-CTA phase timestamps of the next launches
-static unsigned long long* g_timing = nullptr;
-static int g_timing_iters = 0;
 
 static vt_status check_device() {
   int dev = 0;
@@ -744,6 +741,25 @@ static bool encode_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, 
   return r == CUDA_SUCCESS;
 }
 
+// Logits [T][B][A] viewed as [T][B / (4g)][4gA] (column segments of 4g trajectories),
+// with the segment index as the OUTER box dimension: a box {4gA, Ts, nseg_box} lands in
+// shared memory as [segment][t][4gA], so one warp's 4 columns x 8 steps are 32
+// consecutive rows (column-block kernel).
+static bool encode_logits_3d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem,
+                             int seg, long long T, long long nseg, long long row_elems, int box_t,
+                             int box_seg) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)seg, (cuuint64_t)T, (cuuint64_t)nseg};
+  cuuint64_t strides[2] = {(cuuint64_t)(row_elems * elem), (cuuint64_t)((long long)seg * elem)};
+  cuuint32_t box[3] = {(cuuint32_t)seg, (cuuint32_t)box_t, (cuuint32_t)box_seg};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 static bool encode_1d(CUtensorMap* m, const void* base, long long n, int box) {
   auto enc = get_encode();
   if (!enc) return false;
@@ -762,18 +778,19 @@ template <typename LT, int A_CT, bool LOSS, bool TMA, int MODE, bool GEN>
 static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& plan,
                             cudaStream_t st) {
   auto kern = vtrace_fused_kernel<LT, A_CT, LOSS, TMA, MODE, GEN>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int num_sms = 0;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kMaxSmem);
-    int dev = 0;
-    if (attr_err == cudaSuccess) attr_err = cudaGetDevice(&dev);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  });
-  if (attr_err != cudaSuccess) return VT_ERR_CUDA;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return VT_ERR_CUDA;
+  // the dynamic shared-memory limit is a per-device function attribute: set once per device
+  static std::atomic<unsigned long long> attr_set{0};
+  const unsigned long long bit = 1ull << dev;
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem) !=
+        cudaSuccess)
+      return VT_ERR_CUDA;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  const int num_sms = cb_num_sms(dev);
+  if (num_sms <= 0) return VT_ERR_CUDA;
   // persistent, co-resident grid: every CTA slot of the device, never more CTAs
   // than units (cooperative launch guarantees co-residency for the look-back)
   int per_sm = 0;
@@ -786,8 +803,8 @@ static vt_status launch_one(const Params& P, const TmaMaps& maps, const Plan& pl
   Params Pl = P;
   Pl.stride_q = (int)(grid / P.G);
   Pl.stride_r = (int)(grid % P.G);
-  Pl.timing = g_timing;
-  Pl.timing_iters = g_timing_iters;
+  Pl.timing = nullptr;
+  Pl.timing_iters = 0;
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)grid);
@@ -824,32 +841,12 @@ template <typename LT, bool LOSS>
 static vt_status dispatch(const Params& P, const TmaMaps& maps, const Plan& plan, bool tma,
                           cudaStream_t st) {
   // plain V-trace from logits takes the instantiation with the GEN logic compiled out
-  // (MUFU mode; the fp64 reference mode always uses the general one)
   const bool gen = P.correction != VT_CORRECTION_VTRACE || P.q_values != 0 || P.mu_lp != 0;
-  if (exp_mode() == EXP_MUFU) {
-    return gen ? dispatch_t<LT, LOSS, EXP_MUFU, true>(P, maps, plan, tma, st)
-               : dispatch_t<LT, LOSS, EXP_MUFU, false>(P, maps, plan, tma, st);
-  }
-  return dispatch_t<LT, LOSS, EXP_F64, true>(P, maps, plan, tma, st);
+  return gen ? dispatch_t<LT, LOSS, EXP_MUFU, true>(P, maps, plan, tma, st)
+             : dispatch_t<LT, LOSS, EXP_MUFU, false>(P, maps, plan, tma, st);
 }
 
 static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
-
-// ---- column-task kernel selection ----------------------------------------------------
-constexpr long long kCtMinTasks = 1024;  // >= ~7 warps per SM
-
-// VTRACE_KERNEL=lookback forces the look-back kernel, =ct the column-task kernel where
-// it applies (tests, A/B)
-static int kernel_override() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("VTRACE_KERNEL");
-    v = (e && e[0] == 'l') ? 0 : ((e && e[0] == 'c') ? 2 : 1);
-  }
-  return v;
-}
-static bool ct_enabled() { return kernel_override() != 0; }
-
 
 static vt_status check_params(const vt_vtrace_params* p) {
   if (!p) return VT_ERR_INVALID_ARG;
@@ -867,29 +864,33 @@ static vt_status check_params(const vt_vtrace_params* p) {
   if (p->q_from_values != 0 && p->q_from_values != 1) return VT_ERR_PARAM;
   if (p->behaviour_log_probs != 0 && p->behaviour_log_probs != 1) return VT_ERR_PARAM;
   if (p->overlap_previous != 0 && p->overlap_previous != 1) return VT_ERR_PARAM;
+  if (p->kernel < VT_KERNEL_AUTO || p->kernel > VT_KERNEL_LOOKBACK) return VT_ERR_PARAM;
+  if (p->sm_budget < 0) return VT_ERR_PARAM;
   return VT_OK;
 }
 
-enum KernelChoice { K_CT = 0, K_LOOKBACK_TMA = 1, K_LOOKBACK_PLAIN = 2 };
+enum KernelChoice { K_CB = 0, K_LOOKBACK_TMA = 1, K_LOOKBACK_PLAIN = 2 };
 
-// Which kernel a call takes (a pure function of the shape and pointer alignment):
-// the column-task kernel for wide batches, else the look-back kernel, with TMA
-// staging when pitches and bases are 16-byte aligned.
+static unsigned out_mask_for(bool loss, bool vs, bool pg, bool lr, bool lp, bool lm) {
+  return (loss ? (OUT_DZ | OUT_DV) : 0u) | (vs ? OUT_VS : 0u) | (pg ? OUT_PG : 0u) |
+         (lr ? OUT_LR : 0u) | (lp ? OUT_LP : 0u) | (lm ? OUT_LM : 0u);
+}
+
+// Which kernel a call takes (a pure function of the shape, the pointer alignment and the
+// SM budget): the column-block kernel where its TMA boxes apply, else the look-back kernel,
+// with TMA staging when pitches and bases are 16-byte aligned.
 static KernelChoice choose_kernel(long long T, long long B, long long A, int elem,
-                                  const Plan& plan, bool ptrs16) {
+                                  const Plan& plan, bool ptrs16, bool mu_lp, unsigned out_mask,
+                                  int sms, int forced, CbPlan* cbp) {
   const bool tma = (A * BC <= 256) && (B * A < (1LL << 31)) && (T < (1LL << 31)) &&
                    ((B * A * elem) % 16 == 0) && ((B * 4) % 16 == 0) && ptrs16 &&
                    plan.Tc + 1 <= 256 && plan.smem <= kMaxSmem;
-  if (!tma) return K_LOOKBACK_PLAIN;
-  const long long tasks = (B + CT_COLS - 1) / CT_COLS;
-  // wide batches, or short unrolls at any width: a task's ceil(T / 8) chunks then take
-  // less than the look-back pipeline's fixed latency (atari T=20: 5.4 vs 8.6 us)
-  const bool wide_or_short = tasks >= kCtMinTasks || (T + CT_STEPS - 1) / CT_STEPS <= 4;
-  const bool ct = ct_enabled() && (wide_or_short || kernel_override() == 2) &&
-                  (A * elem) % 4 == 0 &&
-                  CT_COLS * A <= 256 && (B % CT_COLS) == 0 &&
-                  (T + CT_STEPS) * B < (1LL << 31);  // 32-bit row offsets
-  return ct ? K_CT : K_LOOKBACK_TMA;
+  CbPlan tmp;
+  CbPlan& cp = cbp ? *cbp : tmp;
+  const bool cb = ptrs16 && forced != VT_KERNEL_LOOKBACK &&
+                  cb_plan(T, B, (int)A, elem, mu_lp, out_mask, sms, cp);
+  if (cb) return K_CB;
+  return tma ? K_LOOKBACK_TMA : K_LOOKBACK_PLAIN;
 }
 
 static vt_status common_launch(bool loss, long long T, long long B, long long A, vt_dtype dt,
@@ -967,13 +968,62 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   P.cta_partials = reinterpret_cast<double*>(wsb + wl.cta);
 
   // TMA eligibility: 16-byte aligned bases and row pitches, box inner <= 256 elements
-  TmaMaps maps;
-  std::memset(&maps, 0, sizeof(maps));
   const bool ptrs16 = aligned(mu, 16) && aligned(pi, 16) && aligned(actions, 16) &&
                       aligned(disc, 16) && aligned(rew, 16) && aligned(val, 16) &&
-                      aligned(boot, 16) && (!loss || aligned(dlogits, 16));
-  const KernelChoice kc = choose_kernel(T, B, A, elem, plan, ptrs16);
-  bool tma = kc != K_LOOKBACK_PLAIN;
+                      aligned(boot, 16) && (!loss || (aligned(dlogits, 16) && aligned(dvalues, 16))) &&
+                      (!vs || aligned(vs, 16)) && (!pg_adv || aligned(pg_adv, 16)) &&
+                      (!lr || aligned(lr, 16)) && (!lp || aligned(lp, 16)) && (!lm || aligned(lm, 16));
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return VT_ERR_CUDA;
+  const int all_sms = cb_num_sms(dev);
+  if (all_sms <= 0) return VT_ERR_CUDA;
+  const int sms = prm->sm_budget > 0 ? std::min(prm->sm_budget, all_sms) : all_sms;
+  const unsigned om = out_mask_for(loss, vs != nullptr, pg_adv != nullptr, lr != nullptr,
+                                   lp != nullptr, lm != nullptr);
+  CbPlan cp;
+  const KernelChoice kc = choose_kernel(T, B, A, elem, plan, ptrs16, mu_lp, om, sms,
+                                        prm->kernel, &cp);
+  if (prm->kernel == VT_KERNEL_COLUMN_BLOCK && kc != K_CB) return VT_ERR_SHAPE;
+  if (kc == K_CB) {
+    const CUtensorMapDataType ldt =
+        dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CbMaps cm;
+    std::memset(&cm, 0, sizeof(cm));
+    const int seg = 4 * cp.g * (int)A;  // elements per logits column segment
+    const long long nseg = B / (4 * cp.g);
+    bool ok = encode_logits_3d(&cm.pi, pi, ldt, elem, seg, T, nseg, B * A, cp.Ts, cp.ncg / cp.g) &&
+              (mu_lp ? encode_2d(&cm.mu, mu, f32, 4, B, T, cp.Bc, cp.Ts)
+                     : encode_logits_3d(&cm.mu, mu, ldt, elem, seg, T, nseg, B * A, cp.Ts, cp.ncg / cp.g)) &&
+              encode_2d(&cm.a, actions, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, B, T, cp.Bc, cp.Ts) &&
+              encode_2d(&cm.r, rew, f32, 4, B, T, cp.Bc, cp.Ts) &&
+              encode_2d(&cm.g, disc, f32, 4, B, T, cp.Bc, cp.Ts) &&
+              encode_2d(&cm.v, val, f32, 4, B, T, cp.Bc, cp.Ts + 1);
+    if (loss)
+      ok = ok && encode_logits_3d(&cm.dz, dlogits, ldt, elem, seg, T, nseg, B * A, cp.Ts, cp.ncg / cp.g) &&
+           encode_2d(&cm.dv, dvalues, f32, 4, B, T, cp.Bc, cp.Ts);
+    if (vs) ok = ok && encode_2d(&cm.vs, vs, f32, 4, B, T, cp.Bc, cp.Ts);
+    if (pg_adv) ok = ok && encode_2d(&cm.pg, pg_adv, f32, 4, B, T, cp.Bc, cp.Ts);
+    if (lr) ok = ok && encode_2d(&cm.lr, lr, f32, 4, B, T, cp.Bc, cp.Ts);
+    if (lp) ok = ok && encode_2d(&cm.lp, lp, f32, 4, B, T, cp.Bc, cp.Ts);
+    if (lm) ok = ok && encode_2d(&cm.lm, lm, f32, 4, B, T, cp.Bc, cp.Ts);
+    if (!ok) return VT_ERR_CUDA;
+    CbParams C;
+    std::memset(&C, 0, sizeof(C));
+    C.ncg = cp.ncg; C.nts = cp.nts; C.Ts = cp.Ts; C.J = cp.J; C.nstage = cp.nstage; C.g = cp.g;
+    C.Bc = cp.Bc;
+    C.pi = cp.pi; C.mu = cp.mu; C.a = cp.a; C.r = cp.r; C.gm = cp.gm; C.v = cp.v; C.dv = cp.dv;
+    C.vs = cp.vs; C.pg = cp.pg; C.lr = cp.lr; C.lp = cp.lp; C.lm = cp.lm; C.stage = cp.stage;
+    C.tx_bytes = cp.tx_bytes; C.out_mask = cp.out_mask; C.ebuf = cp.ebuf;
+    const WsLayout wl2 = ws_layout(plan);
+    C.cta_recs = reinterpret_cast<TagRec*>(wsb + wl2.cb_recs);
+    C.top_count = reinterpret_cast<unsigned int*>(wsb + wl2.cb_count);
+    return dt == VT_BFLOAT16 ? cb_launch_bf16(loss, P, C, cm, cp.grid, cp.smem, dev, st)
+                             : cb_launch_f32(loss, P, C, cm, cp.grid, cp.smem, dev, st);
+  }
+  TmaMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  bool tma = kc == K_LOOKBACK_TMA;
   if (tma) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -988,36 +1038,6 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
           (!loss || encode_2d(&maps.dz, dlogits, ldt, elem, B * A, T, BC * (int)A, plan.Tc));
   }
   if (plan.smem > kMaxSmem) return VT_ERR_SHAPE;
-
-  // column-task kernel: wide batches (enough 4-trajectory tasks to fill the GPU)
-  const long long tasks = (B + CT_COLS - 1) / CT_COLS;
-  const bool ct = tma && kc == K_CT;
-  if (ct) {
-    const CUtensorMapDataType ldt =
-        dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    TmaMaps cm;
-    std::memset(&cm, 0, sizeof(cm));
-    const bool ok =
-        (mu_lp || encode_2d(&cm.mu, mu, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS)) &&
-        encode_2d(&cm.pi, pi, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS) &&
-        (!loss || encode_2d(&cm.dz, dlogits, ldt, elem, B * A, T, CT_COLS * (int)A, CT_STEPS));
-    if (ok) {
-      const CtLayout cl = make_ct_layout((int)A, elem);
-      CtParams C;
-      std::memset(&C, 0, sizeof(C));
-      C.pi = (unsigned)cl.pi; C.mu = (unsigned)cl.mu; C.stage = (unsigned)cl.stage;
-      C.warp_bytes = (unsigned)cl.warp_bytes;
-      C.tasks = (int)tasks;
-      C.K = (int)((T + CT_STEPS - 1) / CT_STEPS);
-      const WsLayout wl2 = ws_layout(plan);
-      C.task_recs = reinterpret_cast<TagRec*>(wsb + wl2.ct_task);
-      C.timing = g_timing;
-      C.group_recs = reinterpret_cast<TagRec*>(wsb + wl2.ct_group);
-      C.group_count = reinterpret_cast<unsigned int*>(wsb + wl2.ct_count);
-      C.top_count = C.group_count + (C.tasks + CT_GROUP - 1) / CT_GROUP;
-      return ct_launch(dt == VT_BFLOAT16, loss, P, C, cm, st);
-    }
-  }
   if (dt == VT_BFLOAT16) {
     return loss ? dispatch<__nv_bfloat16, true>(P, maps, plan, tma, st)
                 : dispatch<__nv_bfloat16, false>(P, maps, plan, tma, st);
@@ -1157,30 +1177,14 @@ const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_d
   if (logits_dtype != VT_FLOAT32 && logits_dtype != VT_BFLOAT16) return "none (invalid dtype)";
   const int elem = logits_dtype == VT_BFLOAT16 ? 2 : 4;
   const Plan plan = make_plan(T, B, (int)A, elem);
-  switch (choose_kernel(T, B, A, elem, plan, true)) {
-    case K_CT: {
-      CtParams C;
-      std::memset(&C, 0, sizeof(C));
-      C.warp_bytes = (unsigned)make_ct_layout((int)A, elem).warp_bytes;
-      C.tasks = (int)((B + CT_COLS - 1) / CT_COLS);
-      C.K = (int)((T + CT_STEPS - 1) / CT_STEPS);
-      int S = 0, dev = 0;  // the balanced split needs the SM count of the current device
-      if (cudaGetDevice(&dev) == cudaSuccess &&
-          cudaDeviceGetAttribute(&S, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-          ct_plan_balanced(C, S))
-        return "vtrace_ctb_kernel";
-      return "vtrace_ct_kernel";
-    }
+  int dev = 0;
+  const int sms = cudaGetDevice(&dev) == cudaSuccess ? cb_num_sms(dev) : 0;
+  switch (choose_kernel(T, B, A, elem, plan, true, false, OUT_DZ | OUT_DV, sms > 0 ? sms : 148,
+                        VT_KERNEL_AUTO, nullptr)) {
+    case K_CB: return "vtrace_cb_kernel";
     case K_LOOKBACK_TMA: return "vtrace_fused_kernel";
     default: return "vtrace_fused_kernel (plain loads)";
   }
-}
-
-// Debug hook, not declared in include/vtrace.h: while set, every launch records
-// clock64() per CTA and iteration into buf[grid][iters][8] (device memory).
-void vtrace_debug_set_timing(void* buf, int32_t iters) {
-  g_timing = static_cast<unsigned long long*>(buf);
-  g_timing_iters = buf ? iters : 0;
 }
 
 }  // extern "C"

@@ -1,6 +1,6 @@
 // vtrace_kernels.cuh -- shared types and device helpers of the fused V-trace +
 // actor-critic loss + gradient kernels for sm_100a (the look-back kernel in
-// vtrace_api.cu, the column-task kernels in vtrace_ct.cuh).
+// vtrace_api.cu, the column-block kernel in vtrace_cb.cuh).
 //
 // Look-back kernel: a work unit = (column group of BC=8 trajectories) x (time chunk
 // of Tc <= 20 steps); unit ids run in REVERSE time order.  A co-resident persistent
@@ -23,8 +23,8 @@
 // Precision: every quantity that feeds the recursion (sum_j exp, the ratio,
 // delta, the scan) is carried well beyond fp32 (fp64 or compensated fp32);
 // the gradient epilogue is fp32 (its outputs are fp32/bf16).  See DESIGN.md.
-// The column-task kernels (vtrace_ct.cuh) follow the same steps with one warp per
-// 4 trajectories over the whole unroll.
+// The column-block kernel (vtrace_cb.cuh) follows the same steps with one warp per
+// 4 trajectories x 8 steps of a CTA-wide TMA tile.
 #pragma once
 
 #include <cuda.h>
@@ -248,6 +248,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
 __device__ __forceinline__ double shfl_down_d(double v, int off) {
   return __shfl_down_sync(0xffffffffu, v, off);

@@ -1,7 +1,6 @@
 // vtrace_rows.cuh -- row arithmetic shared by the look-back kernel (vtrace_api.cu)
-// and the column-task kernels (vtrace_ct_launch.cu), plus small shared constants.
+// and the column-block kernel (vtrace_cb.cuh), plus small shared constants.
 #pragma once
-#include <cstdlib>
 
 #include "../../include/vtrace.h"
 #include "vtrace_kernels.cuh"
@@ -12,16 +11,6 @@ __host__ __device__ inline size_t a128(size_t x) { return (x + 127) & ~size_t(12
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 constexpr size_t kMaxSmem = 220 * 1024;  // dynamic shared memory bound of every launch
-
-static inline int exp_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    // default: compensated MUFU exps; VTRACE_EXP_MODE=f64 selects fp64 exps (reference mode)
-    const char* e = getenv("VTRACE_EXP_MODE");
-    mode = (e && (e[0] == 'f' || e[0] == 'F' || e[0] == '0')) ? EXP_F64 : EXP_MUFU;
-  }
-  return mode;
-}
 
 // ---------------------------------------------------------------------------
 // Row arithmetic.  Each thread owns one row
@@ -112,7 +101,7 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
   const float mL = m * L16;                         // exact for bf16 m
   double S64a = 0.0;
   [[maybe_unused]] double S64b = 0.0;
-  float s_hi = 1.f, s_lo = 0.f, sd = 0.f, chk = 0.f;
+  float s_hi = 1.f, s_lo = 0.f, sd = 0.f, chk = 0.f, cw = 0.f;
   auto term = [&](float z, int j) {
     if constexpr (MODE == EXP_F64) {
       const double e = exp64((double)z - (double)m);
@@ -126,7 +115,12 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
         d = z - m;
       } else {
         d = z - m;
-        e = ex2_approx(d * L32);
+        const float y = d * L32;
+        e = ex2_approx(y);
+        // exact errors of d = z - m (TwoSum) and of y = d L32 (FMA residual)
+        const float bb = d - z;
+        const float dlo = (z - (d - bb)) + (-m - bb);
+        cw = fmaf(e, fmaf(dlo, L32, fmaf(d, L32, -y)), cw);
       }
       sd = fmaf(e, d, sd);  // NaN if some z is inf/nan (0 * inf for -inf)
 #ifdef VTRACE_SUM_F64
@@ -158,6 +152,7 @@ __device__ __forceinline__ void row_stats(const RowRegs<LT, A_CT>& R, int A, int
     const double S0 = (double)(s_hi - 1.f) + (double)s_lo;
 #endif
     S = S0 + (double)(sd * (EXACT_DIFF ? CORR16 : CORR32));
+    if constexpr (!EXACT_DIFF) S += (double)(cw * 0.693147182f);  // first order in the errors
     finite = isfinite(S) && isfinite(sd) && isfinite(m);
   }
 }

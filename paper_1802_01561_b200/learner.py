@@ -1,24 +1,39 @@
-"""Data-parallel learner plumbing (the paper's synchronous learners).
+"""Data-parallel learner step (the paper's synchronous learners).
 
-Each rank (one process per GPU) owns a contiguous block of trajectories
-(columns of the [T, B] batch) and runs the fused kernel on it with no
-data-path collective; the one exchange is the sum of the 8 fp64 partials
-(losses and gradient-norm sums), all-reduced over the process group.  The
-functions here are backend-agnostic (NCCL on GPUs, gloo in the CPU tests).
+Each rank (one process per GPU) owns a contiguous block of trajectories (columns
+of the [T, B] batch) and runs the fused V-trace + loss + gradient kernel on it
+with no data-path collective: trajectories are independent through every step of
+Section 4.  The one exchange is the sum of the 8 fp64 partials (losses and
+gradient-norm sums; the losses add over learners because the loss is summed over
+the batch), all-reduced over the process group.
+
+:class:`LearnerStep` is the product API of that step on a GPU: the kernel on a
+main stream, step k's 64-byte partials all-reduce on a side stream so that it runs
+under step k+1's kernel (nothing on the path consumes the reduced scalars), the
+kernel launched as a programmatic dependent of the previous step
+(``overlap_previous``: a step's inputs are a fresh trajectory batch), an SM left
+free for the collective, and CUDA-graph capture of a sequence of steps.  The
+functions below it are backend-agnostic (NCCL on GPUs, gloo in the CPU tests).
 """
 from __future__ import annotations
+
+from typing import Callable, Sequence
 
 import torch
 
 
-def shard_columns(B: int, world: int, rank: int) -> tuple[int, int]:
-    """Column block [b0, b1) of rank `rank`: equal blocks, the first B % world
-    ranks get one extra column."""
+def shard_columns(B: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:
+    """Column block [b0, b1) of rank `rank`: equal blocks of whole `align`-column units
+    (the first ranks get one extra unit when they do not divide evenly).  align = 8
+    keeps every shard on the column-block kernel's 16-byte TMA segments."""
     if not 0 <= rank < world:
         raise ValueError("rank out of range")
-    base, extra = divmod(B, world)
-    b0 = rank * base + min(rank, extra)
-    return b0, b0 + base + (1 if rank < extra else 0)
+    if align < 1 or B % align:
+        raise ValueError("B must be a multiple of align")
+    units = B // align
+    base, extra = divmod(units, world)
+    u0 = rank * base + min(rank, extra)
+    return u0 * align, (u0 + base + (1 if rank < extra else 0)) * align
 
 
 def allreduce_partials(partials: torch.Tensor, group=None, async_op: bool = False):
@@ -34,7 +49,7 @@ def allreduce_partials(partials: torch.Tensor, group=None, async_op: bool = Fals
 
 
 def max_over_ranks(x: float, device="cpu", group=None) -> float:
-    """Max of a host float over ranks (used for the slowest rank's time)."""
+    """Max of a host float over ranks (the slowest rank's time)."""
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return float(x)
@@ -61,3 +76,100 @@ def allreduce_grads(grads: torch.Tensor, group=None, async_op: bool = False):
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return None
     return dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+
+
+def _world(group=None) -> tuple[int, int]:
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+class LearnerStep:
+    """One learner's step on its trajectory shard: the fused kernel, then the
+    partials all-reduce (row a13) overlapped with the next step.
+
+    ``kernel`` computes one shard: ``kernel(inputs, out, **kw)`` with the seven
+    input tensors in ``inputs`` and the outputs (grad_target_logits, grad_values,
+    partials) in ``out``; the default is :func:`vtrace.loss_and_grad` on the GPU
+    (the CPU tests pass the oracle).  On a CUDA device the kernel runs on
+    ``self.stream`` and the collective on ``self.comm_stream``; call :meth:`join`
+    (or synchronise) before reading a reduced ``partials``.
+
+    overlap:      launch each step's kernel as a programmatic dependent of the
+                  previous one (its prologue overlaps the previous step's tail;
+                  valid because every step reads a fresh batch, never the
+                  previous step's outputs).
+    reserve_sms:  SMs the kernel leaves free at N > 1 so that step k's collective
+                  is not queued behind step k+1's CTAs (default 1).
+    """
+
+    def __init__(self, T: int, B: int, A: int, logits_dtype, *, device=None, group=None,
+                 overlap: bool = True, reserve_sms: int | None = None,
+                 kernel: Callable | None = None, **method_kw):
+        self.T, self.B, self.A = int(T), int(B), int(A)
+        self.group = group
+        self.world, self.rank = _world(group)
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        self.cuda = self.device.type == "cuda"
+        self.kw = dict(method_kw)
+        if kernel is None:
+            from . import vtrace
+            code = logits_dtype if isinstance(logits_dtype, int) else {
+                torch.float32: vtrace.VT_FLOAT32, torch.bfloat16: vtrace.VT_BFLOAT16}[logits_dtype]
+            self.workspace = vtrace.Workspace(T, B, A, code, self.device)
+            self._kernel = vtrace.loss_and_grad
+            reserve = (1 if self.world > 1 else 0) if reserve_sms is None else int(reserve_sms)
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            self.kw.update(workspace=self.workspace, overlap_previous=bool(overlap),
+                           sm_budget=(sms - reserve) if reserve > 0 else 0)
+        else:
+            self.workspace = None
+            self._kernel = kernel
+        if self.cuda:
+            self.stream = torch.cuda.Stream(self.device)
+            self.comm_stream = torch.cuda.Stream(self.device)
+        else:
+            self.stream = self.comm_stream = None
+
+    def _launch(self, inputs: dict, out: dict):
+        from .vtrace import INPUT_NAMES
+        self._kernel(*[inputs[k] for k in INPUT_NAMES], out=out, **self.kw)
+
+    def __call__(self, inputs: dict, out: dict):
+        """Enqueue one step: the shard's kernel, then (N > 1) the SUM all-reduce of
+        out['partials'] over the group."""
+        if not self.cuda:
+            self._launch(inputs, out)
+            allreduce_partials(out["partials"], self.group)
+            return
+        with torch.cuda.stream(self.stream):
+            self._launch(inputs, out)
+        if self.world > 1:
+            self.comm_stream.wait_stream(self.stream)
+            with torch.cuda.stream(self.comm_stream):
+                allreduce_partials(out["partials"], self.group)
+
+    def join(self):
+        """The main stream waits for the outstanding collectives."""
+        if self.cuda and self.world > 1:
+            self.stream.wait_stream(self.comm_stream)
+
+    def run(self, batches: Sequence[tuple[dict, dict]]):
+        """Enqueue the steps over (inputs, out) pairs, then join."""
+        for inputs, out in batches:
+            self(inputs, out)
+        self.join()
+
+    def capture(self, batches: Sequence[tuple[dict, dict]]) -> "torch.cuda.CUDAGraph":
+        """A CUDA graph of the step sequence (kernels, cross-stream events and the
+        NCCL collectives), joined at the end; replay with ``g.replay()`` on any
+        stream (it runs in the graph's own stream order)."""
+        if not self.cuda:
+            raise RuntimeError("graph capture needs a CUDA device")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self.run(batches)
+        return g

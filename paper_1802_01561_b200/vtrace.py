@@ -50,7 +50,12 @@ class _Params(ctypes.Structure):
                 ("clip_pg_rho_threshold", ctypes.c_float), ("lambda_", ctypes.c_float),
                 ("reward_mode", ctypes.c_int32), ("correction", ctypes.c_int32),
                 ("epsilon", ctypes.c_float), ("q_from_values", ctypes.c_int32),
-                ("behaviour_log_probs", ctypes.c_int32), ("overlap_previous", ctypes.c_int32)]
+                ("behaviour_log_probs", ctypes.c_int32), ("overlap_previous", ctypes.c_int32),
+                ("kernel", ctypes.c_int32), ("sm_budget", ctypes.c_int32)]
+
+
+# vt_kernel: which kernel runs a call (0 = automatic; tests / A-B only)
+KERNEL_AUTO, KERNEL_COLUMN_BLOCK, KERNEL_LOOKBACK = 0, 1, 2
 
 
 # vt_correction: Section 5.2.2 off-policy correction variants
@@ -149,11 +154,12 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 def params(rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0, reward_mode=0,
            correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
-           behaviour_log_probs=0, overlap_previous=0) -> _Params:
+           behaviour_log_probs=0, overlap_previous=0, kernel=KERNEL_AUTO,
+           sm_budget=0) -> _Params:
     return _Params(float(rho_bar), float(c_bar),
                    float(rho_bar if pg_rho_bar is None else pg_rho_bar), float(lambda_),
                    int(reward_mode), int(correction), float(epsilon), int(q_from_values),
-                   int(behaviour_log_probs), int(overlap_previous))
+                   int(behaviour_log_probs), int(overlap_previous), int(kernel), int(sm_budget))
 
 
 def workspace_bytes(T: int, B: int, A: int, dtype_code: int) -> int:
@@ -180,23 +186,53 @@ class Workspace:
         return _ptr(self.tensor)
 
 
-def _shapes(behaviour_logits, target_logits, actions):
-    """(T, B, A, mu_lp): the behaviour input is either mu's [T, B, A] logits or, in
-    behaviour-log-prob mode, log mu(a_t) as a [T, B] float32 tensor."""
+def _shapes(behaviour_logits, target_logits, actions, discounts, rewards, values,
+            bootstrap_value):
+    """(T, B, A, mu_lp) after checking every input's shape, dtype, layout and device
+    (the kernels trust these; a wrong dtype or an undersized buffer would be misread).
+    The behaviour input is either mu's [T, B, A] logits (the target logits' dtype) or,
+    in behaviour-log-prob mode, log mu(a_t) as a [T, B] float32 tensor."""
     if target_logits.dim() != 3:
         raise ValueError("target logits must be [T, B, A]")
     T, B, A = target_logits.shape
+    _dtype_code(target_logits)
     if behaviour_logits.dim() == 2:
         if behaviour_logits.shape != (T, B) or behaviour_logits.dtype != torch.float32:
             raise ValueError("behaviour log-probs must be a [T, B] float32 tensor")
         mu_lp = 1
     elif behaviour_logits.shape != target_logits.shape:
         raise ValueError("behaviour and target logits must have equal [T, B, A] shapes")
+    elif behaviour_logits.dtype != target_logits.dtype:
+        raise ValueError("behaviour and target logits must have the same dtype")
     else:
         mu_lp = 0
-    if actions.shape != (T, B):
-        raise ValueError("actions must be [T, B]")
+    if actions.shape != (T, B) or actions.dtype != torch.int32:
+        raise ValueError("actions must be a [T, B] int32 tensor")
+    for name, t in (("discounts", discounts), ("rewards", rewards), ("values", values)):
+        if t.shape != (T, B) or t.dtype != torch.float32:
+            raise ValueError(f"{name} must be a [T, B] float32 tensor")
+    if bootstrap_value.shape != (B,) or bootstrap_value.dtype != torch.float32:
+        raise ValueError("bootstrap_value must be a [B] float32 tensor")
+    _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
+    dev = target_logits.device
+    for t in (behaviour_logits, actions, discounts, rewards, values, bootstrap_value):
+        if t.device != dev:
+            raise ValueError("all inputs must be on the same device")
     return T, B, A, mu_lp
+
+
+def _check_out(out: dict, specs: dict, dev):
+    """Caller-supplied outputs: present where required, right dtype, shape, layout, device."""
+    for k, (shape, dtype, required) in specs.items():
+        t = out.get(k)
+        if t is None:
+            if required:
+                raise ValueError(f"out[{k!r}] is required")
+            continue
+        if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_contiguous() or \
+                t.device != dev:
+            raise ValueError(f"out[{k!r}] must be a contiguous {dtype} tensor of shape "
+                             f"{tuple(shape)} on {dev}")
 
 
 def _contig(*ts):
@@ -211,22 +247,27 @@ def from_logits(behaviour_logits, target_logits, actions, discounts, rewards, va
                 bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
                 reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
                 overlap_previous=False, workspace: Workspace | None = None, with_log_probs=True,
-                out: dict | None = None):
+                out: dict | None = None, kernel=KERNEL_AUTO, sm_budget=0):
     """vtrace_from_logits.  Returns dict of fp32 [T, B] tensors: vs,
     pg_advantages (+ log_rhos, target_action_log_probs, behaviour_action_log_probs)."""
     lib = load_library()
-    T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions)
+    T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions, discounts, rewards, values,
+                             bootstrap_value)
     dt = _dtype_code(target_logits)
     dev = target_logits.device
-    _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
     ws = workspace if workspace is not None else Workspace(T, B, A, dt, dev)
     if out is None:
         out = {k: torch.empty(T, B, dtype=torch.float32, device=dev) for k in ("vs", "pg_advantages")}
         if with_log_probs:
             for k in ("log_rhos", "target_action_log_probs", "behaviour_action_log_probs"):
                 out[k] = torch.empty(T, B, dtype=torch.float32, device=dev)
+    else:
+        f = torch.float32
+        _check_out(out, {"vs": ((T, B), f, True), "pg_advantages": ((T, B), f, True),
+                         "log_rhos": ((T, B), f, False), "target_action_log_probs": ((T, B), f, False),
+                         "behaviour_action_log_probs": ((T, B), f, False)}, dev)
     p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
-               mu_lp, int(overlap_previous))
+               mu_lp, int(overlap_previous), kernel, sm_budget)
     st = lib.vtrace_from_logits(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
         _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), _ptr(out["vs"]),
@@ -241,15 +282,16 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
                   bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None, lambda_=1.0,
                   reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
                   baseline_cost=0.5, entropy_cost=0.01, overlap_previous=False,
-                  workspace: Workspace | None = None, with_targets=True, out: dict | None = None):
+                  workspace: Workspace | None = None, with_targets=True, out: dict | None = None,
+                  kernel=KERNEL_AUTO, sm_budget=0):
     """vtrace_loss_and_grad.  Returns dict: grad_target_logits [T,B,A] (logits
     dtype), grad_values [T,B] fp32, partials [8] fp64 (device), and, if
     with_targets, vs and pg_advantages [T,B] fp32."""
     lib = load_library()
-    T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions)
+    T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions, discounts, rewards, values,
+                             bootstrap_value)
     dt = _dtype_code(target_logits)
     dev = target_logits.device
-    _contig(behaviour_logits, target_logits, actions, discounts, rewards, values, bootstrap_value)
     ws = workspace if workspace is not None else Workspace(T, B, A, dt, dev)
     if out is None:
         out = {"grad_target_logits": torch.empty_like(target_logits),
@@ -258,8 +300,13 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
         if with_targets:
             out["vs"] = torch.empty(T, B, dtype=torch.float32, device=dev)
             out["pg_advantages"] = torch.empty(T, B, dtype=torch.float32, device=dev)
+    else:
+        f = torch.float32
+        _check_out(out, {"grad_target_logits": ((T, B, A), target_logits.dtype, True),
+                         "grad_values": ((T, B), f, True), "partials": ((P_COUNT,), torch.float64, True),
+                         "vs": ((T, B), f, False), "pg_advantages": ((T, B), f, False)}, dev)
     p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
-               mu_lp, int(overlap_previous))
+               mu_lp, int(overlap_previous), kernel, sm_budget)
     w = _Weights(float(baseline_cost), float(entropy_cost))
     st = lib.vtrace_loss_and_grad(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
@@ -430,6 +477,11 @@ def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
     if global_norm_out is not None and not (global_norm_out.is_cuda and
                                             global_norm_out.dtype == torch.float64):
         raise ValueError("global_norm_out must be a float64 CUDA tensor")
+    if learner_flags is not None and workspace is None:
+        # the in-kernel learner sync counts calls in the workspace: a fresh one per call
+        # would restart the count and let learners read peers' buffers early
+        raise ValueError("learner_flags needs a persistent RmspropWorkspace (one per learner, "
+                         "reused every step)")
     ws = workspace if workspace is not None else RmspropWorkspace(n, params.device)
     key = (float(learning_rate), float(decay), float(epsilon), float(max_global_norm))
     prm = _RMS_PRM_CACHE.get(key)
@@ -476,13 +528,26 @@ def output_layer(hidden: torch.Tensor, w_t: torch.Tensor, bias: torch.Tensor | N
     for d in lead:
         M *= int(d)
     _contig(hidden, w_t)
-    if bias is not None:
-        bias = bias.to(device=hidden.device, dtype=torch.float32).contiguous()
     dev = hidden.device
+    if w_t.device != dev:
+        raise ValueError("output_layer: hidden and w_t must be on the same device")
+    if bias is not None:
+        if bias.numel() != A + 1:
+            raise ValueError(f"output_layer: bias must have A + 1 = {A + 1} elements "
+                             "(policy logits then the baseline)")
+        bias = bias.to(device=dev, dtype=torch.float32).contiguous()
     if logits_out is None:
         logits_out = torch.empty(lead + (A,), dtype=torch.float32, device=dev)
+    elif not (logits_out.dtype == torch.float32 and logits_out.is_contiguous() and
+              logits_out.numel() == M * A and logits_out.device == dev):
+        raise ValueError("output_layer: logits_out must be a contiguous fp32 tensor of M * A "
+                         "elements on hidden's device")
     if values_out is None:
         values_out = torch.empty(lead, dtype=torch.float32, device=dev)
+    elif not (values_out.dtype == torch.float32 and values_out.is_contiguous() and
+              values_out.numel() == M and values_out.device == dev):
+        raise ValueError("output_layer: values_out must be a contiguous fp32 tensor of M "
+                         "elements on hidden's device")
     st = load_library().vtrace_output_layer(M, H, A, _ptr(hidden), _ptr(w_t), _ptr(bias),
                                             _ptr(logits_out), _ptr(values_out), _stream(dev))
     _check(st, "vtrace_output_layer")

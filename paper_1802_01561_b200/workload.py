@@ -98,13 +98,16 @@ def toy_inputs() -> dict:
 
 
 def make_inputs(config, seed: int | None = None, B: int | None = None, T: int | None = None,
-                A: int | None = None, dtype: int | None = None) -> dict:
+                A: int | None = None, dtype: int | None = None, spread: float = 1.5,
+                lag: float = 0.3, p_done: float | None = None) -> dict:
     """Seeded synthetic batch for ``config`` (a name or a Config).
 
     Returns a dict of numpy arrays in the library's layout: logits [T,B,A]
     (float32, or uint16 bf16 bits), actions int32 [T,B], rewards / values /
     discounts float32 [T,B], bootstrap_value float32 [B]; plus T, B, A, dtype,
-    reward_mode.  Shape overrides keep the config's distributions."""
+    reward_mode.  Shape overrides keep the config's distributions; ``spread`` / ``lag``
+    (std of z_pi and of z_mu - z_pi) and ``p_done`` override them for stress tests
+    (p_done = 0: no episode end at all)."""
     cfg = CONFIGS[config] if isinstance(config, str) else config
     T = cfg.T if T is None else T
     B = cfg.B if B is None else B
@@ -112,8 +115,8 @@ def make_inputs(config, seed: int | None = None, B: int | None = None, T: int | 
     dtype = cfg.dtype if dtype is None else dtype
     seed = cfg.seed if seed is None else seed
     g = torch.Generator().manual_seed(int(seed))
-    zp = torch.randn(T, B, A, generator=g) * 1.5
-    zm = zp + torch.randn(T, B, A, generator=g) * 0.3
+    zp = torch.randn(T, B, A, generator=g) * spread
+    zm = zp + torch.randn(T, B, A, generator=g) * lag
     if dtype == DTYPE_BF16:
         zp_s = f32_to_bf16_bits(zp.numpy())
         zm_s = f32_to_bf16_bits(zm.numpy())
@@ -132,8 +135,9 @@ def make_inputs(config, seed: int | None = None, B: int | None = None, T: int | 
     rew = torch.where(ur >= 0.90, torch.full_like(rew, 1.0), rew)
     rew = torch.where(ur >= 0.96, torch.full_like(rew, 10.0), rew)
     rew = torch.where(ur >= 0.98, torch.full_like(rew, -1.0), rew)
-    done = torch.rand(T, B, generator=g) < cfg.p_done
-    if cfg.p_done > 0 and not bool(done.any()):
+    pd = cfg.p_done if p_done is None else p_done
+    done = torch.rand(T, B, generator=g) < pd
+    if pd > 0 and not bool(done.any()):
         done[T // 2, 0] = True     # at least one episode end in the batch
     disc = torch.where(done, torch.zeros(T, B), torch.full((T, B), GAMMA))
     return dict(T=T, B=B, A=A, dtype=dtype, reward_mode=cfg.reward_mode,

@@ -119,19 +119,28 @@ def test_binding_has_no_cpu_fallback(lib):
 
 
 def test_kernel_choice(lib):
-    """Host-only query of the kernel a shape takes: wide batches (>= 1024 tasks of 4
-    trajectories) or short unrolls (<= 4 chunks of 8 steps) the column-task kernel,
-    else the look-back kernel (TMA when the pitches are 16-byte multiples)."""
-    wide = ("vtrace_ct_kernel", "vtrace_ctb_kernel")  # ctb needs a device's SM count
-    assert vt.kernel_for(100, 8192, 18, 1) in wide                        # large
-    assert vt.kernel_for(100, 4096, 18, 1) in wide
-    assert vt.kernel_for(100, 4092, 18, 1) == "vtrace_fused_kernel"       # 1023 tasks
-    assert vt.kernel_for(2000, 1024, 9, 0) == "vtrace_fused_kernel"       # stress
-    assert vt.kernel_for(20, 32, 18, 0) == "vtrace_ct_kernel"             # atari: short T
-    assert vt.kernel_for(33, 32, 18, 0) == "vtrace_fused_kernel"          # 5 chunks
+    """Host-only query of the kernel a shape takes: the column-block kernel wherever its
+    TMA boxes apply (16-byte segments of 4 or 8 trajectories, an instantiated A), else
+    the look-back kernel (TMA when the pitches are 16-byte multiples, else plain loads)."""
+    cb = "vtrace_cb_kernel"
+    assert vt.kernel_for(100, 8192, 18, 1) == cb                          # large
+    assert vt.kernel_for(100, 4096, 18, 1) == cb                          # its N=2 shard
+    assert vt.kernel_for(100, 1024, 18, 1) == cb                          # its N=8 shard
+    assert vt.kernel_for(2000, 1024, 9, 0) == cb                          # stress
+    assert vt.kernel_for(20, 32, 18, 0) == cb                             # atari
+    assert vt.kernel_for(100, 32, 9, 1) == cb                             # dmlab (8-column segments)
+    assert vt.kernel_for(100, 4096, 24, 1) == "vtrace_fused_kernel"       # A not instantiated
+    assert vt.kernel_for(100, 4092, 9, 1) == "vtrace_fused_kernel (plain loads)"  # pitch % 16
+    assert vt.kernel_for(100, 4096, 40, 1) == "vtrace_fused_kernel (plain loads)"  # 8 A > 256
     assert vt.kernel_for(5, 2, 3, 0) == "vtrace_fused_kernel (plain loads)"  # toy: pitch 24 B
     assert vt.kernel_for(0, 8, 3, 0).startswith("none")
     assert vt.kernel_for(5, 8, 3, 7).startswith("none")
+
+
+def test_kernel_and_sm_budget_param_checks(lib):
+    assert _call_loss(lib, params=vt.params(kernel=3)) == 4
+    assert _call_loss(lib, params=vt.params(kernel=-1)) == 4
+    assert _call_loss(lib, params=vt.params(sm_budget=-2)) == 4
 
 
 def test_behaviour_log_prob_param_check(lib):

@@ -126,3 +126,78 @@ def test_gradient_allreduce_gives_identical_replicas():
     np.testing.assert_allclose(g0, total, rtol=1e-15)
     np.testing.assert_allclose(t0, theta, rtol=1e-14)
     assert n0 == pytest.approx(norm, rel=1e-14)
+
+
+def _oracle_kernel(*args, out, **kw):
+    """LearnerStep's per-shard compute, on the CPU: the fp64 oracle on the shard's
+    tensors (test infrastructure standing in for the CUDA kernel)."""
+    import oracle
+    from paper_1802_01561_b200 import vtrace as vt
+    inp = {k: a.numpy() for k, a in zip(vt.INPUT_NAMES, args)}
+    T, B, A = inp["target_logits"].shape
+    inp.update(T=T, B=B, A=A, dtype=0)
+    r = oracle.loss_and_grad(inp, **kw)
+    out["partials"].copy_(torch.from_numpy(r["partials"]))
+    out["grad_values"].copy_(torch.from_numpy(r["grad_values"]))
+    out["grad_target_logits"].copy_(torch.from_numpy(r["grad_target_logits"]))
+
+
+def _step_worker(rank, world, port, name, B, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1802_01561_b200 import vtrace as vt
+        from paper_1802_01561_b200 import workload as wl
+        full = wl.make_inputs(name, B=B, dtype=wl.DTYPE_F32)
+        b0, b1 = learner.shard_columns(B, world, rank, align=4)
+        sh = wl.column_slice(full, b0, b1)
+        step = learner.LearnerStep(sh["T"], sh["B"], sh["A"], torch.float32, device="cpu",
+                                   kernel=_oracle_kernel, reward_mode=sh["reward_mode"])
+        assert step.world == world and step.rank == rank
+        x = {k: torch.from_numpy(np.ascontiguousarray(sh[k])) for k in vt.INPUT_NAMES}
+        out = {"grad_target_logits": torch.zeros(sh["T"], sh["B"], sh["A"], dtype=torch.float64),
+               "grad_values": torch.zeros(sh["T"], sh["B"], dtype=torch.float64),
+               "partials": torch.zeros(8, dtype=torch.float64)}
+        step.run([(x, out)])
+        q.put((rank, out["partials"].numpy().copy(), out["grad_values"].numpy().copy(), (b0, b1)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_learner_step_strong_scaling(world):
+    """LearnerStep (the product's multi-learner step) at world sizes 2 and 8 over gloo:
+    the global batch B = 64 column-sharded in 4-column units (strong scaling, the
+    BASELINE multi-GPU config), each rank's kernel (here the oracle) on its shard, the
+    partials SUM-all-reduced: every rank holds the whole batch's partials and
+    its shard's gradient is the matching slice of the whole batch's."""
+    import oracle
+    from paper_1802_01561_b200 import workload as wl
+    B = 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, "atari", B, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = wl.make_inputs("atari", B=B, dtype=wl.DTYPE_F32)
+    ref = oracle.loss_and_grad(full, reward_mode=full["reward_mode"])
+    assert [r[3] for r in res] == [learner.shard_columns(B, world, r, 4) for r in range(world)]
+    assert res[0][3][0] == 0 and res[-1][3][1] == B
+    for rank, parts, gv, (b0, b1) in res:
+        np.testing.assert_allclose(parts, ref["partials"], rtol=1e-12)
+        np.testing.assert_array_equal(gv, ref["grad_values"][:, b0:b1])
+
+
+def test_shard_columns_align():
+    assert learner.shard_columns(8192, 8, 3, align=8) == (3072, 4096)
+    assert learner.shard_columns(40, 3, 0, align=8) == (0, 16)
+    assert learner.shard_columns(40, 3, 2, align=8) == (32, 40)
+    with pytest.raises(ValueError):
+        learner.shard_columns(30, 2, 0, align=8)

@@ -74,10 +74,35 @@ def test_toy_fixture_matches_survey():
     np.testing.assert_allclose(P[3], gp["total_loss"], rtol=1e-6)
     np.testing.assert_allclose(P[4], gp["sumsq_dlogits"], rtol=1e-6)
     np.testing.assert_allclose(P[5], gp["sumsq_dvalues"], rtol=1e-6)
+    # the rho diagnostics (readings r2, r6): counting ratios >= rho_bar
+    # instead of > rho_bar gives 9, not 7 (log rho = 0 exactly at two steps)
+    np.testing.assert_allclose(P[6], gp["sum_rho"], rtol=1e-9)
+    assert P[7] == gp["n_rho_clipped"]
     np.testing.assert_allclose(lg["grad_target_logits"][0, 0], g["grad_target_logits"]["t0_b0"],
                                rtol=1e-6, atol=1e-8)
     np.testing.assert_allclose(lg["grad_target_logits"][4, 1], g["grad_target_logits"]["t4_b1"],
                                rtol=1e-6, atol=1e-8)
+
+
+def test_rho_diagnostics_chosen_ratios():
+    """Partials 6-7 (Sum rho, #clipped; P:196 rho_t = min(rho_bar, pi/mu), readings
+    r2/r6) on rows whose ratio pi/mu at the taken action is chosen: A=2, mu uniform,
+    pi = (q/2, 1 - q/2).  With c_bar < rho_bar and lambda = 1/2, a sum of
+    c = lambda min(c_bar, q) (2.35) instead of rho (5.9), or clipping at c_bar
+    (4 clipped, not 2), give different numbers.  The strict '>' of the count is
+    pinned by the toy fixture (log rho = 0 exactly at two steps)."""
+    ratios = [0.25, 0.5, 0.9, 1.1, 1.5, 1.75, 0.75]
+    rho_bar, c_bar = 1.2, 0.8
+    zp, zm = _logits_for_ratios(ratios)
+    n = len(ratios)
+    inp = dict(T=n, B=1, A=2, dtype=0, target_logits=zp, behaviour_logits=zm,
+               actions=np.zeros((n, 1), np.int32), rewards=np.ones((n, 1), np.float32),
+               values=np.zeros((n, 1), np.float32), bootstrap_value=np.zeros(1, np.float32),
+               discounts=np.full((n, 1), 0.5, np.float32))
+    P = oracle.loss_and_grad(inp, rho_bar=rho_bar, c_bar=c_bar, lambda_=0.5)["partials"]
+    # the ratios pass through fp32 logits (log(q/2) rounded): compare at 1e-6
+    np.testing.assert_allclose(P[6], 0.25 + 0.5 + 0.9 + 1.1 + 1.2 + 1.2 + 0.75, rtol=1e-6)
+    assert P[7] == 2  # 1.5 and 1.75 exceed rho_bar = 1.2
 
 
 def test_toy_column0_by_hand():
