@@ -24,6 +24,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstddef>
 
 #include "vtrace.h"
 #include "vtrace_kernels.cuh"
@@ -35,12 +36,17 @@ constexpr int RMS_MAX_CTAS = 1024;
 constexpr size_t RMS_RECS_OFF = 256;
 constexpr int RMS_MAX_GRADS = 8;  // gradients summed in the kernel (learners' buffers)
 
-struct RmsHeader {  // workspace bytes [0, 8); vtrace_workspace_init zeroes it
+struct RmsHeader {  // workspace bytes [0, 16); vtrace_workspace_init zeroes them
   unsigned int epoch;   // calls completed (tags this call's records with epoch + 1)
   unsigned int ticket;  // CTAs done with phase 1 (the last one bumps the epoch)
   unsigned int done_ticket;  // CTAs done reading (learner sync: the last one signals)
   unsigned int go;           // learner sync: every learner ready for epoch go - 1 (CTA 0)
 };
+// vtrace_workspace_init zeroes the workspace and then sets the V-trace status word
+// (WsHeader::status, bytes [16, 24)) to ~0: the RMSProp header must stay below it, or
+// a field initialised to 0xFFFFFFFF would never match a ticket and the learners hang
+static_assert(sizeof(RmsHeader) <= offsetof(vtb200::WsHeader, status),
+              "RmsHeader overlaps the status word vtrace_workspace_init sets to ~0");
 
 struct RmsArgs {
   long long n;

@@ -86,6 +86,23 @@ __device__ __forceinline__ void mbar_wait32(uint32_t addr, uint32_t phase) {
       : "memory");
 }
 
+// the producer's wait for the compute warps: test, then back off (its issue slots belong
+// to the compute warps of its sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep32(uint32_t addr, uint32_t phase) {
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive32(uint32_t addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
@@ -127,6 +144,30 @@ __device__ __forceinline__ void tma_store_2d32(const CUtensorMap* map, int x, in
                    reinterpret_cast<uint64_t>(map)),
                "r"(x), "r"(y), "r"(src)
                : "memory");
+}
+
+// One level of the suffix scan of affine maps over the warp's 8 steps: compose this
+// lane's (G, D) with the map `o` lanes further down, (G, D) o (Go, Do) = (G Go, D + G Do);
+// lanes whose partner is past the warp (steps beyond the 8) keep theirs (identity).
+// The shuffle's in-range predicate guards the two fp64 ops: no selects, no branch.
+__device__ __forceinline__ void scan_level(double& G, double& D, int o) {
+  asm("{\n"
+      ".reg .pred p;\n"
+      ".reg .b32 g0, g1, d0, d1;\n"
+      ".reg .f64 go, dd;\n"
+      "mov.b64 {g0, g1}, %0;\n"
+      "mov.b64 {d0, d1}, %1;\n"
+      "shfl.sync.down.b32 g0|p, g0, %2, 31, -1;\n"
+      "shfl.sync.down.b32 g1, g1, %2, 31, -1;\n"
+      "shfl.sync.down.b32 d0, d0, %2, 31, -1;\n"
+      "shfl.sync.down.b32 d1, d1, %2, 31, -1;\n"
+      "mov.b64 go, {g0, g1};\n"
+      "mov.b64 dd, {d0, d1};\n"
+      "@p fma.rn.f64 %1, %0, dd, %1;\n"
+      "@p mul.rn.f64 %0, %0, go;\n"
+      "}\n"
+      : "+d"(G), "+d"(D)
+      : "r"(o));
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -401,7 +442,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int j = 0; j < C.J; ++j) {
-        mbar_wait32(done0 + 8u * s, ph);
+        mbar_wait_sleep32(done0 + 8u * s, ph);
         // (programmatic dependent launch: the first global write waits for the
         // previous kernel on the stream)
         if (P.pdl && j == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -430,7 +471,9 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
           ph ^= 1u;
         }
       }
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      // the last stores must have read their stage before the CTA's shared memory goes
+      // away (their global writes complete with the grid)
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
   } else {
     // ---------------- compute warp (cg, ts) ----------------
@@ -508,13 +551,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       double Gi = row_ok ? (double)gm * sw.c : 1.0;  // gamma_t c_t
       double Di = row_ok ? sw.rho * td : 0.0;        // delta_t V
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        const double Go = shfl_down_d(Gi, o), Do = shfl_down_d(Di, o);
-        if (lane + o < 32) {  // beyond the warp's steps: identity
-          Di = fma(Gi, Do, Di);
-          Gi = Gi * Go;
-        }
-      }
+      for (int o = 4; o < 32; o <<= 1) scan_level(Gi, Di, o);
       if (C.nts > 1 && tl == 0) {  // the warp's 8-step aggregate for the column group
         agg[j & 1][warp][c][0] = Gi;
         agg[j & 1][warp][c][1] = Di;
@@ -553,11 +590,13 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       }
       if (row_ok) {
         acc.rho += sw.rho;  // the rho_t in delta_t (reading r6)
-        acc.clip += ((!GEN || P.correction == VT_CORRECTION_VTRACE) && ratio > P.rho_bar) ? 1u : 0u;
+        if ((!GEN || P.correction == VT_CORRECTION_VTRACE) && ratio > P.rho_bar) ++acc.clip;
         if constexpr (LOSS) acc.H += (double)(lse - cshift);
       }
-      bool bad = (a_raw != a) || !R.finite || !isfinite(rt) || !isfinite(Vt) || !isfinite(Vn) ||
-                 !(gm >= 0.f && gm <= 1.f);
+      // data checks (reading r3): one NaN probe for r, V and V' (x * 0 is NaN for +-inf and
+      // NaN), a range test for gamma, the action clamp, the row statistics' finiteness
+      const float probe = fmaf(rt, 0.f, fmaf(Vt, 0.f, Vn * 0.f));
+      bool bad = (a_raw != a) || !R.finite || (probe != 0.f) || !(gm >= 0.f && gm <= 1.f);
       if constexpr (MULP) bad = bad || !isfinite(lmu);
       if (row_ok && bad) {
         if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");

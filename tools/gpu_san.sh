@@ -1,6 +1,9 @@
 #!/bin/bash
+# One compute-sanitizer tool per call (B200_PROFILING.md): TOOL=memcheck|racecheck|synccheck
+# (under gpurun, after tools/san_target.py exited 0 without the sanitizer).
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
-timeout 300 compute-sanitizer --tool memcheck --show-backtrace device --print-limit 5 python tools/repro_small.py dmlab loss 64 > gpurun_out/san_dmlab_loss.txt 2>&1
-timeout 120 python tools/repro_small.py dmlab from 64 > gpurun_out/san_dmlab_from_plain.txt 2>&1
-timeout 120 python tools/repro_small.py large loss 64 > gpurun_out/san_large_loss_plain.txt 2>&1
+T=${TOOL:-memcheck}
+timeout 200 python tools/san_target.py > gpurun_out/san_plain.txt 2>&1 && \
+timeout 1500 compute-sanitizer --tool $T --print-limit 20 python tools/san_target.py > gpurun_out/san_$T.txt 2>&1
+echo "rc=$?" >> gpurun_out/san_$T.txt
