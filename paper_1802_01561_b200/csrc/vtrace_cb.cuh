@@ -204,8 +204,10 @@ __device__ __forceinline__ void cb_load_pairs(const LT* row, float2 (&z)[(A_CT +
     if constexpr (A_CT % 2 == 0) {  // rows start 4-byte aligned
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
+        // exact bf16 -> fp32 on the ALU pipe (PRMT, LOP3): the FMA pipe carries the math
         const uint32_t x = reinterpret_cast<const uint32_t*>(row)[k];
-        z[k] = make_float2(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u));
+        z[k] = make_float2(__uint_as_float(__byte_perm(x, 0u, 0x1044)),
+                           __uint_as_float(x & 0xffff0000u));
       }
     } else {
       const unsigned short* h = reinterpret_cast<const unsigned short*>(row);
@@ -502,12 +504,18 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     const bool one_bar = !GEN && P.rho_bar == P.c_bar && P.rho_bar == P.pg_rho_bar && P.lambda == 1.0;
     double carry = 0.0;  // A = v - V just after the next iteration to finish (A_T = 0)
     CbAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0u};
+    // loop-invariant switches, kept in predicates (not re-read from parameter space)
+    const bool want_vs = (C.out_mask & OUT_VS) != 0, want_pg = (C.out_mask & OUT_PG) != 0;
+    const bool want_lr = (C.out_mask & OUT_LR) != 0, want_lp = (C.out_mask & OUT_LP) != 0;
+    const bool want_lm = (C.out_mask & OUT_LM) != 0;
+    const int tdec = C.Ts;  // X(j) rows: t = t_first - j * Ts
+    const int t_first = (C.J - 1) * C.Ts + 8 * ts + tl;
     int sx = 0, sy = 0;         // stages of the next X and the next Y
     uint32_t phx = 0;           // parity of full[sx]'s next completion
 
     // ---- X(j): a1-a7 and the local scan of this lane's row (no carry) ------------
     auto X = [&](const int j, CbSt<A_CT>& S) {
-      const int t = (C.J - 1 - j) * C.Ts + 8 * ts + tl;
+      const int t = t_first - j * tdec;
       const bool row_ok = col_ok && (t < T);
       unsigned char* sb = smem + (size_t)sx * C.stage;
       mbar_wait32(full0 + 8u * sx, phx);
@@ -515,7 +523,8 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       const float rt = lds<float>(sb + C.r + soff);
       const float gm = lds<float>(sb + C.gm + soff);
       const float Vt = lds<float>(sb + C.v + soff);
-      const float Vn = (t + 1 < T) ? lds<float>(sb + C.v + voff) : boot;  // V(x_T) = bootstrap
+      const float Vnt = lds<float>(sb + C.v + voff);  // (row T of the tile: zero-filled)
+      const float Vn = (t + 1 < T) ? Vnt : boot;        // V(x_T) = bootstrap
       const int a = min(max(a_raw, 0), A - 1);
       const LT* zrow = reinterpret_cast<const LT*>(sb + C.pi + zoff);
       const LT* mrow = reinterpret_cast<const LT*>(sb + C.mu + zoff);
@@ -583,9 +592,9 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       S.row_ok = row_ok;
       if constexpr (!LOSS) {  // carry-free outputs of vtrace_from_logits
         if (row_ok) {
-          if (C.out_mask & OUT_LR) *reinterpret_cast<float*>(sb + C.lr + soff) = (float)log(ratio);
-          if (C.out_mask & OUT_LP) *reinterpret_cast<float*>(sb + C.lp + soff) = (float)(xa_p - log(R.S_p));
-          if (C.out_mask & OUT_LM) *reinterpret_cast<float*>(sb + C.lm + soff) = (float)(xa_m - log(R.S_m));
+          if (want_lr) *reinterpret_cast<float*>(sb + C.lr + soff) = (float)log(ratio);
+          if (want_lp) *reinterpret_cast<float*>(sb + C.lp + soff) = (float)(xa_p - log(R.S_p));
+          if (want_lm) *reinterpret_cast<float*>(sb + C.lm + soff) = (float)(xa_m - log(R.S_m));
         }
       }
       if (row_ok) {
@@ -608,10 +617,8 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
         if (!(gm >= 0.f && gm <= 1.f)) record_bad(P.ws, row, VT_DATA_DISCOUNT);
         if (!isfinite(Vn) && t + 1 == T) record_bad(P.ws, (long long)T * B + b, VT_DATA_VALUE);
       }
-      if (++sx == C.nstage) {
-        sx = 0;
-        phx ^= 1u;
-      }
+      sx = (sx + 1 == C.nstage) ? 0 : sx + 1;
+      phx ^= (sx == 0) ? 1u : 0u;
     };
 
     // ---- Y(j): the carry, a9-a11, release of the stage ------------------------------
@@ -641,8 +648,8 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       // (q_s = r_s + gamma V(x_{s+1}) instead with q_values: App. E.3)
       const double pgd = S.rho_pg * ((GEN && P.q_values) ? S.td : fma((double)S.gm, A_n, S.td));
       const float pgr = (float)pgd;
-      if (C.out_mask & OUT_VS) *reinterpret_cast<float*>(sb + C.vs + soff) = (float)((double)S.Vt + A_t);
-      if (C.out_mask & OUT_PG) *reinterpret_cast<float*>(sb + C.pg + soff) = pgr;
+      if (want_vs) *reinterpret_cast<float*>(sb + C.vs + soff) = (float)((double)S.Vt + A_t);
+      if (want_pg) *reinterpret_cast<float*>(sb + C.pg + soff) = pgr;
       if constexpr (LOSS) {
         // epsilon-correction (readings c11, r7): the policy-gradient term uses
         // log(pi_a + eps); its logit gradient is the plain one times pi_a / (pi_a + eps)
@@ -718,7 +725,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive32(done0 + 8u * sy);
-      if (++sy == C.nstage) sy = 0;
+      sy = (sy + 1 == C.nstage) ? 0 : sy + 1;
     };
 
     auto group_sync = [&]() {
@@ -802,30 +809,50 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
   prev = __shfl_sync(0xffffffffu, prev, 0);
   if (prev != (unsigned int)(S - 1)) return;
   if (lane == 0) *C.top_count = 0u;
-  // the last CTA: lane l adds CTAs l, l + 32, ... in order, then a fixed tree
+  // the last CTA: lane l adds CTAs l, l + 32, ... in order, then a fixed tree.  The
+  // records of 4 CTAs per lane are requested at once (one L2 round trip per 128 CTAs,
+  // not one per CTA); a record whose tag is not this call's yet is polled again.
   double tp[NPART];
 #pragma unroll
   for (int k = 0; k < NPART; ++k) tp[k] = 0.0;
-  for (int ci = lane; ci < S; ci += 32) {
-    double x[NPART];
-    if (ci == (int)blockIdx.x) {
+  constexpr int QB = 4;
+  for (int c0r = 0; c0r < S; c0r += 32 * QB) {
+    double x[QB][NPART];
+    unsigned long long tg[QB][NPART];
 #pragma unroll
-      for (int k = 0; k < NPART; ++k) x[k] = cs[k];
-    } else {
-      int spins = 0;
-      while (true) {  // (value, tag) records: no fence on either side
-        unsigned long long tg[NPART];
+    for (int q = 0; q < QB; ++q) {
+      const int ci = c0r + 32 * q + lane;
 #pragma unroll
-        for (int k = 0; k < NPART; ++k) ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[k], tg[k]);
-        bool ok = true;
-#pragma unroll
-        for (int k = 0; k < NPART; ++k) ok = ok && (tg[k] == tag);
-        if (ok) break;
-        if (++spins > 4) __nanosleep(32);
+      for (int k = 0; k < NPART; ++k) {
+        x[q][k] = 0.0;
+        tg[q][k] = tag;
+        if (ci < S && ci != (int)blockIdx.x)
+          ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[q][k], tg[q][k]);
       }
     }
 #pragma unroll
-    for (int k = 0; k < NPART; ++k) tp[k] += x[k];
+    for (int q = 0; q < QB; ++q) {
+      const int ci = c0r + 32 * q + lane;
+      if (ci == (int)blockIdx.x) {
+#pragma unroll
+        for (int k = 0; k < NPART; ++k) x[q][k] = cs[k];
+      }
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) ok = ok && (tg[q][k] == tag);
+      int spins = 0;
+      while (!ok) {  // (value, tag) records: no fence on either side
+        if (++spins > 4) __nanosleep(32);
+        ok = true;
+#pragma unroll
+        for (int k = 0; k < NPART; ++k) {
+          ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[q][k], tg[q][k]);
+          ok = ok && (tg[q][k] == tag);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NPART; ++k) tp[k] += x[q][k];
+    }
   }
 #pragma unroll
   for (int k = 0; k < NPART; ++k) {
