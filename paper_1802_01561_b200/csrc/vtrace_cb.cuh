@@ -30,8 +30,18 @@
 // 14 + 1 warps) and its strong-scaling shards (B = 4096: 28 columns, nts = 2; ...).
 #pragma once
 
+#include <cassert>
+
 #include "vtrace_kernels.cuh"
 #include "vtrace_rows.cuh"
+
+// -DVT_DEBUG_CHECKS: device-side bounds checks of every shared-memory tile index, stage
+// and record index (a build for small test runs; compute-sanitizer is closed on the pool)
+#ifdef VT_DEBUG_CHECKS
+#define VT_CHECK(c) assert(c)
+#else
+#define VT_CHECK(c) ((void)0)
+#endif
 
 namespace vtb200 {
 
@@ -499,6 +509,12 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     const float ce = (float)P.c_e, cv = (float)P.c_v;
     const uint32_t full0 = smem_u32(&full[0]), done0 = smem_u32(&done[0]);
     constexpr int NPc = CbRow<LT, A_CT>::NP;
+    // the lane's row inside each tile of a stage (logits tile [ncg/g][Ts][4gA], step
+    // tiles [Ts][Bc], V tile [Ts + 1][Bc], output tiles [Ts][Bc])
+    VT_CHECK(zoff + (unsigned)(A * sizeof(LT)) <= (unsigned)(C.Bc * A * sizeof(LT) * C.Ts));
+    VT_CHECK(C.pi + zoff + (unsigned)(A * sizeof(LT)) <= C.mu);
+    VT_CHECK(soff + 4u <= (unsigned)(C.Bc * 4 * C.Ts) && voff + 4u <= (unsigned)(C.Bc * 4 * (C.Ts + 1)));
+    VT_CHECK(C.nstage >= 2 && C.nstage <= CB_MAX_STAGES && NW <= CB_MAX_WARPS);
     // one threshold for rho, c and rho_pg (rho_bar = c_bar = pg_rho_bar, lambda = 1: the
     // paper's setting): one min instead of three
     const bool one_bar = !GEN && P.rho_bar == P.c_bar && P.rho_bar == P.pg_rho_bar && P.lambda == 1.0;
@@ -518,6 +534,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       const int t = t_first - j * tdec;
       const bool row_ok = col_ok && (t < T);
       unsigned char* sb = smem + (size_t)sx * C.stage;
+      VT_CHECK(sx >= 0 && sx < C.nstage);
       mbar_wait32(full0 + 8u * sx, phx);
       const int a_raw = lds<int>(sb + C.a + soff);
       const float rt = lds<float>(sb + C.r + soff);
@@ -526,6 +543,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       const float Vnt = lds<float>(sb + C.v + voff);  // (row T of the tile: zero-filled)
       const float Vn = (t + 1 < T) ? Vnt : boot;        // V(x_T) = bootstrap
       const int a = min(max(a_raw, 0), A - 1);
+      VT_CHECK(a >= 0 && a < A);
       const LT* zrow = reinterpret_cast<const LT*>(sb + C.pi + zoff);
       const LT* mrow = reinterpret_cast<const LT*>(sb + C.mu + zoff);
       CbRow<LT, A_CT> R;
@@ -624,10 +642,12 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     // ---- Y(j): the carry, a9-a11, release of the stage ------------------------------
     auto Y = [&](const int j, const CbSt<A_CT>& S) {
       unsigned char* sb = smem + (size_t)sy * C.stage;
+      VT_CHECK(sy >= 0 && sy < C.nstage && S.a >= 0 && S.a < A);
       double cin = carry;  // A just after this warp's 8 steps
       if (C.nts > 1) {
         // the group's aggregates of iteration j (published by X(j), before the barrier)
         const int par = j & 1;
+        VT_CHECK((C.nts - 1) * C.ncg + cg < NW);
         if (tl == 0) {
           double x = carry;
           for (int q = C.nts - 1; q > ts; --q)
@@ -731,6 +751,12 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     auto group_sync = [&]() {
       if (C.nts > 1) named_bar(1 + cg, 32 * C.nts);  // the group's X(j) aggregates are out
     };
+#if defined(CB_STAGGER) && CB_STAGGER > 0
+    // phase offset between the warps of a sub-partition (warps w and w + 4 share one):
+    // odd slots start later, so the sub-partition's warps are not all in their
+    // MUFU-heavy statistics (or fp64 chain) at the same time
+    if ((warp >> 2) & 1) __nanosleep(CB_STAGGER);
+#endif
 #if defined(CB_ABLATE) && CB_ABLATE == 2
     // timing ablation: data movement only (no arithmetic; garbage outputs)
     for (int j = 0; j < C.J; ++j) {
@@ -802,6 +828,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     double v = cs[0];
 #pragma unroll
     for (int k = 1; k < NPART; ++k) v = (lane == k) ? cs[k] : v;
+    VT_CHECK((int)blockIdx.x < S);
     if (lane < NPART) st_tag16(C.cta_recs + (size_t)blockIdx.x * NPART + lane, v, tag);
   }
   unsigned int prev = 0;
