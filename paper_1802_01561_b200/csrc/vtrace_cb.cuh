@@ -43,6 +43,17 @@
 #define VT_CHECK(c) ((void)0)
 #endif
 
+// compile-time variants (A/B builds, VTRACE_DEFINES)
+#ifndef CB_F32_EXACT
+#define CB_F32_EXACT 1  // fp32 logits: first-order correction for the roundings of z - m, (z - m) L32
+#endif
+#ifndef CB_PIPE
+#define CB_PIPE 0  // 1: X(j+1) next to Y(j) (software pipeline); 0: X(j) then Y(j)
+#endif
+#ifndef CB_EBUF
+#define CB_EBUF 0  // 1: the target exps wait in shared memory between X and Y
+#endif
+
 namespace vtb200 {
 
 constexpr int CB_MAX_WARPS = 14;   // compute warps per CTA (+1 producer: <= 128 registers)
@@ -289,12 +300,16 @@ __device__ __forceinline__ void cb_exps(const float2 (&z)[(A_CT + 1) / 2], float
     } else {
       d = __fadd2_rn(z[k], nm);
       y = __fmul2_rn(d, Lp);
+#if CB_F32_EXACT
       // TwoSum error of d = z - m, and the FMA residual of y = d L32
       const float2 bb = __fadd2_rn(d, make_float2(-z[k].x, -z[k].y));
       const float2 t = __fadd2_rn(d, make_float2(-bb.x, -bb.y));
       const float2 dlo = __fadd2_rn(__fadd2_rn(z[k], make_float2(-t.x, -t.y)),
                                     __fadd2_rn(nm, make_float2(-bb.x, -bb.y)));
       w = __ffma2_rn(dlo, Lp, __ffma2_rn(d, Lp, make_float2(-y.x, -y.y)));
+#else
+      w = f2(0.f);
+#endif
     }
     float2 ek = make_float2(ex2_approx(y.x), ex2_approx(y.y));
     if constexpr (A_CT % 2 == 1) {
@@ -306,7 +321,7 @@ __device__ __forceinline__ void cb_exps(const float2 (&z)[(A_CT + 1) / 2], float
     }
     if constexpr (KEEP) e[k] = ek;
     sdz = __ffma2_rn(ek, d, sdz);  // NaN if some z is inf/nan
-    if constexpr (!BF16) cw = __ffma2_rn(ek, w, cw);
+    if constexpr (!BF16 && CB_F32_EXACT) cw = __ffma2_rn(ek, w, cw);
     // Fast2Sum: h >= 1 >= e, so s = h + e and (h - s) + e is its exact error
     const float2 s = __fadd2_rn(h, ek);
     l = __fadd2_rn(l, __fadd2_rn(__fadd2_rn(h, make_float2(-s.x, -s.y)), ek));
@@ -368,12 +383,6 @@ __device__ __forceinline__ void cb_stats(const LT* zrow, const LT* mrow, int a,
 }
 
 // What X(j) hands to Y(j) for one lane's row (a3-a8 results that do not need the carry).
-#ifndef CB_PIPE
-#define CB_PIPE 0  // 1: X(j+1) next to Y(j) (software pipeline); 0: X(j) then Y(j)
-#endif
-#ifndef CB_EBUF
-#define CB_EBUF 0  // 1: the target exps wait in shared memory between X and Y
-#endif
 
 template <int A_CT>
 struct CbSt {
