@@ -348,7 +348,7 @@ def run_ours(args):
         sampler.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
     elapsed_max = max_over_ranks(elapsed_ms, world)
-    kw_step = dict(kw, workspace=ws, overlap_previous=overlap, sm_budget=step_obj.kw["sm_budget"])
+    kw_step = dict(kw, overlap_previous=overlap, sm_budget=step_obj.kw["sm_budget"])
 
     # kernel-only timing for the roofline: the same kernels, no collective
     Kk = min(K, 2000)
@@ -368,8 +368,14 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s_main)
     with torch.cuda.stream(s_main):
-        for _ in range(reps):
-            gk.replay()
+        for r_ in range(reps):
+            if gk is not None:
+                gk.replay()
+            else:  # (capture failed: the same launches eagerly)
+                for i in range(min(Kk, C)):
+                    x = sets[i % R]
+                    pkg.loss_and_grad(*[x[k] for k in vt.INPUT_NAMES], workspace=ws,
+                                      out=outs[i % R], **kw_step)
     e1.record(s_main)
     torch.cuda.synchronize()
     kernel_ms = e0.elapsed_time(e1) / (reps * min(Kk, C))
@@ -941,7 +947,14 @@ if __name__ == "__main__":
             run_reference(a)
         else:
             run_ours(a)
-    finally:
-        import torch.distributed as _dist
-        if _dist.is_available() and _dist.is_initialized():
-            _dist.destroy_process_group()
+    except BaseException:  # noqa: BLE001
+        # a failed rank must not hang in NCCL teardown (the others would wait for it):
+        # report and leave at once with a non-zero status
+        import traceback
+        traceback.print_exc()
+        sys.stderr.flush()
+        sys.stdout.flush()
+        os._exit(1)
+    import torch.distributed as _dist
+    if _dist.is_available() and _dist.is_initialized():
+        _dist.destroy_process_group()
