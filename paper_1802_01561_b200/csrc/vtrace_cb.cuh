@@ -56,6 +56,20 @@
 
 namespace vtb200 {
 
+#ifdef CB_TIMING
+// timing build only: per-CTA globaltimer stamps [start, first stage landed (warp 0),
+// last stage released (warp 0), partials published, exit of the last CTA's reduction]
+__device__ unsigned long long cb_stamps[4096][8];
+__device__ __forceinline__ unsigned long long cb_now() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return g;
+}
+#define CB_STAMP(k) (cb_stamps[blockIdx.x][k] = cb_now())
+#else
+#define CB_STAMP(k) ((void)0)
+#endif
+
 constexpr int CB_MAX_WARPS = 14;   // compute warps per CTA (+1 producer: <= 128 registers)
 constexpr int CB_MAX_STAGES = 4;
 
@@ -414,9 +428,11 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[CB_MAX_STAGES], done[CB_MAX_STAGES];
   __shared__ double agg[2][CB_MAX_WARPS][4][2];  // [parity][warp][column][G, D]
-  __shared__ double wpart[CB_MAX_WARPS][NPART];
+  __shared__ double wpart[CB_MAX_WARPS + 2][NPART];  // [warps | producer | own CTA sum]
+  __shared__ unsigned int s_epoch, s_last;
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) CB_STAMP(0);
   constexpr int A = A_CT;
   constexpr bool BF16 = sizeof(LT) == 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -458,15 +474,25 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
         tma_load_2d32(sb + C.gm, &M.g, c0, tb, fb);
         tma_load_2d32(sb + C.v, &M.v, c0, tb, fb);
       };
+      // the first stage alone, then the rest once it has landed: the first iteration's
+      // data is not queued behind the whole ring's (all SMs fill their rings at once)
       const int npre = min(C.nstage, C.J);
-      for (int s = 0; s < npre; ++s) load(s, s);
+      load(0, 0);
+      if (npre > 1) {
+        mbar_wait32(full0, 0u);
+        for (int s = 1; s < npre; ++s) load(s, s);
+      }
       int s = 0;
       uint32_t ph = 0;
       for (int j = 0; j < C.J; ++j) {
-        mbar_wait_sleep32(done0 + 8u * s, ph);
-        // (programmatic dependent launch: the first global write waits for the
-        // previous kernel on the stream)
-        if (P.pdl && j == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+        mbar_wait32(done0 + 8u * s, ph);
+        if (j == 0) {
+          // (programmatic dependent launch: the first global write waits for the previous
+          // kernel on the stream).  The call's epoch (it tags the partial-sum records) is
+          // final from here on: read it now, off the tail of the kernel
+          if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+          s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+        }
         const int tb = (C.J - 1 - j) * C.Ts;
         const uint32_t sb = sm0 + (uint32_t)s * C.stage;
 #if defined(CB_ABLATE) && CB_ABLATE == 1
@@ -545,6 +571,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       unsigned char* sb = smem + (size_t)sx * C.stage;
       VT_CHECK(sx >= 0 && sx < C.nstage);
       mbar_wait32(full0 + 8u * sx, phx);
+      if (j == 0 && threadIdx.x == 0) CB_STAMP(1);
       const int a_raw = lds<int>(sb + C.a + soff);
       const float rt = lds<float>(sb + C.r + soff);
       const float gm = lds<float>(sb + C.gm + soff);
@@ -754,6 +781,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive32(done0 + 8u * sy);
+      if (j == C.J - 1 && threadIdx.x == 0) CB_STAMP(2);
       sy = (sy + 1 == C.nstage) ? 0 : sy + 1;
     };
 
@@ -774,6 +802,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       group_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive32(done0 + 8u * sy);
+      if (j == C.J - 1 && threadIdx.x == 0) CB_STAMP(2);
       if (++sy == C.nstage) sy = 0;
     }
 #elif !CB_PIPE
@@ -820,86 +849,91 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     }
   }
   if (!LOSS || P.partials == nullptr) return;
-  __syncthreads();
-  if (warp != 0) return;
-  if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-  double cs[NPART];  // this CTA's sums, warps in order
-#pragma unroll
-  for (int k = 0; k < NPART; ++k) {
-    double x = 0.0;
-    for (int v = 0; v < NW; ++v) x += wpart[v][k];
-    cs[k] = x;
-  }
+  __syncthreads();  // wpart complete; s_epoch set (the producer's first iteration)
   const int S = gridDim.x;
-  const unsigned int epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+  const unsigned int epoch = s_epoch;
   const unsigned long long tag = ((unsigned long long)epoch << 2) | 3ull;
-  {
-    double v = cs[0];
-#pragma unroll
-    for (int k = 1; k < NPART; ++k) v = (lane == k) ? cs[k] : v;
+  if (warp == 0) {
+    if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    double v = 0.0;  // lane k < NPART: this CTA's sum k, warps in order
+    if (lane < NPART)
+      for (int w2 = 0; w2 < NW; ++w2) v += wpart[w2][lane];
     VT_CHECK((int)blockIdx.x < S);
     if (lane < NPART) st_tag16(C.cta_recs + (size_t)blockIdx.x * NPART + lane, v, tag);
-  }
-  unsigned int prev = 0;
-  if (lane == 0) prev = atomicAdd(C.top_count, 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != (unsigned int)(S - 1)) return;
-  if (lane == 0) *C.top_count = 0u;
-  // the last CTA: lane l adds CTAs l, l + 32, ... in order, then a fixed tree.  The
-  // records of 4 CTAs per lane are requested at once (one L2 round trip per 128 CTAs,
-  // not one per CTA); a record whose tag is not this call's yet is polled again.
-  double tp[NPART];
-#pragma unroll
-  for (int k = 0; k < NPART; ++k) tp[k] = 0.0;
-  constexpr int QB = 4;
-  for (int c0r = 0; c0r < S; c0r += 32 * QB) {
-    double x[QB][NPART];
-    unsigned long long tg[QB][NPART];
-#pragma unroll
-    for (int q = 0; q < QB; ++q) {
-      const int ci = c0r + 32 * q + lane;
-#pragma unroll
-      for (int k = 0; k < NPART; ++k) {
-        x[q][k] = 0.0;
-        tg[q][k] = tag;
-        if (ci < S && ci != (int)blockIdx.x)
-          ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[q][k], tg[q][k]);
-      }
+    if (lane < NPART) wpart[CB_MAX_WARPS + 1][lane] = v;  // (the last CTA's own, from shared)
+    unsigned int prev = 0;
+    if (lane == 0) prev = atomicAdd(C.top_count, 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (lane == 0) {
+      CB_STAMP(3);
+      s_last = (prev == (unsigned int)(S - 1)) ? 1u : 0u;
+      if (s_last) *C.top_count = 0u;  // every ticket of this call is taken: re-arm
     }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) CB_STAMP(5);
+  // the last CTA: all its warps request the other CTAs' records at once (warp w2 takes
+  // the contiguous CTA range [w2 S / W, (w2 + 1) S / W), lane = (CTA, partial)), re-poll
+  // any record whose tag is not this call's yet, add their range in CTA order; warp 0
+  // then adds the warps' sums in order: a fixed tree, independent of the arrival order
+  const int W = NW + 1;
+  {
+    const int c_lo = warp * S / W, c_hi = (warp + 1) * S / W;
+    const int k = lane & (NPART - 1), sub = lane >> 3;  // 4 CTAs per pass, one partial per lane
+    double acc_k = 0.0;
+    for (int cbase = c_lo; cbase < c_hi; cbase += 4 * 4) {
+      double x[4];
+      unsigned long long tg[4];
 #pragma unroll
-    for (int q = 0; q < QB; ++q) {
-      const int ci = c0r + 32 * q + lane;
-      if (ci == (int)blockIdx.x) {
-#pragma unroll
-        for (int k = 0; k < NPART; ++k) x[q][k] = cs[k];
-      }
-      bool ok = true;
-#pragma unroll
-      for (int k = 0; k < NPART; ++k) ok = ok && (tg[q][k] == tag);
-      int spins = 0;
-      while (!ok) {  // (value, tag) records: no fence on either side
-        if (++spins > 4) __nanosleep(32);
-        ok = true;
-#pragma unroll
-        for (int k = 0; k < NPART; ++k) {
-          ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[q][k], tg[q][k]);
-          ok = ok && (tg[q][k] == tag);
+      for (int q = 0; q < 4; ++q) {
+        const int ci = cbase + 4 * q + sub;
+        x[q] = 0.0;
+        tg[q] = tag;
+        if (ci < c_hi) {
+          if (ci == (int)blockIdx.x) x[q] = wpart[CB_MAX_WARPS + 1][k];
+          else ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[q], tg[q]);
         }
       }
 #pragma unroll
-      for (int k = 0; k < NPART; ++k) tp[k] += x[q][k];
+      for (int q = 0; q < 4; ++q) {
+        const int ci = cbase + 4 * q + sub;
+        int spins = 0;
+        while (ci < c_hi && ci != (int)blockIdx.x && tg[q] != tag) {
+          if (++spins > 4) __nanosleep(32);
+          ld_tag16(C.cta_recs + (size_t)ci * NPART + k, x[q], tg[q]);
+        }
+      }
+      // CTA order inside the pass: q major, sub minor -> ci = cbase + 4 q + sub
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double y = x[q];
+        // add the 4 CTAs of step q (lanes sub = 0..3 hold consecutive CTAs) in order
+        const double y1 = __shfl_sync(0xffffffffu, y, (lane & 7) + 8);
+        const double y2 = __shfl_sync(0xffffffffu, y, (lane & 7) + 16);
+        const double y3 = __shfl_sync(0xffffffffu, y, (lane & 7) + 24);
+        const double y0 = __shfl_sync(0xffffffffu, y, lane & 7);
+        acc_k += ((y0 + y1) + y2) + y3;
+      }
     }
+    if (lane < NPART) wpart[warp][lane] = acc_k;
+    if (threadIdx.x == 0) CB_STAMP(6);
   }
+  __syncthreads();
+  if (threadIdx.x == 0) CB_STAMP(7);
+  if (warp == 0 && lane == 0) {
+    double tp[NPART];
 #pragma unroll
-  for (int k = 0; k < NPART; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tp[k] += __shfl_xor_sync(0xffffffffu, tp[k], o);
-  }
-  if (lane == 0) {
+    for (int k = 0; k < NPART; ++k) {
+      double x = 0.0;
+      for (int w2 = 0; w2 < W; ++w2) x += wpart[w2][k];
+      tp[k] = x;
+    }
     tp[VT_P_TOTAL_LOSS] = tp[VT_P_PG_LOSS] + P.c_v * tp[VT_P_BASELINE_LOSS] - P.c_e * tp[VT_P_ENTROPY_SUM];
 #pragma unroll
     for (int k = 0; k < NPART; ++k) P.partials[k] = tp[k];
     *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
+    CB_STAMP(4);
   }
 }
 

@@ -161,6 +161,12 @@ static vt_status cb_dispatch(bool loss, const Params& P, const CbParams& C, cons
 }
 
 #if VT_CB_PART == 0
+#ifdef CB_TIMING
+// timing build only (not part of the ABI): copy the per-CTA stamps of the last launch
+extern "C" int vtrace_debug_cb_stamps(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, cb_stamps, sizeof(unsigned long long) * 8 * n);
+}
+#endif
 vt_status cb_launch_bf16(bool loss, const Params& P, const CbParams& C, const CbMaps& maps,
                          int grid, size_t smem, int dev, cudaStream_t st) {
   return cb_dispatch<__nv_bfloat16>(loss, P, C, maps, grid, smem, dev, st);
