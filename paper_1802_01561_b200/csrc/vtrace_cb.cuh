@@ -921,19 +921,19 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) CB_STAMP(7);
-  if (warp == 0 && lane == 0) {
-    double tp[NPART];
-#pragma unroll
-    for (int k = 0; k < NPART; ++k) {
-      double x = 0.0;
-      for (int w2 = 0; w2 < W; ++w2) x += wpart[w2][k];
-      tp[k] = x;
-    }
-    tp[VT_P_TOTAL_LOSS] = tp[VT_P_PG_LOSS] + P.c_v * tp[VT_P_BASELINE_LOSS] - P.c_e * tp[VT_P_ENTROPY_SUM];
-#pragma unroll
-    for (int k = 0; k < NPART; ++k) P.partials[k] = tp[k];
-    *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
-    CB_STAMP(4);
+  if (warp == 0) {
+    // lane k < NPART adds partial k over the warps in order (one short chain per lane,
+    // not one serial chain through all of them)
+    double x = 0.0;
+    if (lane < NPART)
+      for (int w2 = 0; w2 < W; ++w2) x += wpart[w2][lane];
+    const double pg = __shfl_sync(0xffffffffu, x, VT_P_PG_LOSS);
+    const double bl = __shfl_sync(0xffffffffu, x, VT_P_BASELINE_LOSS);
+    const double en = __shfl_sync(0xffffffffu, x, VT_P_ENTROPY_SUM);
+    if (lane == VT_P_TOTAL_LOSS) x = pg + P.c_v * bl - P.c_e * en;
+    if (lane < NPART) P.partials[lane] = x;
+    if (lane == 0) *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
+    if (lane == 0) CB_STAMP(4);
   }
 }
 
