@@ -588,7 +588,9 @@ __global__ void __launch_bounds__(NTHREADS, 4)
   }
   __syncthreads();
   if (tid == 0) {
-    if constexpr (LOSS && USE_TMA) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // (the gradient stores must have read the CTA's shared memory; their global writes
+    // complete with the grid)
+    if constexpr (LOSS && USE_TMA) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __threadfence();
     const unsigned int prev = atomicAdd(&P.ws->exited, 1u);
     s_last = (prev == gridDim.x - 1);
@@ -611,9 +613,10 @@ __global__ void __launch_bounds__(NTHREADS, 4)
 #pragma unroll
           for (int q = 0; q < 8; ++q) x += buf[q];
         }
-        double tot = 0.0;
-        for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, x, l);
-        if (lane == 0) s_fin[k] = tot;
+        // a fixed butterfly over the 32 lane sums (deterministic; not a serial chain)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) s_fin[k] = x;
       }
       __syncthreads();
       if (tid == 0) {
