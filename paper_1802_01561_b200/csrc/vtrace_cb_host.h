@@ -14,6 +14,10 @@ struct CbPlan {
   size_t smem;
 };
 
+// Dynamic shared memory of one column-block CTA: the stages (+ ~9 KB of static arrays,
+// within the 227 KB per-CTA opt-in limit)
+constexpr size_t kCbMaxDynSmem = kMaxSmem - 12 * 1024;
+
 // Compile-time action counts the column-block kernel is instantiated for.
 inline bool cb_supported_a(long long A) { return A == 3 || A == 4 || A == 6 || A == 9 || A == 18; }
 

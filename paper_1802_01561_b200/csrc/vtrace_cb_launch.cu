@@ -73,7 +73,7 @@ bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out
   };
   // shared memory: the stages, the compute warps' exps buffers (2 per warp, NP float2
   // per lane), plus ~3.5 KB of static arrays
-  const size_t budget = kMaxSmem;
+  const size_t budget = kCbMaxDynSmem;
   const auto ebuf_bytes = [&](int nts_) {
     return CB_EBUF ? (size_t)ncg * nts_ * 2 * ((A + 1) / 2) * 32 * 8 : (size_t)0;
   };
@@ -111,8 +111,8 @@ static vt_status cb_launch_one(const Params& P, const CbParams& C, const CbMaps&
   static std::atomic<unsigned long long> attr_set{0};
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kCbMaxDynSmem) != cudaSuccess)
       return VT_ERR_CUDA;
     attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
