@@ -890,9 +890,12 @@ static KernelChoice choose_kernel(long long T, long long B, long long A, int ele
                    plan.Tc + 1 <= 256 && plan.smem <= kMaxSmem;
   CbPlan tmp;
   CbPlan& cp = cbp ? *cbp : tmp;
-  const bool cb = ptrs16 && forced != VT_KERNEL_LOOKBACK &&
-                  cb_plan(T, B, (int)A, elem, mu_lp, out_mask, sms, cp);
-  if (cb) return K_CB;
+  if (forced != VT_KERNEL_LOOKBACK) {
+    if (ptrs16 && cb_plan(T, B, (int)A, elem, mu_lp, out_mask, sms, cp, false)) return K_CB;
+    // small shapes whose pitches or bases rule out TMA: the same kernel with plain loads
+    if (cb_supported_a(A) && cb_plan(T, B, (int)A, elem, mu_lp, out_mask, sms, cp, true))
+      return K_CB;
+  }
   return tma ? K_LOOKBACK_TMA : K_LOOKBACK_PLAIN;
 }
 
@@ -987,6 +990,22 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   const KernelChoice kc = choose_kernel(T, B, A, elem, plan, ptrs16, mu_lp, om, sms,
                                         prm->kernel, &cp);
   if (prm->kernel == VT_KERNEL_COLUMN_BLOCK && kc != K_CB) return VT_ERR_SHAPE;
+  if (kc == K_CB && cp.plain) {
+    CbMaps cm;
+    std::memset(&cm, 0, sizeof(cm));
+    CbParams C;
+    std::memset(&C, 0, sizeof(C));
+    C.ncg = cp.ncg; C.nts = cp.nts; C.Ts = cp.Ts; C.J = cp.J; C.nstage = cp.nstage; C.g = cp.g;
+    C.Bc = cp.Bc;
+    C.pi = cp.pi; C.mu = cp.mu; C.a = cp.a; C.r = cp.r; C.gm = cp.gm; C.v = cp.v; C.dv = cp.dv;
+    C.vs = cp.vs; C.pg = cp.pg; C.lr = cp.lr; C.lp = cp.lp; C.lm = cp.lm; C.stage = cp.stage;
+    C.tx_bytes = cp.tx_bytes; C.out_mask = cp.out_mask;
+    const WsLayout wl2 = ws_layout(plan);
+    C.cta_recs = reinterpret_cast<TagRec*>(wsb + wl2.cb_recs);
+    C.top_count = reinterpret_cast<unsigned int*>(wsb + wl2.cb_count);
+    return dt == VT_BFLOAT16 ? cb_launch_bf16(loss, true, P, C, cm, cp.grid, cp.smem, dev, st)
+                             : cb_launch_f32(loss, true, P, C, cm, cp.grid, cp.smem, dev, st);
+  }
   if (kc == K_CB) {
     const CUtensorMapDataType ldt =
         dt == VT_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -1021,8 +1040,8 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
     const WsLayout wl2 = ws_layout(plan);
     C.cta_recs = reinterpret_cast<TagRec*>(wsb + wl2.cb_recs);
     C.top_count = reinterpret_cast<unsigned int*>(wsb + wl2.cb_count);
-    return dt == VT_BFLOAT16 ? cb_launch_bf16(loss, P, C, cm, cp.grid, cp.smem, dev, st)
-                             : cb_launch_f32(loss, P, C, cm, cp.grid, cp.smem, dev, st);
+    return dt == VT_BFLOAT16 ? cb_launch_bf16(loss, false, P, C, cm, cp.grid, cp.smem, dev, st)
+                             : cb_launch_f32(loss, false, P, C, cm, cp.grid, cp.smem, dev, st);
   }
   TmaMaps maps;
   std::memset(&maps, 0, sizeof(maps));
@@ -1182,9 +1201,10 @@ const char* vtrace_kernel_for(int64_t T, int64_t B, int64_t A, vt_dtype logits_d
   const Plan plan = make_plan(T, B, (int)A, elem);
   int dev = 0;
   const int sms = cudaGetDevice(&dev) == cudaSuccess ? cb_num_sms(dev) : 0;
+  CbPlan cpk;
   switch (choose_kernel(T, B, A, elem, plan, true, false, OUT_DZ | OUT_DV, sms > 0 ? sms : 148,
-                        VT_KERNEL_AUTO, nullptr)) {
-    case K_CB: return "vtrace_cb_kernel";
+                        VT_KERNEL_AUTO, &cpk)) {
+    case K_CB: return cpk.plain ? "vtrace_cb_kernel (plain loads)" : "vtrace_cb_kernel";
     case K_LOOKBACK_TMA: return "vtrace_fused_kernel";
     default: return "vtrace_fused_kernel (plain loads)";
   }

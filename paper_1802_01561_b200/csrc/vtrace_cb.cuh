@@ -424,7 +424,90 @@ struct CbAcc {
 // log-probs (false: plain V-trace, that logic compiled out); MULP: the behaviour is
 // log mu(a_t) [T][B] (no mu tile, no mu statistics; implies GEN).  LOSS: the fused
 // loss + gradients (vtrace_loss_and_grad), else vtrace_from_logits' outputs.
-template <typename LT, int A_CT, bool LOSS, bool GEN, bool MULP>
+// Plain-load producer (PLAIN: shapes whose pitches or bases do not allow TMA boxes, e.g. the
+// toy's 24-byte rows): the producer warp's 32 lanes copy the same tiles with ordinary loads
+// into the same shared-memory layout (zero outside the batch), arrive on `full` (one arrival
+// per lane), and copy the output tiles back with ordinary stores.  Small problems only.
+template <typename LT, int A_CT, bool LOSS, bool MULP>
+struct CbPlainIO {
+  const Params& P;
+  const CbParams& C;
+  unsigned char* smem;
+  int c0, lane;
+  __device__ __forceinline__ void load(int j, int s) const {
+    const int T = P.T32, B = P.B32, Ts = C.Ts, Bc = C.Bc;
+    const int tb = (C.J - 1 - j) * Ts;
+    unsigned char* sb = smem + (size_t)s * C.stage;
+    LT* zp = reinterpret_cast<LT*>(sb + C.pi);
+    LT* zm = reinterpret_cast<LT*>(sb + C.mu);
+    const LT* gp = reinterpret_cast<const LT*>(P.pi);
+    const LT* gm = reinterpret_cast<const LT*>(P.mu);
+    // logits rows ((cg Ts + t) 4 + c) A + k (g = 1)
+    const int nz = Ts * Bc * A_CT;
+    for (int i = lane; i < nz; i += 32) {
+      const int k = i % A_CT, row = i / A_CT;
+      const int c = row & 3, rest = row >> 2;
+      const int t = rest % Ts, cg = rest / Ts;
+      const int tt = tb + t, b = c0 + 4 * cg + c;
+      const bool ok = tt < T && b < B;
+      const size_t gi = ((size_t)tt * B + b) * A_CT + k;
+      zp[i] = ok ? gp[gi] : LT(0.f);
+      if constexpr (!MULP) zm[i] = ok ? gm[gi] : LT(0.f);
+    }
+    const int ns = Ts * Bc;
+    for (int i = lane; i < ns; i += 32) {  // [Ts][Bc] per-step tiles
+      const int t = i / Bc, bl = i - t * Bc;
+      const int tt = tb + t, b = c0 + bl;
+      const bool ok = tt < T && b < B;
+      const size_t gi = (size_t)tt * B + b;
+      reinterpret_cast<int*>(sb + C.a)[i] = ok ? P.actions[gi] : 0;
+      reinterpret_cast<float*>(sb + C.r)[i] = ok ? P.rew[gi] : 0.f;
+      reinterpret_cast<float*>(sb + C.gm)[i] = ok ? P.disc[gi] : 0.f;
+      if constexpr (MULP)
+        reinterpret_cast<float*>(sb + C.mu)[i] = ok ? reinterpret_cast<const float*>(P.mu)[gi] : 0.f;
+    }
+    for (int i = lane; i < ns + Bc; i += 32) {  // V [Ts + 1][Bc]
+      const int t = i / Bc, bl = i - t * Bc;
+      const int tt = tb + t, b = c0 + bl;
+      const bool ok = tt < T && b < B;
+      reinterpret_cast<float*>(sb + C.v)[i] = ok ? P.val[(size_t)tt * B + b] : 0.f;
+    }
+  }
+  __device__ __forceinline__ void store(int j, int s, unsigned om) const {
+    const int T = P.T32, B = P.B32, Ts = C.Ts, Bc = C.Bc;
+    const int tb = (C.J - 1 - j) * Ts;
+    const unsigned char* sb = smem + (size_t)s * C.stage;
+    if (om & OUT_DZ) {
+      const LT* zp = reinterpret_cast<const LT*>(sb + C.pi);
+      LT* gd = reinterpret_cast<LT*>(P.dlogits);
+      const int nz = Ts * Bc * A_CT;
+      for (int i = lane; i < nz; i += 32) {
+        const int k = i % A_CT, row = i / A_CT;
+        const int c = row & 3, rest = row >> 2;
+        const int t = rest % Ts, cg = rest / Ts;
+        const int tt = tb + t, b = c0 + 4 * cg + c;
+        if (tt < T && b < B) gd[((size_t)tt * B + b) * A_CT + k] = zp[i];
+      }
+    }
+    const int ns = Ts * Bc;
+    auto out = [&](unsigned bit, unsigned off, float* g) {
+      if (!(om & bit)) return;
+      for (int i = lane; i < ns; i += 32) {
+        const int t = i / Bc, bl = i - t * Bc;
+        const int tt = tb + t, b = c0 + bl;
+        if (tt < T && b < B) g[(size_t)tt * B + b] = reinterpret_cast<const float*>(sb + off)[i];
+      }
+    };
+    out(OUT_DV, C.dv, P.dvalues);
+    out(OUT_VS, C.vs, P.vs);
+    out(OUT_PG, C.pg, P.pg_adv);
+    out(OUT_LR, C.lr, P.log_rhos);
+    out(OUT_LP, C.lp, P.lp_out);
+    out(OUT_LM, C.lm, P.lm_out);
+  }
+};
+
+template <typename LT, int A_CT, bool LOSS, bool GEN, bool MULP, bool PLAIN = false>
 __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     vtrace_cb_kernel(const Params P, const CbParams C, const __grid_constant__ CbMaps M) {
   static_assert(A_CT > 0, "compile-time A");
@@ -444,14 +527,42 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
   const int c0 = blockIdx.x * C.Bc;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C.nstage; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PLAIN ? 32 : 1);
       mbar_init(&done[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == NW) {
+  if (PLAIN && warp == NW) {
+    // ---------------- producer, plain loads (all 32 lanes) ----------------
+    const CbPlainIO<LT, A_CT, LOSS, MULP> io{P, C, smem, c0, lane};
+    const uint32_t full0 = smem_u32(&full[0]), done0 = smem_u32(&done[0]);
+    const int npre = min(C.nstage, C.J);
+    for (int s2 = 0; s2 < npre; ++s2) {
+      io.load(s2, s2);
+      mbar_arrive32(full0 + 8u * s2);  // (release: this lane's tile writes)
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int j = 0; j < C.J; ++j) {
+      mbar_wait32(done0 + 8u * s, ph);
+      if (j == 0) {
+        if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0) s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+      }
+      io.store(j, s, C.out_mask);
+      __syncwarp();
+      if (j + C.nstage < C.J) {
+        io.load(j + C.nstage, s);
+        mbar_arrive32(full0 + 8u * s);
+      }
+      if (++s == C.nstage) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  } else if (warp == NW) {
     // ---------------- producer ----------------
     if (lane == 0) {
       const int zc = c0 / (4 * C.g);  // first logits column segment of the block

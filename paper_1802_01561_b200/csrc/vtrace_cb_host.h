@@ -12,6 +12,7 @@ struct CbPlan {
   int g, ncg, nts, Bc, Ts, J, nstage, grid;
   unsigned pi, mu, a, r, gm, v, dv, vs, pg, lr, lp, lm, stage, tx_bytes, out_mask, ebuf;
   size_t smem;
+  int plain;  // 1: plain-load producer (no TMA)
 };
 
 // Dynamic shared memory of one column-block CTA: the stages (+ ~9 KB of static arrays,
@@ -23,13 +24,13 @@ inline bool cb_supported_a(long long A) { return A == 3 || A == 4 || A == 6 || A
 
 // Work split for (T, B, A, elem) on `sms` SMs; false if the kernel does not apply.
 bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out_mask, int sms,
-             CbPlan& p);
+             CbPlan& p, bool plain = false);
 
 int cb_num_sms(int dev);  // SM count of device `dev` (cached per device)
 
-vt_status cb_launch_bf16(bool loss, const Params& P, const CbParams& C, const CbMaps& maps,
-                         int grid, size_t smem, int dev, cudaStream_t st);
-vt_status cb_launch_f32(bool loss, const Params& P, const CbParams& C, const CbMaps& maps,
-                        int grid, size_t smem, int dev, cudaStream_t st);
+vt_status cb_launch_bf16(bool loss, bool plain, const Params& P, const CbParams& C,
+                         const CbMaps& maps, int grid, size_t smem, int dev, cudaStream_t st);
+vt_status cb_launch_f32(bool loss, bool plain, const Params& P, const CbParams& C,
+                        const CbMaps& maps, int grid, size_t smem, int dev, cudaStream_t st);
 
 }  // namespace vtb200

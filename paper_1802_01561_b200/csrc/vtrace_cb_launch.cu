@@ -30,16 +30,22 @@ namespace vtb200 {
 //        number of 8-step chunks, spread so that the iterations are evenly filled
 // False if the shape does not fit the kernel (then the look-back kernel runs).
 bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out_mask, int sms,
-             CbPlan& p) {
+             CbPlan& p, bool plain) {
   std::memset(&p, 0, sizeof(p));
   if (sms <= 0 || T <= 0 || B <= 0) return false;
-  const int g = ((4 * A * elem) % 16 == 0) ? 1 : (((8 * A * elem) % 16 == 0) ? 2 : 4);
-  if (g > 2) return false;
-  if (4 * g * A > 256) return false;           // TMA box inner dimension
-  if (B % (4 * g) != 0) return false;          // the [T][B/(4g)][4gA] view is exact
+  int g = 1;
+  if (plain) {
+    // plain loads: no alignment constraint, small problems only (one warp copies the tiles)
+    if (T * B * A > (1LL << 20)) return false;
+  } else {
+    g = ((4 * A * elem) % 16 == 0) ? 1 : (((8 * A * elem) % 16 == 0) ? 2 : 4);
+    if (g > 2) return false;
+    if (4 * g * A > 256) return false;           // TMA box inner dimension
+    if (B % (4 * g) != 0) return false;          // the [T][B/(4g)][4gA] view is exact
+  }
   if ((T + 256) * B >= (1LL << 31)) return false;  // 32-bit row arithmetic
   if (!cb_supported_a(A)) return false;
-  const long long G4 = B / 4;
+  const long long G4 = (B + 3) / 4;
   int ncg = (int)std::min<long long>((G4 + sms - 1) / sms, CB_MAX_WARPS);
   ncg = (ncg + g - 1) / g * g;
   if (ncg > CB_MAX_WARPS) ncg -= g;
@@ -88,6 +94,7 @@ bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out
   p.ebuf = (unsigned)(nstage * st);
   p.smem = nstage * st + ebuf_bytes(nts);
   p.out_mask = out_mask;
+  p.plain = plain ? 1 : 0;
   return true;
 }
 
@@ -103,10 +110,10 @@ int cb_num_sms(int dev) {
 }
 #endif
 
-template <typename LT, int A_CT, bool LOSS, bool GEN, bool MULP>
+template <typename LT, int A_CT, bool LOSS, bool GEN, bool MULP, bool PLAIN>
 static vt_status cb_launch_one(const Params& P, const CbParams& C, const CbMaps& maps, int grid,
                                size_t smem, int dev, cudaStream_t st) {
-  auto kern = vtrace_cb_kernel<LT, A_CT, LOSS, GEN, MULP>;
+  auto kern = vtrace_cb_kernel<LT, A_CT, LOSS, GEN, MULP, PLAIN>;
   // the dynamic shared-memory limit is a per-device function attribute: set once per device
   static std::atomic<unsigned long long> attr_set{0};
   const unsigned long long bit = 1ull << (dev & 63);
@@ -131,33 +138,40 @@ static vt_status cb_launch_one(const Params& P, const CbParams& C, const CbMaps&
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
-template <typename LT, bool LOSS, bool GEN, bool MULP>
+template <typename LT, bool LOSS, bool GEN, bool MULP, bool PLAIN>
 static vt_status cb_dispatch_a(const Params& P, const CbParams& C, const CbMaps& maps, int grid,
                                size_t smem, int dev, cudaStream_t st) {
   switch (P.A) {
-    case 18: return cb_launch_one<LT, 18, LOSS, GEN, MULP>(P, C, maps, grid, smem, dev, st);
-    case 9: return cb_launch_one<LT, 9, LOSS, GEN, MULP>(P, C, maps, grid, smem, dev, st);
-    case 6: return cb_launch_one<LT, 6, LOSS, GEN, MULP>(P, C, maps, grid, smem, dev, st);
-    case 4: return cb_launch_one<LT, 4, LOSS, GEN, MULP>(P, C, maps, grid, smem, dev, st);
-    case 3: return cb_launch_one<LT, 3, LOSS, GEN, MULP>(P, C, maps, grid, smem, dev, st);
+    case 18: return cb_launch_one<LT, 18, LOSS, GEN, MULP, PLAIN>(P, C, maps, grid, smem, dev, st);
+    case 9: return cb_launch_one<LT, 9, LOSS, GEN, MULP, PLAIN>(P, C, maps, grid, smem, dev, st);
+    case 6: return cb_launch_one<LT, 6, LOSS, GEN, MULP, PLAIN>(P, C, maps, grid, smem, dev, st);
+    case 4: return cb_launch_one<LT, 4, LOSS, GEN, MULP, PLAIN>(P, C, maps, grid, smem, dev, st);
+    case 3: return cb_launch_one<LT, 3, LOSS, GEN, MULP, PLAIN>(P, C, maps, grid, smem, dev, st);
     default: return VT_ERR_SHAPE;
   }
 }
 
+template <typename LT, bool LOSS, bool GEN, bool MULP>
+static vt_status cb_dispatch_p(bool plain, const Params& P, const CbParams& C, const CbMaps& maps,
+                               int grid, size_t smem, int dev, cudaStream_t st) {
+  return plain ? cb_dispatch_a<LT, LOSS, GEN, MULP, true>(P, C, maps, grid, smem, dev, st)
+               : cb_dispatch_a<LT, LOSS, GEN, MULP, false>(P, C, maps, grid, smem, dev, st);
+}
+
 template <typename LT>
-static vt_status cb_dispatch(bool loss, const Params& P, const CbParams& C, const CbMaps& maps,
-                             int grid, size_t smem, int dev, cudaStream_t st) {
+static vt_status cb_dispatch(bool loss, bool plain, const Params& P, const CbParams& C,
+                             const CbMaps& maps, int grid, size_t smem, int dev, cudaStream_t st) {
   // plain V-trace from logits takes the instantiation with the variant logic compiled
   // out; behaviour log-probs (MULP) come with the general one
   const bool gen = P.correction != VT_CORRECTION_VTRACE || P.q_values != 0 || P.mu_lp != 0;
   if (loss) {
-    if (P.mu_lp) return cb_dispatch_a<LT, true, true, true>(P, C, maps, grid, smem, dev, st);
-    if (gen) return cb_dispatch_a<LT, true, true, false>(P, C, maps, grid, smem, dev, st);
-    return cb_dispatch_a<LT, true, false, false>(P, C, maps, grid, smem, dev, st);
+    if (P.mu_lp) return cb_dispatch_p<LT, true, true, true>(plain, P, C, maps, grid, smem, dev, st);
+    if (gen) return cb_dispatch_p<LT, true, true, false>(plain, P, C, maps, grid, smem, dev, st);
+    return cb_dispatch_p<LT, true, false, false>(plain, P, C, maps, grid, smem, dev, st);
   }
-  if (P.mu_lp) return cb_dispatch_a<LT, false, true, true>(P, C, maps, grid, smem, dev, st);
-  if (gen) return cb_dispatch_a<LT, false, true, false>(P, C, maps, grid, smem, dev, st);
-  return cb_dispatch_a<LT, false, false, false>(P, C, maps, grid, smem, dev, st);
+  if (P.mu_lp) return cb_dispatch_p<LT, false, true, true>(plain, P, C, maps, grid, smem, dev, st);
+  if (gen) return cb_dispatch_p<LT, false, true, false>(plain, P, C, maps, grid, smem, dev, st);
+  return cb_dispatch_p<LT, false, false, false>(plain, P, C, maps, grid, smem, dev, st);
 }
 
 #if VT_CB_PART == 0
@@ -167,14 +181,14 @@ extern "C" int vtrace_debug_cb_stamps(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, cb_stamps, sizeof(unsigned long long) * 8 * n);
 }
 #endif
-vt_status cb_launch_bf16(bool loss, const Params& P, const CbParams& C, const CbMaps& maps,
-                         int grid, size_t smem, int dev, cudaStream_t st) {
-  return cb_dispatch<__nv_bfloat16>(loss, P, C, maps, grid, smem, dev, st);
+vt_status cb_launch_bf16(bool loss, bool plain, const Params& P, const CbParams& C,
+                         const CbMaps& maps, int grid, size_t smem, int dev, cudaStream_t st) {
+  return cb_dispatch<__nv_bfloat16>(loss, plain, P, C, maps, grid, smem, dev, st);
 }
 #else
-vt_status cb_launch_f32(bool loss, const Params& P, const CbParams& C, const CbMaps& maps,
-                        int grid, size_t smem, int dev, cudaStream_t st) {
-  return cb_dispatch<float>(loss, P, C, maps, grid, smem, dev, st);
+vt_status cb_launch_f32(bool loss, bool plain, const Params& P, const CbParams& C,
+                        const CbMaps& maps, int grid, size_t smem, int dev, cudaStream_t st) {
+  return cb_dispatch<float>(loss, plain, P, C, maps, grid, smem, dev, st);
 }
 #endif
 

@@ -132,7 +132,8 @@ def test_kernel_choice(lib):
     assert vt.kernel_for(100, 4096, 24, 1) == "vtrace_fused_kernel"       # A not instantiated
     assert vt.kernel_for(100, 4092, 9, 1) == "vtrace_fused_kernel (plain loads)"  # pitch % 16
     assert vt.kernel_for(100, 4096, 40, 1) == "vtrace_fused_kernel (plain loads)"  # 8 A > 256
-    assert vt.kernel_for(5, 2, 3, 0) == "vtrace_fused_kernel (plain loads)"  # toy: pitch 24 B
+    assert vt.kernel_for(5, 2, 3, 0) == "vtrace_cb_kernel (plain loads)"   # toy: pitch 24 B
+    assert vt.kernel_for(2000, 1022, 9, 0) == "vtrace_fused_kernel (plain loads)"  # big, unaligned
     assert vt.kernel_for(0, 8, 3, 0).startswith("none")
     assert vt.kernel_for(5, 8, 3, 7).startswith("none")
 
