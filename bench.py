@@ -327,17 +327,23 @@ def run_ours(args):
     # warm the graphs (untimed): replays for at least PREROLL_S of GPU time, so that the
     # timed K steps run at the settled SM clock (a 20-step region right after a cold start
     # otherwise catches the clock ramp: 31.3 vs 27.3 us per step at `large`)
+    # The replay count is agreed over the ranks (the graphs hold the collectives: ranks
+    # that replayed different counts would wait for each other forever).
     preroll_reps = 0
     if g_full is not None or g_rem is not None:
         gw = g_rem or g_full
-        t_pre = time.time()
-        while True:
+        for _ in range(2):  # the first replay uploads the graph: time the second
+            t_pre = time.time()
             with torch.cuda.stream(s_main):
                 gw.replay()
-            preroll_reps += 1
             torch.cuda.synchronize()
-            if time.time() - t_pre >= PREROLL_S or preroll_reps >= 10000:
-                break
+        one = max(time.time() - t_pre, 1e-6)
+        reps = min(10000, max(2, math.ceil(PREROLL_S / one)))
+        reps = int(max_over_ranks(float(reps), world))
+        for _ in range(reps - 2):
+            with torch.cuda.stream(s_main):
+                gw.replay()
+        preroll_reps = reps
     torch.cuda.synchronize()
 
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
@@ -943,6 +949,9 @@ if __name__ == "__main__":
     if _world != a.gpus:
         print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={_world}", file=sys.stderr)
         sys.exit(2)
+    if os.environ.get("VT_BENCH_WATCHDOG"):  # diagnostics: every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["VT_BENCH_WATCHDOG"]), exit=True)
     try:
         if a.path == "head":
             if a.impl == "reference":

@@ -851,7 +851,7 @@ static vt_status dispatch(const Params& P, const TmaMaps& maps, const Plan& plan
 
 static bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
-static vt_status check_params(const vt_vtrace_params* p) {
+vt_status check_params(const vt_vtrace_params* p) {
   if (!p) return VT_ERR_INVALID_ARG;
   const float rb = p->clip_rho_threshold, cb = p->clip_c_threshold,
               pb = p->clip_pg_rho_threshold, l = p->lambda_;

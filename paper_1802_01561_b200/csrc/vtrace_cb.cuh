@@ -59,6 +59,13 @@
 
 namespace vtb200 {
 
+#ifndef CB_PLAIN_SUMS
+#define CB_PLAIN_SUMS 0   // A/B only: plain (uncompensated) exponent sums
+#endif
+#ifndef CB_TD32
+#define CB_TD32 0         // A/B only: r + gamma V' - V in fp32
+#endif
+
 #ifdef CB_TIMING
 // timing build only: per-CTA globaltimer stamps [start, first stage landed (warp 0),
 // last stage released (warp 0), partials published, exit of the last CTA's reduction]
@@ -339,10 +346,14 @@ __device__ __forceinline__ void cb_exps(const float2 (&z)[(A_CT + 1) / 2], float
     if constexpr (KEEP) e[k] = ek;
     sdz = __ffma2_rn(ek, d, sdz);  // NaN if some z is inf/nan
     if constexpr (!BF16 && CB_F32_EXACT) cw = __ffma2_rn(ek, w, cw);
+#if CB_PLAIN_SUMS
+    h = __fadd2_rn(h, ek);
+#else
     // Fast2Sum: h >= 1 >= e, so s = h + e and (h - s) + e is its exact error
     const float2 s = __fadd2_rn(h, ek);
     l = __fadd2_rn(l, __fadd2_rn(__fadd2_rn(h, make_float2(-s.x, -s.y)), ek));
     h = s;
+#endif
   }
 }
 
@@ -706,7 +717,11 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       }
       // a5, a7: pi(a)/mu(a) = exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) S_mu / S_pi
       const double ratio = exp64(xa_p - xa_m) * ddiv_pos(R.S_m, R.S_p);
+#if CB_TD32
+      const double td = (double)(fmaf(gm, Vn, (float)reward_transform(rt, P.reward_mode)) - Vt);
+#else
       const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
+#endif
       StepWeights sw;
       if (one_bar) {
         const double rh = dmin_t(P.rho_bar, ratio);

@@ -28,6 +28,9 @@ bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out
 
 int cb_num_sms(int dev);  // SM count of device `dev` (cached per device)
 
+// Validation of the method parameters shared by every V-trace entry point (vtrace_api.cu).
+vt_status check_params(const vt_vtrace_params* p);
+
 vt_status cb_launch_bf16(bool loss, bool plain, const Params& P, const CbParams& C,
                          const CbMaps& maps, int grid, size_t smem, int dev, cudaStream_t st);
 vt_status cb_launch_f32(bool loss, bool plain, const Params& P, const CbParams& C,
