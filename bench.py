@@ -62,9 +62,12 @@ def parse():
     ap.add_argument("--reserve-sms", type=int, default=1,
                     help="N > 1: SMs the kernel leaves to the per-step NCCL collective so that "
                          "steps can overlap (0: no overlap at N > 1)")
+    ap.add_argument("--collective", choices=["nvlink", "nccl"], default="nvlink",
+                    help="N > 1: how the step's 8 partials are summed over the learners: "
+                         "vtrace_partials_allreduce over NVLink peer memory (default) or NCCL")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
-    ap.add_argument("--path", choices=["vtrace", "update", "head"], default="vtrace",
+    ap.add_argument("--path", choices=["vtrace", "update", "head", "head_fused"], default="vtrace",
                     help="update: the learner's parameter update after the backward "
                          "(SURVEY 8(f) NEXT #4: gradient all-reduce at N > 1, global-norm "
                          "clip, RMSProp) instead of the V-trace path; head: the tcgen05 output "
@@ -281,7 +284,8 @@ def run_ours(args):
     # left to the collective at N > 1
     overlap = not args.no_overlap
     step_obj = learner.LearnerStep(T, B, A, inp["dtype"], overlap=overlap,
-                                   reserve_sms=(args.reserve_sms if world > 1 else 0), **kw)
+                                   reserve_sms=(args.reserve_sms if world > 1 else 0),
+                                   collective=args.collective, **kw)
     ws = step_obj.workspace
     s_main = step_obj.stream
 
@@ -473,9 +477,14 @@ def run_ours(args):
                                     f"replays (>= {PREROLL_S} s, clock settle)",
                    "step_overlap": "programmatic dependent launch (overlap_previous: inputs are "
                                    "fresh batches)" if overlap else "none",
-                   "collective": "NCCL all_reduce of 8 fp64 partials per step (side stream"
-                                 + (f", {args.reserve_sms} SM reserved)" if args.reserve_sms else ")")
-                   if world > 1 else "none",
+                   "collective": ("none" if world == 1 else
+                                  ("vtrace_partials_allreduce: 8 fp64 partials per step through "
+                                   "peer-mapped mailboxes over NVLink, one 32-thread kernel"
+                                   if args.collective == "nvlink" else
+                                   "NCCL all_reduce of 8 fp64 partials per step")
+                                  + " (side stream"
+                                  + (f", {args.reserve_sms} SM reserved)" if args.reserve_sms
+                                     else ")")),
                    "step": "paper_1802_01561_b200.learner.LearnerStep"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -923,6 +932,152 @@ def run_head(args):
     print(json.dumps(line), flush=True)
 
 
+def run_head_fused(args):
+    """K calls of vtrace_head_loss_and_grad (NEXT #3 second half) at the `large` config:
+    T=100, B=8192 trajectories, H=256 hidden, A=18 -- the output layer with the V-trace loss
+    and gradients as its epilogue and the head backward (dh, dW, db).  Each rank its own
+    batch (weak scaling, no collective).  Two input sets alternated; h (419 MB) exceeds L2."""
+    world, rank, local = dist_env()
+    init_dist(world, local)
+    torch.cuda.set_device(local)
+    import paper_1802_01561_b200 as pkg
+    T, B, H, A = 100, 8192, 256, 18
+    M = T * B
+    g = torch.Generator(device="cuda").manual_seed(200 + rank)
+    w = (torch.randn((A + 1, H), generator=g, device="cuda") * 0.1).to(torch.bfloat16)
+    bias = torch.randn(A + 1, generator=g, device="cuda") * 0.1
+    sets = []
+    for _ in range(2):
+        h = torch.randn((T, B, H), generator=g, device="cuda").to(torch.bfloat16)
+        z, _v = pkg.output_layer(h, w, bias)
+        mu = (z + 0.3 * torch.randn(z.shape, generator=g, device="cuda")).contiguous()
+        u = torch.rand(mu.shape, generator=g, device="cuda").clamp_(min=1e-12)
+        act = torch.argmax(mu - torch.log(-torch.log(u)), dim=-1).to(torch.int32).contiguous()
+        done = torch.rand((T, B), generator=g, device="cuda") < 0.01
+        disc = torch.where(done, 0.0, 0.99).to(torch.float32).contiguous()
+        rew = torch.randn((T, B), generator=g, device="cuda").contiguous()
+        boot = torch.randn(B, generator=g, device="cuda")
+        sets.append((h, mu, act, disc, rew, boot))
+        del z, _v, u
+    torch.cuda.empty_cache()
+    ws = pkg.HeadWorkspace(T, B, H, A)
+    out = {"grad_hidden": torch.empty((T, B, H), dtype=torch.bfloat16, device="cuda"),
+           "grad_w_t": torch.empty((A + 1, H), device="cuda"),
+           "grad_bias": torch.empty(A + 1, device="cuda"),
+           "partials": torch.empty(8, dtype=torch.float64, device="cuda")}
+    kw = dict(rho_bar=1.0, c_bar=1.0, baseline_cost=0.5, entropy_cost=0.01, workspace=ws, out=out)
+
+    def step(i):
+        h, mu, act, disc, rew, boot = sets[i % 2]
+        pkg.head_loss_and_grad(h, w, bias, mu, act, disc, rew, boot, **kw)
+
+    s_main = torch.cuda.Stream()
+    K, W = args.steps, max(args.warmup, 3)
+    with torch.cuda.stream(s_main):
+        for i in range(W):
+            step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    tw0 = time.time()
+    e0.record(s_main)
+    with torch.cuda.stream(s_main):
+        for i in range(K):
+            step(i)
+    e1.record(s_main)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if sampler:
+        sampler.stop()
+    barrier(world)
+    step_ms = max_over_ranks(e0.elapsed_time(e1), world) / K
+    e2e = None
+    if not args.no_e2e:  # the step's inputs from pinned host memory, the partials back
+        host = [t.cpu().pin_memory() for t in sets[0]]
+        p_host = torch.empty(8, dtype=torch.float64).pin_memory()
+        Ke = min(K, 10)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s_main)
+        with torch.cuda.stream(s_main):
+            for i in range(Ke):
+                for dst, src in zip(sets[0], host):
+                    dst.copy_(src, non_blocking=True)
+                step(0)
+                p_host.copy_(out["partials"], non_blocking=True)
+        a1.record(s_main)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(a0.elapsed_time(a1), world) / Ke
+        e2e = {"value": world * M / (e2e_ms * 1e-3), "unit": "trajectory-steps/s",
+               "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in host),
+               "d2h_bytes_per_step": 64, "ms_per_step": e2e_ms}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import numpy as np
+        import oracle
+        from oracle import output_layer_oracle as ol
+        cols = 64
+        h, mu, act, disc, rew, boot = sets[0]
+        inp = dict(T=T, B=cols, A=A, dtype=oracle.DTYPE_F32,
+                   target_logits=np.zeros((T, cols, A), np.float32),
+                   behaviour_logits=mu[:, :cols].cpu().numpy(),
+                   actions=act[:, :cols].cpu().numpy(), rewards=rew[:, :cols].cpu().numpy(),
+                   values=np.zeros((T, cols), np.float32),
+                   bootstrap_value=boot[:cols].cpu().numpy(),
+                   discounts=disc[:, :cols].cpu().numpy())
+        hh = h[:, :cols].float().cpu().numpy().astype(np.float64)
+        Wn = w.float().cpu().numpy().astype(np.float64).T
+        bn = bias.cpu().numpy().astype(np.float64)
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < min(args.cpu_seconds, 5.0) or reps == 0:
+            ol.loss_and_grad_from_hidden(inp, hh, Wn, bn, baseline_cost=0.5, entropy_cost=0.01)
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        cpu = {"value": T * cols / dt, "unit": "trajectory-steps/s",
+               "cores": torch.get_num_threads(), "kind": "oracle",
+               "sample": f"{reps} x oracle.output_layer_oracle.loss_and_grad_from_hidden on "
+                         f"trajectories [0, {cols}) x T={T}"}
+    if rank != 0:
+        return
+    peak, peak_src = load_peak()
+    # algorithmic bytes per call: h read + dh write (bf16), behaviour logits (fp32), a, r,
+    # gamma, bootstrap, W^T, bias; grad_w_t, grad_bias, partials
+    alg = (2 * M * H * 2 + M * A * 4 + 3 * M * 4 + B * 4 + (A + 1) * H * 2 + (A + 1) * 4
+           + (A + 1) * H * 4 + (A + 1) * 4 + 64)
+    # the same work unfused: the head forward writes z^pi, V (fp32), the path reads them
+    # back with the behaviour logits and writes dz, dV, the backward reads dZ and h again
+    unfused = (M * H * 2 + M * (A + 1) * 4                      # head forward
+               + M * (A + 1) * 4 + M * A * 4 + 3 * M * 4 + M * (A + 1) * 4  # V-trace path
+               + M * (A + 1) * 4 + M * H * 2 + M * H * 2)          # dh, dW (reads dZ, h)
+    achieved = alg / (step_ms * 1e-3) / 1e9
+    line = {
+        "metric": "fused head + V-trace + loss + grad + head backward trajectory-steps/s",
+        "value": world * M / (step_ms * 1e-3), "unit": "trajectory-steps/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 h, W; f32 accumulate (tcgen05); f32 path; bf16 hi+lo dZ backward",
+        "path": "head_fused",
+        "data": "synthetic (seeded N(0,1) hidden, N(0,0.01) weights, behaviour = z + N(0,0.3^2))",
+        "config": {"workload": "head + path at large: T=100 B=8192 H=256 A=18",
+                   "parallelism": f"dp{world}", "collective": "none",
+                   "l2": "h (419 MB per copy, 2 copies alternated) exceeds L2", "timing": "eager",
+                   "fused_bytes_per_call": alg, "unfused_bytes_per_call": unfused},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": load_traffic("head_fused:large"),
+                     "kernel": "head_fused_kernel + head_reduce_kernel",
+                     "kernel_ms": step_ms, "algorithmic_bytes_per_launch": alg,
+                     "peak_source": peak_src},
+        "gpu_launches": 2 * K,
+        "clocks": sampler.summary(tw0, tw1) if sampler else None,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def spawn_ranks(args) -> int:
     """--gpus N without a launcher: start the N ranks with torch.distributed.run on
     127.0.0.1 (one process per GPU) and return their exit status."""
@@ -953,7 +1108,13 @@ if __name__ == "__main__":
         import faulthandler
         faulthandler.dump_traceback_later(float(os.environ["VT_BENCH_WATCHDOG"]), exit=True)
     try:
-        if a.path == "head":
+        if a.path == "head_fused":
+            if a.impl == "reference":
+                print(json.dumps({"impl": "reference", "path": "head_fused", "unavailable":
+                                  "the fused head's CPU baseline is in the ours line"}))
+            else:
+                run_head_fused(a)
+        elif a.path == "head":
             if a.impl == "reference":
                 print(json.dumps({"impl": "reference", "path": "head", "unavailable":
                                   "the head path's CPU baseline is in the ours line"}))

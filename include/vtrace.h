@@ -326,6 +326,31 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
                                        void* workspace, size_t workspace_bytes,
                                        vt_stream_t stream);
 
+/* ---- SURVEY.md 8(a) a13 over NVLink peer memory ----
+ * The sum of the synchronous learners' partials (every learner computes the
+ * loss of its own trajectories and the losses add, summed loss P:789) in one 32-thread
+ * kernel per step instead of a collective-library call: learner `self` stores its
+ * VT_P_COUNT partials (value, then a call tag with release semantics) into its slot of
+ * every learner's mailbox, waits until every learner's slot of this call has landed in
+ * its own mailbox, and adds them in learner order (bitwise identical on every learner).
+ *   partials      double[VT_P_COUNT] device, 8-byte aligned: this learner's partials
+ *   mailboxes     host array of num_learners device pointers (16-byte aligned): learner
+ *                 j's mailbox of vtrace_partials_mailbox_bytes(num_learners) bytes,
+ *                 zero-initialised once, reachable from this GPU (peer-mapped, e.g.
+ *                 symmetric memory over NVLink); mailboxes[self] is this learner's own
+ *   num_learners  1..16;  self  0..num_learners-1
+ *   counter       device uint64, zero-initialised once: this learner's call count
+ *   out           double[VT_P_COUNT] device: the sum over learners (may alias partials)
+ * Every learner must make the same sequence of calls; a learner that does not call
+ * leaves the others waiting inside the kernel (as with any collective) -- for at most
+ * 20 s, after which the missing learner's terms read as NaN (no hang).  Errors:
+ * VT_ERR_INVALID_ARG (NULL pointer, num_learners or self out of range),
+ * VT_ERR_ALIGNMENT, VT_ERR_DEVICE, VT_ERR_CUDA.  One launch on `stream`; capturable. */
+size_t vtrace_partials_mailbox_bytes(int32_t num_learners);
+vt_status vtrace_partials_allreduce(const double* partials, double* const* mailboxes,
+                                   int32_t num_learners, int32_t self, uint64_t* counter,
+                                   double* out, vt_stream_t stream);
+
 /* ---- NEXT #3, first half: the output layer in front of the path ----
  * [z^pi | V] = h W + b over all M = T*B time-folded steps (time folded into the
  * batch; Fig. 3: linear policy and baseline heads on the LSTM output; DESIGN.md
@@ -346,6 +371,44 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
 vt_status vtrace_output_layer(int64_t M, int32_t H, int32_t A, const void* hidden,
                               const void* w_t, const float* bias, float* logits_out,
                               float* values_out, vt_stream_t stream);
+
+/* ---- NEXT #3, second half: the head fused with the whole path and its backward ----
+ * One call = the learner's output layer over all T*B folded steps (Fig. 3:
+ * [z^pi | V] = h W + b, reading r12), the V-trace targets, loss and gradients of
+ * Section 4 (summed over the batch P:789) as the GEMM's
+ * epilogue -- z^pi and V never reach HBM -- and the head's backward on the same tile:
+ *   dZ = [dL/dz^pi | dL/dV]  (the vtrace_loss_and_grad gradients of that z^pi and V)
+ *   grad_hidden = dZ W^T,  grad_w_t = dZ^T h  (= (h^T dZ)^T),  grad_bias = sum_rows dZ.
+ *   T, B        unroll length and trajectories; B a multiple of 4
+ *   H, A        hidden width 128 or 256; actions A in {3, 4, 6, 9, 18}
+ *   hidden      h [T][B][H] bf16 device (time-major, row t*B + b), 16-byte aligned
+ *   w_t         W^T [A+1][H] bf16 device (rows 0..A-1 the policy logits, row A the baseline)
+ *   bias        b [A+1] fp32 device, or NULL
+ *   behaviour_logits  z^mu [T][B][A] fp32 device (the actors' policy)
+ *   actions, discounts, rewards  [T][B] (int32 / fp32 / fp32), bootstrap_value [B] fp32
+ *               (as vtrace_loss_and_grad; 16-byte aligned except bootstrap_value)
+ *   params, weights   as vtrace_loss_and_grad (behaviour_log_probs must be 0;
+ *               overlap_previous, kernel and sm_budget are ignored)
+ * Outputs (caller-owned, device): grad_hidden [T][B][H] bf16 (round-to-nearest-even of
+ *   the fp32 product of dZ, carried as bf16 hi + lo, with W), grad_w_t [A+1][H] fp32,
+ *   grad_bias [A+1] fp32, partials [VT_P_COUNT] double (as vtrace_loss_and_grad).
+ * Precision: z^pi, V are fp32 tensor-core accumulations of the bf16 h and W; the path
+ * then runs as in vtrace_loss_and_grad with fp32 logits; dZ enters both backward
+ * products as two bf16 terms (hi + lo: 2^-17 relative), accumulated in fp32, the
+ * per-CTA partials of grad_w_t / grad_bias added in fp64 in a fixed order
+ * (deterministic).  workspace: vtrace_head_workspace_bytes(T, B, H, A) bytes,
+ * 256-byte aligned, no initialisation.  Errors: VT_ERR_INVALID_ARG (NULL pointer),
+ * VT_ERR_SHAPE (T, B, H, A out of range), VT_ERR_PARAM, VT_ERR_ALIGNMENT,
+ * VT_ERR_WORKSPACE, VT_ERR_DEVICE, VT_ERR_CUDA.  Two launches on `stream` (the fused
+ * persistent kernel, then the fixed-order sum of its per-CTA partials); capturable. */
+size_t vtrace_head_workspace_bytes(int64_t T, int64_t B, int32_t H, int32_t A);
+vt_status vtrace_head_loss_and_grad(
+    int64_t T, int64_t B, int32_t H, int32_t A, const void* hidden, const void* w_t,
+    const float* bias, const float* behaviour_logits, const int32_t* actions,
+    const float* discounts, const float* rewards, const float* bootstrap_value,
+    const vt_vtrace_params* params, const vt_loss_weights* weights, void* grad_hidden,
+    float* grad_w_t, float* grad_bias, double* partials, void* workspace,
+    size_t workspace_bytes, vt_stream_t stream);
 
 #ifdef __cplusplus
 }

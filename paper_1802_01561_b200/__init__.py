@@ -7,8 +7,9 @@ fallback.
 """
 from . import workload  # noqa: F401
 from .vtrace import (  # noqa: F401
-    RmspropWorkspace, VtraceError, Workspace, from_logits, kernel_for, load_library, loss_and_grad,
-    loss_and_grad_from_host, output_layer, read_device_status, rmsprop_step, status_string,
+    HeadWorkspace, RmspropWorkspace, VtraceError, Workspace, from_logits, head_loss_and_grad,
+    kernel_for, load_library, loss_and_grad, loss_and_grad_from_host, output_layer,
+    partials_allreduce, partials_mailbox_bytes, read_device_status, rmsprop_step, status_string,
     tensors_from_workload, version, workspace_bytes)
 
 __version__ = "0.1.0"

@@ -1,8 +1,9 @@
 """Builds libvtrace.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-Five objects (the look-back kernel + the C ABI; the column-block kernels for bf16
-and for fp32 logits; the learner update; the tcgen05 output layer) are compiled in parallel and linked into
-one shared library.
+Seven objects (the look-back kernel + the C ABI; the column-block kernels for bf16
+and for fp32 logits; the learner update; the tcgen05 output layer; the learners' partials
+sum over NVLink; the head fused with the path and its backward) are compiled in parallel
+and linked into one shared library.
 """
 from __future__ import annotations
 
@@ -16,13 +17,16 @@ ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libvtrace.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(CSRC, "vtrace_api.cu"), os.path.join(CSRC, "vtrace_cb_launch.cu"),
-           os.path.join(CSRC, "learner_update.cu"), os.path.join(CSRC, "output_layer.cu")]
+           os.path.join(CSRC, "learner_update.cu"), os.path.join(CSRC, "output_layer.cu"),
+           os.path.join(CSRC, "partials_allreduce.cu"), os.path.join(CSRC, "head_fused.cu")]
 # (source, object, defines): the column-block unit is compiled once per logits dtype
 UNITS = [(SOURCES[0], "vtrace_api.o", []),
          (SOURCES[1], "vtrace_cb_bf16.o", ["-DVT_CB_PART=0"]),
          (SOURCES[1], "vtrace_cb_f32.o", ["-DVT_CB_PART=1"]),
          (SOURCES[2], "learner_update.o", []),
-         (SOURCES[3], "output_layer.o", [])]
+         (SOURCES[3], "output_layer.o", []),
+         (SOURCES[4], "partials_allreduce.o", []),
+         (SOURCES[5], "head_fused.o", [])]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

@@ -102,11 +102,18 @@ class LearnerStep:
                   previous step's outputs).
     reserve_sms:  SMs the kernel leaves free at N > 1 so that step k's collective
                   is not queued behind step k+1's CTAs (default 1).
+    collective:   how the partials are summed over the learners at N > 1 on GPUs:
+                  "nvlink" (default) -- vtrace_partials_allreduce, one 32-thread kernel
+                  that exchanges the 64 bytes through peer-mapped mailboxes in
+                  symmetric memory; "nccl" -- torch.distributed.all_reduce.
+    A step's kernel never overwrites a partials buffer whose previous collective is
+    still pending: it waits for that collective's event (with buffers rotated over R
+    sets, the collective of R steps ago).
     """
 
     def __init__(self, T: int, B: int, A: int, logits_dtype, *, device=None, group=None,
                  overlap: bool = True, reserve_sms: int | None = None,
-                 kernel: Callable | None = None, **method_kw):
+                 kernel: Callable | None = None, collective: str = "nvlink", **method_kw):
         self.T, self.B, self.A = int(T), int(B), int(A)
         self.group = group
         self.world, self.rank = _world(group)
@@ -133,6 +140,30 @@ class LearnerStep:
             self.comm_stream = torch.cuda.Stream(self.device)
         else:
             self.stream = self.comm_stream = None
+        if collective not in ("nvlink", "nccl"):
+            raise ValueError("collective must be 'nvlink' or 'nccl'")
+        self.collective = collective if (self.cuda and self.world > 1) else "none"
+        self._pending: dict = {}  # partials data_ptr -> event after its collective
+        if self.collective == "nvlink":
+            self._setup_mailboxes()
+
+    def _setup_mailboxes(self):
+        """Every learner's mailbox in symmetric memory (peer-mapped over NVLink)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import vtrace
+        nbytes = vtrace.partials_mailbox_bytes(self.world)
+        if nbytes <= 0:
+            raise ValueError(f"collective='nvlink' supports up to 16 learners, not {self.world}")
+        with torch.cuda.device(self.device):
+            self._mbox = symm_mem.empty(nbytes // 8, dtype=torch.float64, device=self.device)
+            self._mbox.zero_()
+            name = (self.group or dist.group.WORLD).group_name
+            hdl = symm_mem.rendezvous(self._mbox, name)
+            self._mbox_ptrs = [int(p) for p in hdl.buffer_ptrs]
+            self._counter = torch.zeros(1, dtype=torch.int64, device=self.device)
+            torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
 
     def _launch(self, inputs: dict, out: dict):
         from .vtrace import INPUT_NAMES
@@ -145,17 +176,30 @@ class LearnerStep:
             self._launch(inputs, out)
             allreduce_partials(out["partials"], self.group)
             return
+        key = out["partials"].data_ptr()
+        ev = self._pending.pop(key, None)
+        if ev is not None:  # that buffer's previous collective must have read it
+            self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
             self._launch(inputs, out)
         if self.world > 1:
             self.comm_stream.wait_stream(self.stream)
             with torch.cuda.stream(self.comm_stream):
-                allreduce_partials(out["partials"], self.group)
+                if self.collective == "nvlink":
+                    from . import vtrace
+                    vtrace.partials_allreduce(out["partials"], self._mbox_ptrs, self.rank,
+                                              self._counter)
+                else:
+                    allreduce_partials(out["partials"], self.group)
+                ev = torch.cuda.Event()
+                ev.record(self.comm_stream)
+            self._pending[key] = ev
 
     def join(self):
         """The main stream waits for the outstanding collectives."""
         if self.cuda and self.world > 1:
             self.stream.wait_stream(self.comm_stream)
+            self._pending.clear()
 
     def run(self, batches: Sequence[tuple[dict, dict]]):
         """Enqueue the steps over (inputs, out) pairs, then join."""
@@ -170,6 +214,7 @@ class LearnerStep:
         if not self.cuda:
             raise RuntimeError("graph capture needs a CUDA device")
         g = torch.cuda.CUDAGraph()
+        self.join()  # no event of an eager step may be waited on inside the capture
         with torch.cuda.graph(g, stream=self.stream):
-            self.run(batches)
+            self.run(batches)  # (ends with join: no captured event leaks out)
         return g

@@ -36,7 +36,9 @@ EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_f
                     "vtrace_read_device_status", "vtrace_status_string", "vtrace_version",
                     "vtrace_kernel_for", "vtrace_rmsprop_workspace_bytes", "vtrace_rmsprop_step",
                     "vtrace_rmsprop_step_multi", "vtrace_rmsprop_step_learners",
-                    "vtrace_output_layer")
+                    "vtrace_output_layer", "vtrace_partials_mailbox_bytes",
+                    "vtrace_partials_allreduce", "vtrace_head_workspace_bytes",
+                    "vtrace_head_loss_and_grad")
 
 
 class VtraceError(RuntimeError):
@@ -123,6 +125,16 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_rmsprop_step_learners.restype = ctypes.c_int
     lib.vtrace_output_layer.argtypes = [i64, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P]
     lib.vtrace_output_layer.restype = ctypes.c_int
+    lib.vtrace_partials_mailbox_bytes.argtypes = [ctypes.c_int32]
+    lib.vtrace_partials_mailbox_bytes.restype = ctypes.c_size_t
+    lib.vtrace_partials_allreduce.argtypes = [P, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                              ctypes.c_int32, P, P, P]
+    lib.vtrace_partials_allreduce.restype = ctypes.c_int
+    lib.vtrace_head_workspace_bytes.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_int32]
+    lib.vtrace_head_workspace_bytes.restype = ctypes.c_size_t
+    lib.vtrace_head_loss_and_grad.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_int32] + [P] * 8 + [
+        ctypes.POINTER(_Params), ctypes.POINTER(_Weights)] + [P] * 5 + [ctypes.c_size_t, P]
+    lib.vtrace_head_loss_and_grad.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -552,3 +564,106 @@ def output_layer(hidden: torch.Tensor, w_t: torch.Tensor, bias: torch.Tensor | N
                                             _ptr(logits_out), _ptr(values_out), _stream(dev))
     _check(st, "vtrace_output_layer")
     return logits_out, values_out
+
+
+# ---- a13 over NVLink peer memory (include/vtrace.h vtrace_partials_allreduce) ----
+
+def partials_mailbox_bytes(num_learners: int) -> int:
+    """Bytes of one learner's mailbox for vtrace_partials_allreduce (0: out of range)."""
+    return int(load_library().vtrace_partials_mailbox_bytes(int(num_learners)))
+
+
+def partials_allreduce(partials: torch.Tensor, mailbox_ptrs, self_index: int,
+                       counter: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Sum of the learners' [8] fp64 partials over NVLink peer memory (row a13):
+    ``mailbox_ptrs`` are the learners' mailbox device pointers (zero-initialised once,
+    peer-mapped, e.g. symmetric memory), ``counter`` this learner's int64 call counter
+    (zero-initialised once).  Every learner makes the same sequence of calls; the sums
+    are bitwise identical.  Marshalling only: the kernel does the exchange."""
+    if partials.dtype != torch.float64 or partials.numel() != 8 or not partials.is_contiguous():
+        raise ValueError("partials_allreduce: partials must be a contiguous float64 tensor of 8")
+    if counter.dtype != torch.int64 or counter.numel() != 1 or counter.device != partials.device:
+        raise ValueError("partials_allreduce: counter must be one int64 on partials' device")
+    if out is None:
+        out = partials
+    elif out.dtype != torch.float64 or out.numel() != 8 or not out.is_contiguous() or \
+            out.device != partials.device:
+        raise ValueError("partials_allreduce: out must be a contiguous float64 tensor of 8")
+    ptrs = [int(p) for p in mailbox_ptrs]
+    arr = _ptr_array(ptrs)
+    st = load_library().vtrace_partials_allreduce(_ptr(partials), arr, len(ptrs), int(self_index),
+                                                  _ptr(counter), _ptr(out),
+                                                  _stream(partials.device))
+    _check(st, "vtrace_partials_allreduce")
+    return out
+
+
+# ---- NEXT #3 second half: the head fused with the path and its backward ----
+
+class HeadWorkspace:
+    """Device scratch of vtrace_head_loss_and_grad (per-CTA partials; no init needed)."""
+
+    def __init__(self, T: int, B: int, H: int, A: int, device=None):
+        self.nbytes = int(load_library().vtrace_head_workspace_bytes(T, B, H, A))
+        if self.nbytes == 0:
+            raise ValueError("head workspace: bad shape")
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8, device=dev)
+        off = (-self.buf.data_ptr()) % 256
+        self.ptr = ctypes.c_void_p(self.buf.data_ptr() + off)
+
+
+def head_loss_and_grad(hidden, w_t, bias, behaviour_logits, actions, discounts, rewards,
+                       bootstrap_value, *, rho_bar=1.0, c_bar=1.0, pg_rho_bar=None,
+                       lambda_=1.0, reward_mode=0, correction=CORRECTION_VTRACE,
+                       epsilon=1e-6, q_from_values=0, baseline_cost=0.5, entropy_cost=0.01,
+                       workspace: HeadWorkspace | None = None, out: dict | None = None):
+    """vtrace_head_loss_and_grad (NEXT #3, P:173-174 + Section 4): the output layer
+    ``[z^pi | V] = h W + b`` with the V-trace loss and gradients as its epilogue and the
+    head's backward.  hidden [T,B,H] bf16, w_t = W^T [A+1,H] bf16, bias [A+1] fp32 or None,
+    behaviour_logits [T,B,A] fp32, actions/discounts/rewards [T,B], bootstrap_value [B].
+    Returns dict grad_hidden [T,B,H] bf16, grad_w_t [A+1,H] fp32, grad_bias [A+1] fp32,
+    partials [8] fp64.  Marshalling only: the two kernels do the work."""
+    lib = load_library()
+    if hidden.dtype != torch.bfloat16 or w_t.dtype != torch.bfloat16:
+        raise TypeError("head_loss_and_grad: hidden and w_t must be bfloat16")
+    if hidden.dim() != 3 or w_t.dim() != 2:
+        raise ValueError("head_loss_and_grad: hidden [T,B,H], w_t [A+1,H]")
+    T, B, H = (int(x) for x in hidden.shape)
+    A = int(w_t.shape[0]) - 1
+    dev = hidden.device
+    if int(w_t.shape[1]) != H:
+        raise ValueError("head_loss_and_grad: w_t must be [A+1, H]")
+    want = {"behaviour_logits": (behaviour_logits, (T, B, A), torch.float32),
+            "actions": (actions, (T, B), torch.int32), "discounts": (discounts, (T, B), torch.float32),
+            "rewards": (rewards, (T, B), torch.float32),
+            "bootstrap_value": (bootstrap_value, (B,), torch.float32)}
+    for name, (t, shp, dt) in want.items():
+        if tuple(t.shape) != shp or t.dtype != dt or t.device != dev:
+            raise ValueError(f"head_loss_and_grad: {name} must be {dt} {shp} on {dev}")
+    _contig(hidden, w_t, behaviour_logits, actions, discounts, rewards, bootstrap_value)
+    if bias is not None:
+        if bias.numel() != A + 1:
+            raise ValueError(f"head_loss_and_grad: bias must have A + 1 = {A + 1} elements")
+        bias = bias.to(device=dev, dtype=torch.float32).contiguous()
+    ws = workspace if workspace is not None else HeadWorkspace(T, B, H, A, dev)
+    if out is None:
+        out = {"grad_hidden": torch.empty_like(hidden),
+               "grad_w_t": torch.empty(A + 1, H, dtype=torch.float32, device=dev),
+               "grad_bias": torch.empty(A + 1, dtype=torch.float32, device=dev),
+               "partials": torch.empty(P_COUNT, dtype=torch.float64, device=dev)}
+    else:
+        _check_out(out, {"grad_hidden": ((T, B, H), torch.bfloat16, True),
+                         "grad_w_t": ((A + 1, H), torch.float32, True),
+                         "grad_bias": ((A + 1,), torch.float32, True),
+                         "partials": ((P_COUNT,), torch.float64, True)}, dev)
+    p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon,
+               q_from_values, 0, 0)
+    w = _Weights(float(baseline_cost), float(entropy_cost))
+    st = lib.vtrace_head_loss_and_grad(
+        T, B, H, A, _ptr(hidden), _ptr(w_t), _ptr(bias), _ptr(behaviour_logits), _ptr(actions),
+        _ptr(discounts), _ptr(rewards), _ptr(bootstrap_value), ctypes.byref(p), ctypes.byref(w),
+        _ptr(out["grad_hidden"]), _ptr(out["grad_w_t"]), _ptr(out["grad_bias"]),
+        _ptr(out["partials"]), ws.ptr, ws.nbytes, _stream(dev))
+    _check(st, "vtrace_head_loss_and_grad")
+    return out

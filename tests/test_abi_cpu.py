@@ -226,3 +226,49 @@ def test_output_layer_host_checks(lib):
     assert f(128, 256, 9, p, p, None, p, None, None) == 1
     assert f(128, 256, 9, ctypes.c_void_p(base + 8), p, None, p, p, None) == 5
     assert f(128, 256, 9, p, ctypes.c_void_p(base + 4), None, p, p, None) == 5
+
+
+def test_partials_allreduce_host_checks(lib):
+    """vtrace_partials_allreduce (row a13 over NVLink) checks its arguments on the host:
+    mailbox size for 1..16 learners; NULL pointers, learner count or index out of range ->
+    VT_ERR_INVALID_ARG; misaligned partials / counter / mailbox -> VT_ERR_ALIGNMENT."""
+    assert lib.vtrace_partials_mailbox_bytes(0) == 0
+    assert lib.vtrace_partials_mailbox_bytes(17) == 0
+    assert lib.vtrace_partials_mailbox_bytes(4) == 2 * 4 * 8 * 16
+    p = ctypes.c_void_p(4096)
+    mb = (ctypes.c_void_p * 2)(8192, 12288)
+    f = lib.vtrace_partials_allreduce
+    assert f(None, mb, 2, 0, p, p, None) == 1
+    assert f(p, None, 2, 0, p, p, None) == 1
+    assert f(p, mb, 0, 0, p, p, None) == 1
+    assert f(p, mb, 2, 2, p, p, None) == 1
+    assert f(p, (ctypes.c_void_p * 2)(8192, None), 2, 0, p, p, None) == 1
+    assert f(ctypes.c_void_p(4100), mb, 2, 0, p, p, None) == 5
+    assert f(p, mb, 2, 0, ctypes.c_void_p(4100), p, None) == 5
+    assert f(p, (ctypes.c_void_p * 2)(8192, 12296), 2, 0, p, p, None) == 5
+
+
+def test_head_loss_and_grad_host_checks(lib):
+    """vtrace_head_loss_and_grad (NEXT #3 second half) validates on the host before any
+    device work: NULL -> 1, H / A / B out of range -> 2, misaligned -> 5, workspace -> 6."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    base = (ctypes.addressof(buf) + 255) & ~255
+    p = ctypes.c_void_p(base)
+    prm = vt.params()
+    w = vt._Weights(0.5, 0.01)
+    f = lib.vtrace_head_loss_and_grad
+    big = lib.vtrace_head_workspace_bytes(10, 8, 256, 18)
+    assert big > 0 and lib.vtrace_head_workspace_bytes(10, 8, 256, 5 + 27) == 0
+
+    def call(T=10, B=8, H=256, A=18, h=p, ws=p, nbytes=big, grad=p):
+        return f(T, B, H, A, h, p, None, p, p, p, p, p, ctypes.byref(prm), ctypes.byref(w),
+                 grad, p, p, p, ws, nbytes, None)
+    assert call(h=None) == 1
+    assert call(grad=None) == 1
+    assert call(H=192) == 2
+    assert call(A=5) == 2
+    assert call(B=6) == 2
+    assert call(T=0) == 2
+    assert call(h=ctypes.c_void_p(base + 8)) == 5
+    assert call(nbytes=16) == 6
+    assert call(ws=None) == 6
