@@ -44,7 +44,13 @@ using namespace vtb200;
 constexpr int TB = 8;            // trajectories per tile
 constexpr int TT = 16;           // steps per tile
 constexpr int BM = TB * TT;      // 128 rows: MMA M and TMEM lanes
-constexpr int NS = 2;            // h stages
+#ifndef HF_NS
+#define HF_NS 2
+#endif
+#ifndef HF_ABLATE
+#define HF_ABLATE 0   // A/B only: 1 = the V-trace epilogue's arithmetic compiled out (dZ = 0)
+#endif
+constexpr int NS = HF_NS;        // h stages
 constexpr int NWARPS = 11;
 constexpr int THREADS = NWARPS * 32;
 constexpr int W_PROD = 8, W_FWD = 9, W_BWD = 10;
@@ -386,6 +392,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) mbar_arrive(&zempty[zb]);
       mbar_wait(&full[s], (uint32_t)(j / NS) & 1u);  // the small tiles of this stage
       const uint8_t* sm = smem + s_sm(s);
+#if HF_ABLATE == 1
+      if (true) {
+        if (j >= 1) mbar_wait(&dzempty, (uint32_t)(j - 1) & 1u);
+        uint8_t* hi = smem + G.o_dz + r * 64;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          *reinterpret_cast<uint4*>(hi + q * 16) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(hi + BM * 64 + q * 16) = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dzfull);
+        continue;
+      }
+#endif
       // z^pi and V of this row (+ bias)
       CbRow<float, A_CT> R;
 #pragma unroll
@@ -583,29 +604,55 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TM_COLS));
 }
 
-// Sum of the CTAs' partials in CTA order: grad_w_t [A+1][H], grad_bias [A+1], partials [8].
-__global__ void head_reduce_kernel(int grid, int A1, int H, const float* __restrict__ w_part,
-                                   const double* __restrict__ db_part,
-                                   const double* __restrict__ l_part, float* grad_w_t,
-                                   float* grad_b, double* partials, double c_v, double c_e) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Sum of the CTAs' partials in a fixed order: grad_w_t [A+1][H], grad_bias [A+1] (blocks
+// 0 .. gridDim.x-2, 32 outputs each) and the 8 loss partials (the last block).  Warp g adds
+// CTAs g, g+8, ... in fp64, then the 8 group sums are added in group order (deterministic,
+// and 8x the memory parallelism of one thread per output).
+__global__ void __launch_bounds__(256) head_reduce_kernel(
+    int grid, int A1, int H, const float* __restrict__ w_part, const double* __restrict__ db_part,
+    const double* __restrict__ l_part, float* grad_w_t, float* grad_b, double* partials,
+    double c_v, double c_e) {
+  __shared__ double acc[8][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int nw = A1 * H;
-  if (i < nw) {
+  const bool loss_block = blockIdx.x == gridDim.x - 1;
+  const int i = blockIdx.x * 32 + lane;
+  // four loads in flight per thread, added in CTA order
+  auto sum = [&](auto load) {
     double x = 0.0;
-    for (int c = 0; c < grid; ++c) x += (double)w_part[(size_t)c * nw + i];
-    grad_w_t[i] = (float)x;
+    for (int c = g; c < grid; c += 32) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (c + 8 * u < grid) ? load(c + 8 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x += v[u];
+    }
+    return x;
+  };
+  double x = 0.0;
+  if (loss_block) {
+    if (lane < NPART) x = sum([&](int c) { return l_part[(size_t)c * NPART + lane]; });
+  } else if (i < nw) {
+    x = sum([&](int c) { return (double)w_part[(size_t)c * nw + i]; });
   } else if (i < nw + A1) {
-    const int n = i - nw;
-    double x = 0.0;
-    for (int c = 0; c < grid; ++c) x += db_part[(size_t)c * 32 + n];
-    grad_b[n] = (float)x;
-  } else if (i == nw + A1) {
-    double x[NPART];
-    for (int k = 0; k < NPART; ++k) x[k] = 0.0;
-    for (int c = 0; c < grid; ++c)
-      for (int k = 0; k < NPART; ++k) x[k] += l_part[(size_t)c * NPART + k];
-    x[VT_P_TOTAL_LOSS] = x[VT_P_PG_LOSS] + c_v * x[VT_P_BASELINE_LOSS] - c_e * x[VT_P_ENTROPY_SUM];
-    for (int k = 0; k < NPART; ++k) partials[k] = x[k];
+    x = sum([&](int c) { return db_part[(size_t)c * 32 + (i - nw)]; });
+  }
+  acc[g][lane] = x;
+  __syncthreads();
+  if (g != 0) return;
+  double y = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) y += acc[q][lane];
+  if (loss_block) {
+    const double pg = __shfl_sync(0xffffffffu, y, VT_P_PG_LOSS);
+    const double bl = __shfl_sync(0xffffffffu, y, VT_P_BASELINE_LOSS);
+    const double en = __shfl_sync(0xffffffffu, y, VT_P_ENTROPY_SUM);
+    if (lane == VT_P_TOTAL_LOSS) y = pg + c_v * bl - c_e * en;
+    if (lane < NPART) partials[lane] = y;
+  } else if (i < nw) {
+    grad_w_t[i] = (float)y;
+  } else if (i < nw + A1) {
+    grad_b[i - nw] = (float)y;
   }
 }
 
@@ -730,6 +777,7 @@ extern "C" vt_status vtrace_head_loss_and_grad(
   if (!encoder()) return VT_ERR_CUDA;
 
   const Layout L = layout(H, A);
+  if (L.smem > 232448 - 4096) return VT_ERR_SHAPE;  // (an A/B build with more stages)
   HfArgs G;
   std::memset(&G, 0, sizeof(G));
   G.T = (int)T;
@@ -812,8 +860,8 @@ extern "C" vt_status vtrace_head_loss_and_grad(
     default: s = launch<18>(G, M, grid, L.smem, cs); break;
   }
   if (s) return s;
-  const int n_out = (A + 1) * H + (A + 1) + 1;
-  head_reduce_kernel<<<(n_out + 255) / 256, 256, 0, cs>>>(grid, A + 1, H, G.w_part, G.db_part,
+  const int n_wb = (A + 1) * H + (A + 1);  // grad_w_t and grad_bias; + one block for the loss
+  head_reduce_kernel<<<(n_wb + 31) / 32 + 1, 256, 0, cs>>>(grid, A + 1, H, G.w_part, G.db_part,
                                                           G.l_part, grad_w_t, grad_bias, partials,
                                                           P.c_v, P.c_e);
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;

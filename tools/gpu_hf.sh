@@ -11,3 +11,7 @@ if grep -q "passed" ${P}_tests.txt && ! grep -q "failed" ${P}_tests.txt; then
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:head_ --csv --log-file ${P}_launches.csv python bench.py --path head_fused --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > ${P}_ncu.log 2>&1
 fi
 tail -4 ${P}_tests.txt; cat ${P}_bench.json 2>/dev/null | cut -c1-600
+if [ -n "$FULL" ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:head_fused -s 3 -c 1 -o ${P}_prof python bench.py --path head_fused --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > ${P}_ncufull.log 2>&1
+  echo "ncu rc=$?" >> ${P}_ncufull.log
+fi
