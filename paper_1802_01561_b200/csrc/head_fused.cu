@@ -151,6 +151,28 @@ __device__ __forceinline__ void scan_level16(double& G, double& D, int o) {
       : "r"(o));
 }
 
+#ifndef HF_WAIT
+#define HF_WAIT 0   // 0: try_wait loop; 1: try_wait with a suspend-time hint (HF_HINT ns)
+#endif
+#ifndef HF_HINT
+#define HF_HINT 2000
+#endif
+__device__ __forceinline__ void hf_wait(uint64_t* bar, uint32_t phase) {
+#if HF_WAIT == 1
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITH_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITH_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"((uint32_t)HF_HINT)
+      : "memory");
+#else
+  mbar_wait(bar, phase);
+#endif
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h2);
@@ -222,7 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int q = 0; q < KB; ++q) tma_load_2d(smem + G.o_w + q * 4096, &M.w, q * 64, 0, &wbar);
       for (int j = 0; j < ntiles; ++j) {
         const int s = j % NS;
-        if (j >= NS) mbar_wait(&sfree[s], (uint32_t)((j / NS) - 1) & 1u);
+        if (j >= NS) hf_wait(&sfree[s], (uint32_t)((j / NS) - 1) & 1u);
         int b0, t0;
         tile_of(j, b0, t0);
         mbar_expect_tx(&full[s], G.tx_bytes);
@@ -238,12 +260,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == W_FWD) {
     // ---------------- forward MMA: z = h W^T ----------------
     if (lane == 0 && ntiles > 0) {
-      mbar_wait(&wbar, 0);
+      hf_wait(&wbar, 0);
       const uint32_t id = idesc(BM, 32, false, false);
       for (int j = 0; j < ntiles; ++j) {
         const int s = j % NS, zb = j & 1;
-        mbar_wait(&full[s], (uint32_t)(j / NS) & 1u);
-        if (j >= 2) mbar_wait(&zempty[zb], (uint32_t)((j >> 1) - 1) & 1u);
+        hf_wait(&full[s], (uint32_t)(j / NS) & 1u);
+        if (j >= 2) hf_wait(&zempty[zb], (uint32_t)((j >> 1) - 1) & 1u);
         tc_fence_after();
         const uint32_t hb = s_h(s);
         for (int k = 0; k < KB * 4; ++k) {  // K = 16 per MMA: +32 B inside a 128-byte row
@@ -257,13 +279,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == W_BWD) {
     // ---------------- backward MMAs: dh = dZ W, dW += h^T dZ ----------------
     if (lane == 0 && ntiles > 0) {
-      mbar_wait(&wbar, 0);
+      hf_wait(&wbar, 0);
       const uint32_t id_dh = idesc(BM, G.H, false, true);
       const uint32_t id_dw = idesc(128, 32, true, true);
       for (int j = 0; j < ntiles; ++j) {
         const int s = j % NS;
-        mbar_wait(&dzfull, (uint32_t)j & 1u);
-        if (j >= 1) mbar_wait(&dhempty, (uint32_t)(j - 1) & 1u);
+        hf_wait(&dzfull, (uint32_t)j & 1u);
+        if (j >= 1) hf_wait(&dhempty, (uint32_t)(j - 1) & 1u);
         tc_fence_after();
         // dh [128 x H] = dZ [128 x 32] W [32 x H]; A: dZ rows of 64 B (K-major, 64-byte
         // swizzle, 8-row groups 512 B apart, K = 16 -> +32 B); B: the W^T tile as MN-major
@@ -306,7 +328,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int j = 0; j < ntiles; ++j) {
       int b0, t0;
       tile_of(j, b0, t0);
-      mbar_wait(&dhfull, (uint32_t)j & 1u);
+      hf_wait(&dhfull, (uint32_t)j & 1u);
       tc_fence_after();
       for (int q = 0; q < KB; ++q, ++nst) {
         uint32_t v0[32], v1[32];
@@ -342,7 +364,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     // the CTA's dW partial, after the last tile's backward MMAs: TMEM lane = h row
     if (ntiles > 0) {
-      mbar_wait(&dzempty, (uint32_t)(ntiles - 1) & 1u);
+      hf_wait(&dzempty, (uint32_t)(ntiles - 1) & 1u);
       tc_fence_after();
       for (int half = 0; half < KB / 2; ++half) {
         uint32_t v[32];
@@ -382,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = b0 + bl, t = t0 + tl;
       const bool row_ok = b < B && t < T;
       if (t0 + TT >= T) carry = 0.0;  // a new block starts at its last chunk
-      mbar_wait(&zfull[zb], (uint32_t)(j >> 1) & 1u);
+      hf_wait(&zfull[zb], (uint32_t)(j >> 1) & 1u);
       tc_fence_after();
       uint32_t v[32];
       tmem_ld32(tmem + TM_Z + zb * 32 + ((uint32_t)(warp * 32) << 16), v);
@@ -390,11 +412,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&zempty[zb]);
-      mbar_wait(&full[s], (uint32_t)(j / NS) & 1u);  // the small tiles of this stage
+      hf_wait(&full[s], (uint32_t)(j / NS) & 1u);  // the small tiles of this stage
       const uint8_t* sm = smem + s_sm(s);
 #if HF_ABLATE == 1
       if (true) {
-        if (j >= 1) mbar_wait(&dzempty, (uint32_t)(j - 1) & 1u);
+        if (j >= 1) hf_wait(&dzempty, (uint32_t)(j - 1) & 1u);
         uint8_t* hi = smem + G.o_dz + r * 64;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -535,7 +557,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       // dZ as bf16 hi + lo (K-major rows of 64 B, 64-byte swizzle: 16-byte chunk q of row
       // r at q ^ ((r >> 1) & 3)); the previous tile's backward MMAs must be done with it
-      if (j >= 1) mbar_wait(&dzempty, (uint32_t)(j - 1) & 1u);
+      if (j >= 1) hf_wait(&dzempty, (uint32_t)(j - 1) & 1u);
       {
         uint8_t* hi = smem + G.o_dz + r * 64;
         uint8_t* lo2 = hi + BM * 64;
