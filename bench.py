@@ -1067,10 +1067,10 @@ def run_head_fused(args):
                    "fused_bytes_per_call": alg, "unfused_bytes_per_call": unfused},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic("head_fused:large"),
-                     "kernel": "head_fused_kernel + head_reduce_kernel",
+                     "kernel": "head_fused_kernel",
                      "kernel_ms": step_ms, "algorithmic_bytes_per_launch": alg,
                      "peak_source": peak_src},
-        "gpu_launches": 2 * K,
+        "gpu_launches": K,
         "clocks": sampler.summary(tw0, tw1) if sampler else None,
         "e2e": e2e,
         "cpu_baseline": cpu,

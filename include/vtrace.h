@@ -396,11 +396,13 @@ vt_status vtrace_output_layer(int64_t M, int32_t H, int32_t A, const void* hidde
  * then runs as in vtrace_loss_and_grad with fp32 logits; dZ enters both backward
  * products as two bf16 terms (hi + lo: 2^-17 relative), accumulated in fp32, the
  * per-CTA partials of grad_w_t / grad_bias added in fp64 in a fixed order
- * (deterministic).  workspace: vtrace_head_workspace_bytes(T, B, H, A) bytes,
- * 256-byte aligned, no initialisation.  Errors: VT_ERR_INVALID_ARG (NULL pointer),
+ * (deterministic).  workspace: vtrace_head_workspace_bytes(T, B, H, A) bytes, 256-byte
+ * aligned, zero-initialised once (each call leaves it ready for the next; calls sharing
+ * a workspace must be stream-ordered).  Errors: VT_ERR_INVALID_ARG (NULL pointer),
  * VT_ERR_SHAPE (T, B, H, A out of range), VT_ERR_PARAM, VT_ERR_ALIGNMENT,
- * VT_ERR_WORKSPACE, VT_ERR_DEVICE, VT_ERR_CUDA.  Two launches on `stream` (the fused
- * persistent kernel, then the fixed-order sum of its per-CTA partials); capturable. */
+ * VT_ERR_WORKSPACE, VT_ERR_DEVICE, VT_ERR_CUDA.  One cooperative launch on `stream` (a
+ * persistent grid: the per-CTA partials are summed after an in-kernel grid barrier);
+ * capturable. */
 size_t vtrace_head_workspace_bytes(int64_t T, int64_t B, int32_t H, int32_t A);
 vt_status vtrace_head_loss_and_grad(
     int64_t T, int64_t B, int32_t H, int32_t A, const void* hidden, const void* w_t,

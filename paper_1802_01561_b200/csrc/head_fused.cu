@@ -21,8 +21,9 @@
 //               and dW += h^T [hi|lo] (A = the h tile MN-major, B = dZ MN-major),
 //               accumulated in TMEM over every tile of the CTA
 //   warps 4-7   the dh epilogue: TMEM -> bf16 -> 128-byte-swizzled staging -> TMA store
-// The CTA's dW, db and loss sums go to workspace partials; a second small kernel adds
-// them over CTAs in a fixed order (deterministic).
+// The CTA's dW, db and loss sums go to workspace partials; after a grid barrier (the launch
+// is cooperative) every CTA adds a slice of them over all CTAs in a fixed order
+// (deterministic).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -44,27 +45,29 @@ using namespace vtb200;
 constexpr int TB = 8;            // trajectories per tile
 constexpr int TT = 16;           // steps per tile
 constexpr int BM = TB * TT;      // 128 rows: MMA M and TMEM lanes
-#ifndef HF_NS
-#define HF_NS 2
-#endif
 #ifndef HF_ABLATE
 #define HF_ABLATE 0   // A/B only: 1 = the V-trace epilogue's arithmetic compiled out (dZ = 0)
 #endif
-constexpr int NS = HF_NS;        // h stages
+constexpr int MAX_NS = 4;        // h stages: as many as shared memory holds (2 at H = 256, 3 at 128)
 constexpr int NWARPS = 11;
 constexpr int THREADS = NWARPS * 32;
 constexpr int W_PROD = 8, W_FWD = 9, W_BWD = 10;
 constexpr uint32_t TM_Z = 0, TM_DH = 64, TM_DW = 320, TM_COLS = 512;
 constexpr int NPART = 8;
+constexpr int RSLOT = THREADS / 8;  // outputs per round of the final sum (8 groups of CTAs)
 constexpr uint32_t SW128 = 2, SW64 = 4;  // tcgen05 smem descriptor layout types
 
 struct HfArgs {
-  int T, B, H, A, KB, nblk, nch;
+  int T, B, H, A, KB, nblk, nch, ns;
   const float* bias;  // [A+1] or null
   const float* boot;  // [B]
   float* w_part;      // [grid][A+1][H]
   double* db_part;    // [grid][32]
   double* l_part;     // [grid][8]
+  unsigned* gbar;     // grid barrier {count, generation} (zero-initialised once)
+  float* grad_w_t;    // [A+1][H]
+  float* grad_b;      // [A+1]
+  double* partials;   // [8]
   Params P;           // method parameters (thresholds, lambda, costs, reward mode, correction)
   // dynamic shared memory layout (bytes from the 1024-aligned base)
   uint32_t o_w, o_h, h_stage, o_sm, sm_stage, o_mu, o_a, o_r, o_g, o_dz, o_st;
@@ -178,6 +181,33 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h2);
 }
 
+// Statistics of one behaviour row (fp32 logits in shared memory), the same operations as
+// the column-block kernel's mu half: S_mu with its compensated low part, z^mu_a - m_mu.
+template <int A_CT>
+__device__ __forceinline__ double2 mu_stats(const float* mrow, int a) {
+  constexpr int NP = (A_CT + 1) / 2;
+  constexpr float CORR = 1.3349930e-08f;
+  float2 zm[NP], em[NP], hm, lm, sdm, cwm;
+  cb_load_pairs<float, A_CT>(mrow, zm);
+  const float mm = row_max<NP>(zm);
+  cb_exps<float, A_CT, false>(zm, mm, em, hm, lm, sdm, cwm);
+  const float h0 = hm.x - 1.f, h1 = hm.y - 1.f;
+  const float ss = h0 + h1;
+  const float bb = ss - h0;
+  const float err = (h0 - (ss - bb)) + (h1 - bb);
+  const float sd = sdm.x + sdm.y;
+  const float lo = fmaf(sd, CORR, err + (lm.x + lm.y));
+  float zam = 0.f;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    zam = (2 * k == a) ? zm[k].x : zam;
+    if (2 * k + 1 < A_CT) zam = (2 * k + 1 == a) ? zm[k].y : zam;
+  }
+  const bool finite = isfinite(sd) && isfinite(mm);
+  const double S_m = finite ? (double)ss + (double)lo : __longlong_as_double(0x7ff8000000000000ll);
+  return make_double2(S_m, (double)zam - (double)mm);
+}
+
 // ---------------------------------------------------------------------------
 // The fused kernel
 
@@ -187,7 +217,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  __shared__ __align__(8) uint64_t full[NS], sfree[NS], zfull[2], zempty[2];
+  __shared__ __align__(8) uint64_t full[MAX_NS], sfree[MAX_NS], zfull[2], zempty[2];
+  __shared__ __align__(8) uint64_t mufull[MAX_NS];
+  // the behaviour rows' statistics of a stage (computed by the dh warps one tile ahead):
+  // S_mu (NaN if the row is not finite) and z^mu_a - m_mu, per tile row
+  __shared__ double2 mus[MAX_NS][BM];
   __shared__ __align__(8) uint64_t dzfull, dzempty, dhfull, dhempty, wbar;
   __shared__ uint32_t tmem_base;
   __shared__ double wpart[4][NPART];
@@ -195,7 +229,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ float s_bias[32];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = G.T, B = G.B, A = A_CT, KB = G.KB;
+  const int T = G.T, B = G.B, A = A_CT, KB = G.KB, NS = G.ns;
   // this CTA's tiles: blocks blockIdx.x, +gridDim.x, ...; each block's chunks backwards
   const int my_blocks = G.nblk > (int)blockIdx.x ? (G.nblk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int ntiles = my_blocks * G.nch;
@@ -206,9 +240,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) {
+    for (int i = 0; i < NS; ++i) {  // (NS = G.ns)
       mbar_init(&full[i], 1);
       mbar_init(&sfree[i], 1);
+      mbar_init(&mufull[i], 4);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&zfull[i], 1);
@@ -285,25 +320,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; j < ntiles; ++j) {
         const int s = j % NS;
         hf_wait(&dzfull, (uint32_t)j & 1u);
-        if (j >= 1) hf_wait(&dhempty, (uint32_t)(j - 1) & 1u);
         tc_fence_after();
-        // dh [128 x H] = dZ [128 x 32] W [32 x H]; A: dZ rows of 64 B (K-major, 64-byte
-        // swizzle, 8-row groups 512 B apart, K = 16 -> +32 B); B: the W^T tile as MN-major
-        // (K = head column j = its 128-byte rows, 8-row groups 1024 B apart, K = 16 ->
-        // +2048 B; N = h in 64-element atoms 4096 B apart)
-        for (int p = 0; p < 2; ++p) {
-          const uint32_t dz = p ? s_dzlo : s_dzhi;
-          for (int k = 0; k < 2; ++k) {
-            const uint64_t da = sdesc(dz + k * 32, 16, 512, SW64);
-            const uint64_t db = sdesc(s_w + k * 2048, 4096, 1024, SW128);
-            umma(tmem + TM_DH, da, db, id_dh, (p | k) ? 1u : 0u);
-          }
-        }
-        umma_commit(smem_u32(&dhfull));
         // dW [H x 32] += h^T [H x 128] dZ [128 x 32], per 128-row half of H; A: the h tile
         // as MN-major (K = tile row, 8-row groups 1024 B apart, K = 16 -> +2048 B; M = h in
         // 64-element atoms 16384 B apart); B: dZ as MN-major (N = head column in one
-        // 64-byte atom, 8-row groups 512 B apart, K = 16 -> +1024 B)
+        // 64-byte atom, 8-row groups 512 B apart, K = 16 -> +1024 B).  First: it is the last
+        // reader of the h stage, which goes back to the producer at once.
         const uint32_t hb = s_h(s);
         for (int half = 0; half < KB / 2; ++half) {
           for (int p = 0; p < 2; ++p) {
@@ -315,8 +337,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
-        umma_commit(smem_u32(&dzempty));
         umma_commit(smem_u32(&sfree[s]));
+        // dh [128 x H] = dZ [128 x 32] W [32 x H], once the dh warps have read the previous
+        // tile's; A: dZ rows of 64 B (K-major, 64-byte swizzle, 8-row groups 512 B apart,
+        // K = 16 -> +32 B); B: the W^T tile as MN-major (K = head column j = its 128-byte
+        // rows, 8-row groups 1024 B apart, K = 16 -> +2048 B; N = h in 64-element atoms 4096 B
+        // apart)
+        if (j >= 1) {
+          hf_wait(&dhempty, (uint32_t)(j - 1) & 1u);
+          tc_fence_after();
+        }
+        for (int p = 0; p < 2; ++p) {
+          const uint32_t dz = p ? s_dzlo : s_dzhi;
+          for (int k = 0; k < 2; ++k) {
+            const uint64_t da = sdesc(dz + k * 32, 16, 512, SW64);
+            const uint64_t db = sdesc(s_w + k * 2048, 4096, 1024, SW128);
+            umma(tmem + TM_DH, da, db, id_dh, (p | k) ? 1u : 0u);
+          }
+        }
+        umma_commit(smem_u32(&dhfull));
+        umma_commit(smem_u32(&dzempty));
       }
     }
   } else if (warp >= 4) {
@@ -325,7 +365,27 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r = q4 * 32 + lane;  // tile row = TMEM lane
     const bool leader = (q4 == 0 && lane == 0);
     int nst = 0;  // stores issued (staging buffer = nst & 1)
-    for (int j = 0; j < ntiles; ++j) {
+    const int c = lane >> 4, tl = lane & 15, bl = 2 * q4 + c;  // the V-trace warps' row map
+    for (int jj = 0; jj <= ntiles; ++jj) {
+      if (jj < ntiles) {  // the behaviour statistics of tile jj, ahead of its V-trace warps
+        const int s = jj % NS;
+        hf_wait(&full[s], (uint32_t)(jj / NS) & 1u);
+        const uint8_t* sm = smem + s_sm(s);
+        const float* mrow = reinterpret_cast<const float*>(sm + G.o_mu) +
+                            (((bl >> 2) * TT + tl) * 4 + (bl & 3)) * A_CT;
+        const int a = min(max(reinterpret_cast<const int*>(sm + G.o_a)[tl * TB + bl], 0), A - 1);
+#if HF_ABLATE == 3
+        mus[s][r] = make_double2(1.0, 0.0);
+        (void)mrow;
+        (void)a;
+#else
+        mus[s][r] = mu_stats<A_CT>(mrow, a);
+#endif
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&mufull[s]);
+      }
+      if (jj == 0) continue;
+      const int j = jj - 1;  // the dh epilogue of the previous tile
       int b0, t0;
       tile_of(j, b0, t0);
       hf_wait(&dhfull, (uint32_t)j & 1u);
@@ -340,6 +400,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&dhempty);
         }
+#if HF_ABLATE == 2
+        continue;  // A/B only: no dh output
+#endif
         // the staging buffer's previous store (two atoms ago) must have read it
         if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         named_bar(1, 128);
@@ -394,6 +457,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     float vnext = 0.f;    // V(x) of the step after this chunk
     CbAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0, 0u};
     double db_acc = 0.0;  // lane n: sum of column n of dZ
+    float dsum[A_CT + 1];
+#pragma unroll
+    for (int k = 0; k <= A_CT; ++k) dsum[k] = 0.f;
     float bz[A_CT + 1];
 #pragma unroll
     for (int k = 0; k <= A_CT; ++k) bz[k] = s_bias[k];
@@ -438,9 +504,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         R.z[k] = make_float2(x0, x1);
       }
       const float Vt = __uint_as_float(v[A_CT]) + bz[A_CT];
-      // behaviour row: [seg][t][4 A] floats, seg = 4-trajectory group
-      const float* mrow = reinterpret_cast<const float*>(sm + G.o_mu) +
-                          (((bl >> 2) * TT + tl) * 4 + (bl & 3)) * A_CT;
       const int a_raw = reinterpret_cast<const int*>(sm + G.o_a)[tl * TB + bl];
       const float rt = reinterpret_cast<const float*>(sm + G.o_r)[tl * TB + bl];
       const float gm = reinterpret_cast<const float*>(sm + G.o_g)[tl * TB + bl];
@@ -450,37 +513,31 @@ __global__ void __launch_bounds__(THREADS, 1)
       float Vn = __shfl_down_sync(0xffffffffu, Vt, 1, 16);
       if (tl == TT - 1) Vn = vnext;
       if (t + 1 == T) Vn = (b < B) ? __ldg(G.boot + b) : 0.f;
-      // a3-a7: statistics of both policies (as the column-block kernel, fp32 logits)
+      // a3-a7: statistics of the target row (as the column-block kernel, fp32 logits); the
+      // behaviour row's come from the dh warps (same operations, one tile ahead)
       const float mp = row_max<NP>(R.z);
       float2 hp, lp, sdp, cwp;
       cb_exps<float, A_CT, true>(R.z, mp, R.e, hp, lp, sdp, cwp);
-      float2 zm[NP], em[NP], hm, lm, sdm, cwm;
-      cb_load_pairs<float, A_CT>(mrow, zm);
-      const float mm = row_max<NP>(zm);
-      cb_exps<float, A_CT, false>(zm, mm, em, hm, lm, sdm, cwm);
-      const float2 h0 = __fadd2_rn(make_float2(hp.x, hm.x), f2(-1.f));
-      const float2 h1 = __fadd2_rn(make_float2(hp.y, hm.y), f2(-1.f));
-      const float2 ss = __fadd2_rn(h0, h1);
-      const float2 bb = __fadd2_rn(ss, make_float2(-h0.x, -h0.y));
-      const float2 err = __fadd2_rn(__fadd2_rn(h0, make_float2(bb.x - ss.x, bb.y - ss.y)),
-                                    __fadd2_rn(h1, make_float2(-bb.x, -bb.y)));
-      const float2 sd = make_float2(sdp.x + sdp.y, sdm.x + sdm.y);
-      const float2 lo = __ffma2_rn(sd, f2(CORR), __fadd2_rn(err, __fadd2_rn(make_float2(lp.x, lm.x),
-                                                                             make_float2(lp.y, lm.y))));
-      const double S_p = (double)ss.x + (double)lo.x, S_m = (double)ss.y + (double)lo.y;
-      float zap = 0.f, zam = 0.f;
+      const float h0 = hp.x - 1.f, h1 = hp.y - 1.f;
+      const float ss0 = h0 + h1;
+      const float bb = ss0 - h0;
+      const float err = (h0 - (ss0 - bb)) + (h1 - bb);
+      const float sd0 = sdp.x + sdp.y;
+      const float lo0 = fmaf(sd0, CORR, err + (lp.x + lp.y));
+      const float2 ss = make_float2(ss0, 0.f), lo = make_float2(lo0, 0.f), sd = make_float2(sd0, 0.f);
+      const double S_p = (double)ss0 + (double)lo0;
+      float zap = 0.f;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         zap = (2 * k == a) ? R.z[k].x : zap;
-        zam = (2 * k == a) ? zm[k].x : zam;
-        if (2 * k + 1 < A_CT) {
-          zap = (2 * k + 1 == a) ? R.z[k].y : zap;
-          zam = (2 * k + 1 == a) ? zm[k].y : zam;
-        }
+        if (2 * k + 1 < A_CT) zap = (2 * k + 1 == a) ? R.z[k].y : zap;
       }
-      const double xa_p = (double)zap - (double)mp, xa_m = (double)zam - (double)mm;
+      hf_wait(&mufull[s], (uint32_t)(j / NS) & 1u);
+      const double2 mst = mus[s][r];
+      const double S_m = mst.x, xa_m = mst.y;
+      const double xa_p = (double)zap - (double)mp;
       const float ea_raw = ex2_approx((zap - mp) * L32);
-      const bool finite = isfinite(sd.x) && isfinite(mp) && isfinite(sd.y) && isfinite(mm);
+      const bool finite = isfinite(sd0) && isfinite(mp) && isfinite(S_m);
       // a5, a7: pi(a)/mu(a) = exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) S_mu / S_pi
       const double ratio = exp64(xa_p - xa_m) * ddiv_pos(S_m, S_p);
       const double td = reward_transform(rt, P.reward_mode) + (double)gm * (double)Vn - (double)Vt;
@@ -581,7 +638,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&dzfull);
-      // db: butterfly over the lanes, lane n ends with column n's sum of the warp's rows
+      // db: this lane's running column sums (fp32 over the ~50 tiles of a lane)
+#pragma unroll
+      for (int k = 0; k <= A_CT; ++k) dsum[k] += d[k];
+    }
+    // db: butterfly over the lanes, lane n ends with column n's sum of the warp's rows
+    {
+      float d[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[k] = k <= A_CT ? dsum[k] : 0.f;
 #pragma unroll
       for (int w = 16; w >= 1; w >>= 1) {
         const bool up = (lane & w) != 0;
@@ -592,7 +657,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           d[k] = keep + __shfl_xor_sync(0xffffffffu, send, w);
         }
       }
-      db_acc += (double)d[0];
+      db_acc = (double)d[0];
     }
     // a12: per-lane sums -> warp
     double part[NPART] = {acc.pg, 0.5 * acc.v2, acc.H, 0.0, acc.dz,
@@ -624,57 +689,75 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (warp == W_FWD)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TM_COLS));
-}
 
-// Sum of the CTAs' partials in a fixed order: grad_w_t [A+1][H], grad_bias [A+1] (blocks
-// 0 .. gridDim.x-2, 32 outputs each) and the 8 loss partials (the last block).  Warp g adds
-// CTAs g, g+8, ... in fp64, then the 8 group sums are added in group order (deterministic,
-// and 8x the memory parallelism of one thread per output).
-__global__ void __launch_bounds__(256) head_reduce_kernel(
-    int grid, int A1, int H, const float* __restrict__ w_part, const double* __restrict__ db_part,
-    const double* __restrict__ l_part, float* grad_w_t, float* grad_b, double* partials,
-    double c_v, double c_e) {
-  __shared__ double acc[8][32];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int nw = A1 * H;
-  const bool loss_block = blockIdx.x == gridDim.x - 1;
-  const int i = blockIdx.x * 32 + lane;
-  // four loads in flight per thread, added in CTA order
-  auto sum = [&](auto load) {
+  // ---- the sum of the CTAs' partials: a grid barrier (cooperative launch: every CTA is
+  // resident), then each CTA adds a slice of the outputs over all CTAs in a fixed order ----
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(&G.gbar[1]);
+    if (atomicAdd(&G.gbar[0], 1u) == gridDim.x - 1) {
+      G.gbar[0] = 0u;
+      __threadfence();
+      st_release_u32(&G.gbar[1], gen + 1u);
+    } else {
+      while (ld_acquire_u32(&G.gbar[1]) == gen) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  // (the group sums reuse the behaviour-statistics buffer, idle by now)
+  static_assert(sizeof(double) * 8 * RSLOT <= sizeof(double2) * MAX_NS * BM, "racc fits in mus");
+  double (*racc)[RSLOT] = reinterpret_cast<double (*)[RSLOT]>(&mus[0][0]);
+  const int ncta = gridDim.x, A1 = A + 1, nw = A1 * G.H, nwb = nw + A1;
+  const int chunk = (nwb + ncta - 1) / ncta;
+  const int o_end = min((int)blockIdx.x * chunk + chunk, nwb);
+  const int grp = threadIdx.x / RSLOT, slot = threadIdx.x - grp * RSLOT;
+  auto csum = [&](auto load) {  // CTAs grp, grp + 8, ... (four loads in flight), in order
     double x = 0.0;
-    for (int c = g; c < grid; c += 32) {
+    for (int c = grp; c < ncta; c += 32) {
       double v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (c + 8 * u < grid) ? load(c + 8 * u) : 0.0;
+      for (int u = 0; u < 4; ++u) v[u] = (c + 8 * u < ncta) ? load(c + 8 * u) : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) x += v[u];
     }
     return x;
   };
-  double x = 0.0;
-  if (loss_block) {
-    if (lane < NPART) x = sum([&](int c) { return l_part[(size_t)c * NPART + lane]; });
-  } else if (i < nw) {
-    x = sum([&](int c) { return (double)w_part[(size_t)c * nw + i]; });
-  } else if (i < nw + A1) {
-    x = sum([&](int c) { return db_part[(size_t)c * 32 + (i - nw)]; });
-  }
-  acc[g][lane] = x;
-  __syncthreads();
-  if (g != 0) return;
-  double y = 0.0;
+  for (int base = (int)blockIdx.x * chunk; base < o_end; base += RSLOT) {
+    const int n = min(RSLOT, o_end - base), i = base + slot;
+    double x = 0.0;
+    if (grp < 8 && slot < n) {
+      if (i < nw) x = csum([&](int c) { return (double)__ldcg(G.w_part + (size_t)c * nw + i); });
+      else x = csum([&](int c) { return __ldcg(G.db_part + (size_t)c * 32 + (i - nw)); });
+    }
+    if (grp < 8) racc[grp][slot] = x;
+    __syncthreads();
+    if (threadIdx.x < n) {
+      double y = 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) y += acc[q][lane];
-  if (loss_block) {
-    const double pg = __shfl_sync(0xffffffffu, y, VT_P_PG_LOSS);
-    const double bl = __shfl_sync(0xffffffffu, y, VT_P_BASELINE_LOSS);
-    const double en = __shfl_sync(0xffffffffu, y, VT_P_ENTROPY_SUM);
-    if (lane == VT_P_TOTAL_LOSS) y = pg + c_v * bl - c_e * en;
-    if (lane < NPART) partials[lane] = y;
-  } else if (i < nw) {
-    grad_w_t[i] = (float)y;
-  } else if (i < nw + A1) {
-    grad_b[i - nw] = (float)y;
+      for (int q = 0; q < 8; ++q) y += racc[q][threadIdx.x];
+      const int o = base + threadIdx.x;
+      if (o < nw) G.grad_w_t[o] = (float)y;
+      else G.grad_b[o - nw] = (float)y;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == gridDim.x - 1) {  // the 8 loss partials (and their total)
+    double x = 0.0;
+    if (grp < 8 && slot < NPART)
+      x = csum([&](int c) { return __ldcg(G.l_part + (size_t)c * NPART + slot); });
+    if (grp < 8) racc[grp][slot] = x;
+    __syncthreads();
+    if (warp == 0) {
+      double y = 0.0;
+      if (lane < NPART)
+        for (int q = 0; q < 8; ++q) y += racc[q][lane];
+      const double pg = __shfl_sync(0xffffffffu, y, VT_P_PG_LOSS);
+      const double bl = __shfl_sync(0xffffffffu, y, VT_P_BASELINE_LOSS);
+      const double en = __shfl_sync(0xffffffffu, y, VT_P_ENTROPY_SUM);
+      if (lane == VT_P_TOTAL_LOSS) y = pg + G.P.c_v * bl - G.P.c_e * en;
+      if (lane < NPART) G.partials[lane] = y;
+    }
   }
 }
 
@@ -701,7 +784,7 @@ struct Layout {
   uint32_t o_w, o_h, h_stage, o_sm, sm_stage, o_mu, o_a, o_r, o_g, o_dz, o_st, tx, smem;
 };
 
-Layout layout(int H, int A) {
+Layout layout(int H, int A, int NS) {
   Layout L{};
   const int KB = H / 64;
   auto up = [](uint32_t x, uint32_t a) { return (x + a - 1) / a * a; };
@@ -737,8 +820,17 @@ vt_status launch(const HfArgs& G, const HfMaps& M, int grid, size_t smem, cudaSt
       return VT_ERR_CUDA;
     attr_set.fetch_or(bit);
   }
-  kern<<<grid, THREADS, smem, st>>>(G, M);
-  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // the final sum's grid barrier
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, G, M) == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
 bool encode(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* base, const cuuint64_t* dims,
@@ -754,7 +846,7 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* base, const 
 extern "C" size_t vtrace_head_workspace_bytes(int64_t T, int64_t B, int32_t H, int32_t A) {
   if (T <= 0 || B <= 0 || H <= 0 || A < 1 || A + 1 > 32) return 0;
   const size_t grid = 256;  // upper bound on the persistent grid (SMs per device)
-  return grid * ((size_t)(A + 1) * H * 4 + 32 * 8 + vthf::NPART * 8) + 256;
+  return 256 + grid * ((size_t)(A + 1) * H * 4 + 32 * 8 + vthf::NPART * 8) + 256;
 }
 
 extern "C" vt_status vtrace_head_loss_and_grad(
@@ -798,8 +890,13 @@ extern "C" vt_status vtrace_head_loss_and_grad(
   }
   if (!encoder()) return VT_ERR_CUDA;
 
-  const Layout L = layout(H, A);
-  if (L.smem > 232448 - 4096) return VT_ERR_SHAPE;  // (an A/B build with more stages)
+  // as many h stages as the 227 KB of shared memory hold (the ring depth is what hides the
+  // load latency behind the epilogue: H = 128 runs 3 stages, H = 256 2)
+  constexpr uint32_t kDynMax = 232448 - 12 * 1024;  // 227 KB per CTA minus the static arrays
+  int ns = MAX_NS;
+  while (ns > 2 && layout(H, A, ns).smem > kDynMax) --ns;
+  const Layout L = layout(H, A, ns);
+  if (L.smem > kDynMax) return VT_ERR_SHAPE;
   HfArgs G;
   std::memset(&G, 0, sizeof(G));
   G.T = (int)T;
@@ -809,13 +906,18 @@ extern "C" vt_status vtrace_head_loss_and_grad(
   G.KB = H / 64;
   G.nblk = (int)((B + TB - 1) / TB);
   G.nch = (int)((T + TT - 1) / TT);
+  G.ns = ns;
   const int grid = std::min(std::min(sms, 256), G.nblk);
   G.bias = bias;
   G.boot = bootstrap_value;
   uint8_t* wsb = static_cast<uint8_t*>(workspace);
-  G.w_part = reinterpret_cast<float*>(wsb);
-  G.db_part = reinterpret_cast<double*>(wsb + (size_t)256 * (A + 1) * H * 4);
+  G.gbar = reinterpret_cast<unsigned*>(wsb);
+  G.w_part = reinterpret_cast<float*>(wsb + 256);
+  G.db_part = reinterpret_cast<double*>(wsb + 256 + (size_t)256 * (A + 1) * H * 4);
   G.l_part = G.db_part + (size_t)256 * 32;
+  G.grad_w_t = grad_w_t;
+  G.grad_b = grad_bias;
+  G.partials = partials;
   Params& P = G.P;
   P.T = T; P.B = B; P.A = A; P.T32 = (int)T; P.B32 = (int)B;
   P.rho_bar = (double)params->clip_rho_threshold;
@@ -881,10 +983,5 @@ extern "C" vt_status vtrace_head_loss_and_grad(
     case 9: s = launch<9>(G, M, grid, L.smem, cs); break;
     default: s = launch<18>(G, M, grid, L.smem, cs); break;
   }
-  if (s) return s;
-  const int n_wb = (A + 1) * H + (A + 1);  // grad_w_t and grad_bias; + one block for the loss
-  head_reduce_kernel<<<(n_wb + 31) / 32 + 1, 256, 0, cs>>>(grid, A + 1, H, G.w_part, G.db_part,
-                                                          G.l_part, grad_w_t, grad_bias, partials,
-                                                          P.c_v, P.c_e);
-  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+  return s;
 }

@@ -601,14 +601,15 @@ def partials_allreduce(partials: torch.Tensor, mailbox_ptrs, self_index: int,
 # ---- NEXT #3 second half: the head fused with the path and its backward ----
 
 class HeadWorkspace:
-    """Device scratch of vtrace_head_loss_and_grad (per-CTA partials; no init needed)."""
+    """Device workspace of vtrace_head_loss_and_grad (a grid-barrier word pair and the
+    per-CTA partials): zero-initialised once here, left ready by every call."""
 
     def __init__(self, T: int, B: int, H: int, A: int, device=None):
         self.nbytes = int(load_library().vtrace_head_workspace_bytes(T, B, H, A))
         if self.nbytes == 0:
             raise ValueError("head workspace: bad shape")
         dev = torch.device(device) if device is not None else torch.device("cuda")
-        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8, device=dev)
+        self.buf = torch.zeros(self.nbytes + 256, dtype=torch.uint8, device=dev)
         off = (-self.buf.data_ptr()) % 256
         self.ptr = ctypes.c_void_p(self.buf.data_ptr() + off)
 
