@@ -72,7 +72,7 @@ def parse():
                          "(SURVEY 8(f) NEXT #4: gradient all-reduce at N > 1, global-norm "
                          "clip, RMSProp) instead of the V-trace path; head: the tcgen05 output "
                          "layer [z|V] = hW + b in front of the path (NEXT #3)")
-    ap.add_argument("--update-collective", choices=["symm", "nccl"], default="symm",
+    ap.add_argument("--update-collective", choices=["symm", "symm_sharded", "nccl"], default="symm",
                     help="N > 1 on the update path: symm = the kernel sums every learner's "
                          "gradient over NVLink from symmetric memory (fused); nccl = NCCL "
                          "all_reduce then the single-gradient kernel")
@@ -637,7 +637,8 @@ def run_update(args):
     ws = pkg.RmspropWorkspace(n)
     s_main = torch.cuda.Stream()
 
-    symm = world > 1 and args.update_collective == "symm"
+    symm = world > 1 and args.update_collective in ("symm", "symm_sharded")
+    sharded = world > 1 and args.update_collective == "symm_sharded"
     red = hdl = ptrs = None
     if symm:
         # the learners' gradient buffers in symmetric memory: every GPU maps every
@@ -651,6 +652,20 @@ def run_update(args):
         flg.zero_()
         hdl_f = symm_mem.rendezvous(flg, dist.group.WORLD.group_name)
         fptrs = [int(p) for p in hdl_f.buffer_ptrs]
+        if sharded:
+            # every learner's R parameter copies in one symmetric allocation: a learner
+            # writes its shard of the new theta into all of them (NVLink stores)
+            th_all = symm_mem.empty(R * n, dtype=torch.float32, device="cuda")
+            hdl_t = symm_mem.rendezvous(th_all, dist.group.WORLD.group_name)
+            for j in range(R):
+                th_all[j * n:(j + 1) * n].copy_(theta[j])
+            theta = [th_all[j * n:(j + 1) * n] for j in range(R)]
+            tptrs = [[int(p) + 4 * j * n for p in hdl_t.buffer_ptrs] for j in range(R)]
+            nmb = symm_mem.empty(pkg.vtrace.rmsprop_norm_mailbox_bytes(world) // 8,
+                                 dtype=torch.float64, device="cuda")
+            nmb.zero_()
+            hdl_n = symm_mem.rendezvous(nmb, dist.group.WORLD.group_name)
+            nptrs = [int(p) for p in hdl_n.buffer_ptrs]
         torch.cuda.synchronize()
         barrier(world)
     elif world > 1:
@@ -663,6 +678,12 @@ def run_update(args):
                 # this step's local gradient (the backward's output) -- an SM kernel: a
                 # captured D2D copy_ measured ~70 us per 6.4 MB in graph replay at N = 2
                 torch.mul(grads[j], 1.0, out=red)
+            if sharded:  # this learner's 1/N of the parameters, new theta to every learner
+                pkg.vtrace.rmsprop_step_sharded(tptrs[j], ms[j], ptrs, lr, decay, eps, clip,
+                                                flags=fptrs, norm_mailboxes=nptrs,
+                                                self_index=rank, n=n, workspace=ws,
+                                                global_norm_out=norm)
+                return
             # every learner's buffer summed over NVLink in rank order; ready / done flags
             # inside the kernel replace the barriers around it
             pkg.rmsprop_step(theta[j], ms[j], ptrs, lr, decay, eps, clip,
@@ -742,8 +763,14 @@ def run_update(args):
     # the replicas must agree bitwise (same buffers, same order, same arithmetic)
     replicas_equal = None
     if world > 1:
-        h = torch.tensor([float(torch.sum(theta[0].double())), float(torch.sum(ms[0].double()))],
-                         dtype=torch.float64, device="cuda")
+        # exact checksums of the bits (int64 sums of the fp32 words, two weightings); the
+        # sharded update keeps theta replicated and each learner's own shard of ms
+        def bits(t):
+            w = t.view(torch.int32).long()
+            idx = torch.arange(w.numel(), device=w.device, dtype=torch.int64) % 1009
+            return [int(w.sum()), int((w * idx).sum())]
+        h = torch.tensor(bits(theta[0]) + ([] if sharded else bits(ms[0])), dtype=torch.int64,
+                         device="cuda")
         hs = [torch.zeros_like(h) for _ in range(world)]
         dist.all_gather(hs, h)
         replicas_equal = all(bool(torch.equal(hs[0], x)) for x in hs[1:])
@@ -806,7 +833,12 @@ def run_update(args):
         "config": {"workload": f"learner update, {size} model ({n} parameters)",
                    "n_params": n, "optimizer": "RMSProp momentum 0, decay 0.99, eps 0.01, "
                    "lr 6e-4, clip global norm 40 (P:950-953)",
-                   "collective": ("per step: local gradient into symmetric memory; ONE kernel "
+                   "collective": (("per step: local gradient into symmetric memory; ONE kernel "
+                                   "per learner updates its 1/N shard from every learner's "
+                                   "gradient (NVLink reads), adds the shards' norms through "
+                                   "mailboxes and stores the new theta into every replica "
+                                   "(NVLink writes)") if sharded else
+                                  "per step: local gradient into symmetric memory; ONE kernel "
                                   "syncs the learners (ready/done flags over NVLink), sums "
                                   "every learner's buffer (rank order) and updates" if symm else
                                   "per step: copy of the local fp32 gradient + NCCL all_reduce "

@@ -326,6 +326,33 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
                                        void* workspace, size_t workspace_bytes,
                                        vt_stream_t stream);
 
+/* The learners' update sharded over the learners (a reduce-scatter / all-gather inside
+ * one kernel per learner): learner `self` owns the float4 units
+ * [U*self/N, U*(self+1)/N) of the n parameters (U = n/4; the n % 4 tail belongs to the
+ * last learner).  For its units it sums every learner's gradient (learner order, NVLink
+ * reads), adds its shard's sum of squares to the others' through the peer-mapped norm
+ * mailboxes (learner order: the same norm, bitwise, on every learner), clips, applies
+ * RMSProp to its own mean_square, and stores the new theta into EVERY learner's params
+ * (NVLink stores), so the replicas stay bitwise equal while each learner reads 1/N of
+ * the peers' gradients.  mean_square: each learner's entries outside its shard are not
+ * read or written (each owns its shard's state).
+ *   params          host array of num_learners device pointers, each learner's params
+ *                   (peer-mapped, 16-byte aligned); params[self] is this learner's
+ *   grads, flags    as vtrace_rmsprop_step_learners
+ *   norm_mailboxes  host array of num_learners device pointers: learner j's mailbox of
+ *                   vtrace_rmsprop_norm_mailbox_bytes(num_learners) bytes, zero-initialised
+ *                   once, peer-mapped, 16-byte aligned
+ * Arrays must be 16-byte aligned (else VT_ERR_ALIGNMENT) and a shard must fit the
+ * register-resident form (148 x 512 x 6 float4 units; else VT_ERR_SHAPE).  Other errors
+ * and the call discipline as vtrace_rmsprop_step_learners. */
+size_t vtrace_rmsprop_norm_mailbox_bytes(int32_t num_learners);
+vt_status vtrace_rmsprop_step_sharded(int64_t n, float* const* params, float* mean_square,
+                                      const float* const* grads, uint32_t* const* flags,
+                                      double* const* norm_mailboxes, int32_t num_learners,
+                                      int32_t self, const vt_rmsprop_params* prm,
+                                      double* global_norm_out, void* workspace,
+                                      size_t workspace_bytes, vt_stream_t stream);
+
 /* ---- SURVEY.md 8(a) a13 over NVLink peer memory ----
  * The sum of the synchronous learners' partials (every learner computes the
  * loss of its own trajectories and the losses add, summed loss P:789) in one 32-thread

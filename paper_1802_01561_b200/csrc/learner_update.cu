@@ -48,6 +48,11 @@ struct RmsHeader {  // workspace bytes [0, 16); vtrace_workspace_init zeroes the
 static_assert(sizeof(RmsHeader) <= offsetof(vtb200::WsHeader, status),
               "RmsHeader overlaps the status word vtrace_workspace_init sets to ~0");
 
+struct NormSlot {  // a learner's shard sum of squares and the call tag that published it
+  double v;
+  unsigned long long tag;
+};
+
 struct RmsArgs {
   long long n;
   float* theta;
@@ -59,6 +64,14 @@ struct RmsArgs {
   float lr, decay, eps, clip;
   double* norm_out;
   unsigned char* ws;
+  // sharded learners (vtrace_rmsprop_step_sharded): this learner updates float4 units
+  // [u0, u1) only, writes the new theta of that range into every learner's params, and the
+  // learners add their shards' sums of squares through peer-mapped mailboxes
+  long long u0, u1;                     // (non-sharded: 0, n / 4)
+  int sharded;
+  int tail_owner;                       // this learner updates the n % 4 tail
+  float* peer_theta[RMS_MAX_GRADS];     // every learner's params (sharded)
+  NormSlot* nmail[RMS_MAX_GRADS];       // every learner's norm mailbox [2][ng]
 };
 
 // The gradient element i: the sum of the ng buffers in index order (fp32), so every
@@ -220,8 +233,49 @@ __device__ __forceinline__ double grid_norm(double ss, const RmsArgs& a, unsigne
       hdr->epoch = epoch + 1u;
     }
   }
-  const double norm = sqrt(s_total);
-  if (cta == 0 && tid == 0 && a.norm_out) *a.norm_out = norm;
+  return s_total;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ||g||_2 of the whole gradient: this learner's sum of squares (grid_norm), and, when the
+// learners shard the parameters, the sum of every learner's shard sum in learner order
+// (mailbox slots [parity][learner] in peer memory, value then tag with release
+// semantics; every CTA reads its own learner's mailbox) -- bitwise the same everywhere.
+__device__ __forceinline__ double global_norm(double ss, const RmsArgs& a, unsigned int epoch) {
+  double tot = grid_norm(ss, a, epoch);
+  if (a.sharded) {
+    __shared__ double s_all;
+    const unsigned long long tag = (unsigned long long)epoch + 1ull;
+    const int par = (int)(tag & 1ull);
+    if (threadIdx.x == 0) {
+      if (blockIdx.x == 0) {
+        for (int r = 0; r < a.ng; ++r) {
+          NormSlot* d = a.nmail[r] + (par * a.ng + a.self);
+          asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(&d->v), "d"(tot) : "memory");
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&d->tag), "l"(tag) : "memory");
+        }
+      }
+      double x = 0.0;
+      const NormSlot* own = a.nmail[a.self] + par * a.ng;
+      for (int r = 0; r < a.ng; ++r) {
+        while (ld_acquire_sys64(&own[r].tag) != tag) {
+        }
+        double v;
+        asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(&own[r].v) : "memory");
+        x += v;
+      }
+      s_all = x;
+    }
+    __syncthreads();
+    tot = s_all;
+  }
+  const double norm = sqrt(tot);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.norm_out) *a.norm_out = norm;
   return norm;
 }
 
@@ -234,9 +288,10 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
   const int tid = threadIdx.x;
   const int G = gridDim.x * RMS_THREADS;  // (32-bit: units <= 148 x 512 x 6 here)
   const int gt = blockIdx.x * RMS_THREADS + tid;
-  const int units = (int)(a.n / 4);
-  float4* t4 = reinterpret_cast<float4*>(a.theta);
-  float4* m4 = reinterpret_cast<float4*>(a.ms);
+  // this learner's float4 units [u0, u1) (all of them unless the learners shard)
+  const int units = (int)(a.u1 - a.u0);
+  float4* t4 = reinterpret_cast<float4*>(a.theta) + a.u0;
+  float4* m4 = reinterpret_cast<float4*>(a.ms) + a.u0;
   const unsigned int e = rms_epoch(a);
   peers_ready(a, e);
   float4 gv[V], th[V], m[V];
@@ -246,11 +301,11 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     const int i = gt + k * G;
-    gv[k] = i < units ? gsum4(a, i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[k] = i < units ? gsum4(a, a.u0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  // the n % 4 tail: the grid's last thread
-  const long long tail0 = (long long)units * 4;
-  const bool tail = gt == G - 1 && tail0 < a.n;
+  // the n % 4 tail: the grid's last thread (of the learner that owns it)
+  const long long tail0 = (a.n / 4) * 4;
+  const bool tail = a.tail_owner && gt == G - 1 && tail0 < a.n;
   float tg[3] = {0.f, 0.f, 0.f};
   if (tail)
     for (long long i = tail0; i < a.n; ++i) tg[i - tail0] = gsum1(a, i);
@@ -271,7 +326,7 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
       m[k] = __ldcs(m4 + i);
     }
   }
-  const double norm = grid_norm(ss, a, e);
+  const double norm = global_norm(ss, a, e);
   const float scale =
       (a.clip > 0.f && norm > (double)a.clip) ? (float)((double)a.clip / norm) : 1.f;
 #pragma unroll
@@ -287,8 +342,14 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
 #else
       {
 #endif
-        __stcs(t4 + i, th[k]);
         __stcs(m4 + i, m[k]);
+        if (a.sharded) {  // the new theta into every learner's replica (NVLink stores)
+#pragma unroll
+          for (int j = 0; j < RMS_MAX_GRADS; ++j)
+            if (j < a.ng) reinterpret_cast<float4*>(a.peer_theta[j])[a.u0 + i] = th[k];
+        } else {
+          __stcs(t4 + i, th[k]);
+        }
       }
     }
   }
@@ -296,10 +357,15 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
     for (long long i = tail0; i < a.n; ++i) {
       float t = a.theta[i], mm = a.ms[i];
       rms_update(t, mm, tg[i - tail0], scale, a);
-      a.theta[i] = t;
       a.ms[i] = mm;
+      if (a.sharded) {
+        for (int j = 0; j < a.ng; ++j) a.peer_theta[j][i] = t;
+      } else {
+        a.theta[i] = t;
+      }
     }
   }
+  if (a.sharded) __threadfence_system();  // the peer stores, before this learner's done
   peers_done(a, e);
 }
 
@@ -403,8 +469,19 @@ size_t vtrace_rmsprop_workspace_bytes(int64_t n) {
 static vt_status rmsprop_impl(int64_t n, float* params, float* mean_square,
                               const float* const* grads, int ng, uint32_t* const* flags,
                               int self, const vt_rmsprop_params* prm, double* global_norm_out,
-                              void* workspace, size_t workspace_bytes, vt_stream_t stream) {
+                              void* workspace, size_t workspace_bytes, vt_stream_t stream,
+                              float* const* peer_params = nullptr,
+                              double* const* norm_mailboxes = nullptr) {
   if (!prm || !grads || ng < 1 || ng > RMS_MAX_GRADS) return VT_ERR_INVALID_ARG;
+  const bool sharded = peer_params != nullptr;
+  if (sharded) {
+    if (!flags || !norm_mailboxes) return VT_ERR_INVALID_ARG;
+    for (int j = 0; j < ng; ++j) {
+      if (!peer_params[j] || !norm_mailboxes[j]) return VT_ERR_INVALID_ARG;
+      if (!al(peer_params[j], 16) || !al(norm_mailboxes[j], 16)) return VT_ERR_ALIGNMENT;
+    }
+    if (self >= 0 && self < ng && peer_params[self] != params) return VT_ERR_INVALID_ARG;
+  }
   if (flags) {
     if (self < 0 || self >= ng) return VT_ERR_INVALID_ARG;
     for (int j = 0; j < ng; ++j)
@@ -452,6 +529,20 @@ static vt_status rmsprop_impl(int64_t n, float* params, float* mean_square,
   }
   a.ng = ng;
   a.self = flags ? self : 0;
+  a.sharded = sharded ? 1 : 0;
+  a.u0 = 0;
+  a.u1 = n / 4;
+  a.tail_owner = 1;
+  for (int j = 0; j < RMS_MAX_GRADS; ++j) {
+    a.peer_theta[j] = sharded ? peer_params[j < ng ? j : 0] : nullptr;
+    a.nmail[j] = sharded ? reinterpret_cast<NormSlot*>(norm_mailboxes[j < ng ? j : 0]) : nullptr;
+  }
+  if (sharded) {  // learner self's float4 units: an equal split in learner order
+    const long long U = n / 4;
+    a.u0 = U * self / ng;
+    a.u1 = U * (self + 1) / ng;
+    a.tail_owner = self == ng - 1;
+  }
   a.lr = lr; a.decay = decay; a.eps = eps; a.clip = clip;
   a.norm_out = global_norm_out;
   a.ws = static_cast<unsigned char*>(workspace);
@@ -468,10 +559,11 @@ static vt_status rmsprop_impl(int64_t n, float* params, float* mean_square,
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? VT_OK : VT_ERR_CUDA;
   };
+  if (sharded && !vec) return VT_ERR_ALIGNMENT;  // (the sharded form is vectorised)
   if (vec) {
     // register-resident (one CTA per SM, up to 128 registers a thread): the smallest
     // V (float4 per thread per array) that holds n on the CTAs n can occupy
-    const long long units = n / 4, cap = (long long)sms * RMS_THREADS;
+    const long long units = std::max(a.u1 - a.u0, 1LL), cap = (long long)sms * RMS_THREADS;
     const int Vs[4] = {1, 2, 4, 6};
     for (int V : Vs) {
       if (units > cap * V) continue;
@@ -488,6 +580,7 @@ static vt_status rmsprop_impl(int64_t n, float* params, float* mean_square,
       }
     }
   }
+  if (sharded) return VT_ERR_SHAPE;  // (a shard beyond the register-resident capacity)
   // streaming form: one CTA per SM, at least 4 units per thread before a CTA is added
   const long long units = vec ? n / 4 : n;
   long long want = (units + (long long)RMS_THREADS * 4 - 1) / ((long long)RMS_THREADS * 4);
@@ -523,6 +616,25 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
   if (!flags) return VT_ERR_INVALID_ARG;
   return rmsprop_impl(n, params, mean_square, grads, num_learners, flags, self, prm,
                       global_norm_out, workspace, workspace_bytes, stream);
+}
+
+size_t vtrace_rmsprop_norm_mailbox_bytes(int32_t num_learners) {
+  if (num_learners < 1 || num_learners > RMS_MAX_GRADS) return 0;
+  return (size_t)2 * num_learners * sizeof(NormSlot);
+}
+
+vt_status vtrace_rmsprop_step_sharded(int64_t n, float* const* params, float* mean_square,
+                                      const float* const* grads, uint32_t* const* flags,
+                                      double* const* norm_mailboxes, int32_t num_learners,
+                                      int32_t self, const vt_rmsprop_params* prm,
+                                      double* global_norm_out, void* workspace,
+                                      size_t workspace_bytes, vt_stream_t stream) {
+  if (!params || !flags || !norm_mailboxes) return VT_ERR_INVALID_ARG;
+  if (num_learners < 1 || num_learners > RMS_MAX_GRADS || self < 0 || self >= num_learners)
+    return VT_ERR_INVALID_ARG;
+  return rmsprop_impl(n, params[self], mean_square, grads, num_learners, flags, self, prm,
+                      global_norm_out, workspace, workspace_bytes, stream, params,
+                      norm_mailboxes);
 }
 
 }  // extern "C"

@@ -38,7 +38,8 @@ EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_f
                     "vtrace_rmsprop_step_multi", "vtrace_rmsprop_step_learners",
                     "vtrace_output_layer", "vtrace_partials_mailbox_bytes",
                     "vtrace_partials_allreduce", "vtrace_head_workspace_bytes",
-                    "vtrace_head_loss_and_grad")
+                    "vtrace_head_loss_and_grad", "vtrace_rmsprop_norm_mailbox_bytes",
+                    "vtrace_rmsprop_step_sharded")
 
 
 class VtraceError(RuntimeError):
@@ -130,6 +131,15 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_partials_allreduce.argtypes = [P, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
                                               ctypes.c_int32, P, P, P]
     lib.vtrace_partials_allreduce.restype = ctypes.c_int
+    lib.vtrace_rmsprop_norm_mailbox_bytes.argtypes = [ctypes.c_int32]
+    lib.vtrace_rmsprop_norm_mailbox_bytes.restype = ctypes.c_size_t
+    lib.vtrace_rmsprop_step_sharded.argtypes = [i64, ctypes.POINTER(ctypes.c_void_p), P,
+                                                ctypes.POINTER(ctypes.c_void_p),
+                                                ctypes.POINTER(ctypes.c_void_p),
+                                                ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                                ctypes.c_int32, ctypes.POINTER(_RmsParams), P, P,
+                                                ctypes.c_size_t, P]
+    lib.vtrace_rmsprop_step_sharded.restype = ctypes.c_int
     lib.vtrace_head_workspace_bytes.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_int32]
     lib.vtrace_head_workspace_bytes.restype = ctypes.c_size_t
     lib.vtrace_head_loss_and_grad.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_int32] + [P] * 8 + [
@@ -521,6 +531,37 @@ def rmsprop_step(params, mean_square, grads, learning_rate: float, decay: float,
                                        ctypes.byref(prm), _ptr(global_norm_out), ws.ptr,
                                        ws.nbytes, _stream(params.device))
     _check(st, "vtrace_rmsprop_step_multi")
+
+
+def rmsprop_norm_mailbox_bytes(num_learners: int) -> int:
+    return int(load_library().vtrace_rmsprop_norm_mailbox_bytes(int(num_learners)))
+
+
+def rmsprop_step_sharded(params_ptrs, mean_square, grads_ptrs, learning_rate: float,
+                         decay: float, epsilon: float, max_global_norm: float, *, flags,
+                         norm_mailboxes, self_index: int, n: int, workspace: RmspropWorkspace,
+                         global_norm_out=None):
+    """vtrace_rmsprop_step_sharded: the learners' update sharded over the learners (each
+    updates 1/N of the parameters from the summed gradients and writes the new values into
+    every learner's params).  ``params_ptrs``, ``grads_ptrs``, ``flags``, ``norm_mailboxes``:
+    one device pointer per learner (peer-mapped); ``mean_square`` this learner's fp32
+    tensor of n elements.  Marshalling only."""
+    if not (mean_square.is_cuda and mean_square.dtype == torch.float32 and
+            mean_square.is_contiguous() and mean_square.numel() == n):
+        raise ValueError("mean_square must be a contiguous fp32 CUDA tensor of n elements")
+    N = len(params_ptrs)
+    if not (len(grads_ptrs) == len(flags) == len(norm_mailboxes) == N):
+        raise ValueError("one params / grads / flags / mailbox pointer per learner")
+    key = (float(learning_rate), float(decay), float(epsilon), float(max_global_norm))
+    prm = _RMS_PRM_CACHE.get(key)
+    if prm is None:
+        prm = _RMS_PRM_CACHE.setdefault(key, _RmsParams(*key))
+    st = load_library().vtrace_rmsprop_step_sharded(
+        int(n), _ptr_array([int(p) for p in params_ptrs]), _ptr(mean_square),
+        _ptr_array([int(p) for p in grads_ptrs]), _ptr_array([int(p) for p in flags]),
+        _ptr_array([int(p) for p in norm_mailboxes]), N, int(self_index), ctypes.byref(prm),
+        _ptr(global_norm_out), workspace.ptr, workspace.nbytes, _stream(mean_square.device))
+    _check(st, "vtrace_rmsprop_step_sharded")
 
 
 def output_layer(hidden: torch.Tensor, w_t: torch.Tensor, bias: torch.Tensor | None = None,

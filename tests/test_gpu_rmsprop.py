@@ -245,3 +245,59 @@ def test_rmsprop_learners_sync_path():
         res.append((theta.cpu().numpy(), ms.cpu().numpy()))
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
     assert flags[0].tolist() == [3, 3]  # three calls: ready and done of epoch 2 + 1
+
+
+def test_rmsprop_sharded_learner_with_simulated_peer():
+    """vtrace_rmsprop_step_sharded on one GPU (a second cooperative grid cannot share the
+    GPU, so learner 1 is simulated): learner 0 owns float4 units [0, U/2); the peer's
+    flags read "ready and done", and its shard sum of squares is placed in learner 0's
+    norm mailbox with each call's tag.  Learner 0 must (a) update its shard of theta and
+    ms like the oracle with the GLOBAL norm (own shard + the peer's, learner order),
+    (b) write the same new theta into the peer's params for its shard only, (c) leave
+    its other shard of theta and ms untouched, (d) report the global norm."""
+    n = 200_000
+    inp = wl.update_inputs(n, seed=31, norm=75.0, learners=2)
+    dev = "cuda"
+    gs = [torch.from_numpy(g).to(dev) for g in inp["grads"]]
+    theta = torch.from_numpy(inp["params"]).to(dev)
+    theta_peer = torch.from_numpy(inp["params"]).to(dev)
+    ms = torch.from_numpy(inp["mean_square"]).to(dev)
+    flags = torch.zeros(2, 2, dtype=torch.int32, device=dev)
+    flags[1] = 1 << 30  # the simulated peer: ahead of every epoch used here
+    nb = pkg.vtrace.rmsprop_norm_mailbox_bytes(2)
+    assert nb == 2 * 2 * 16
+    mbox = [torch.zeros(nb // 8, dtype=torch.float64, device=dev) for _ in range(2)]
+    ws = pkg.RmspropWorkspace(n, dev)
+    norm = torch.zeros(1, dtype=torch.float64, device=dev)
+    U = n // 4
+    cut = 4 * (U * 0 // 2), 4 * (U * 1 // 2)  # learner 0: elements [0, 4 * (U // 2))
+    lo, hi = 0, cut[1]
+    th_ref, ms_ref = inp["params"].copy(), inp["mean_square"].copy()
+    total = ro.sum_learner_grads(inp["grads"])
+    for call in range(3):
+        # the peer's shard sum of squares (fp32 sums of the buffers, as the kernel adds them)
+        g32 = (inp["grads"][0] + inp["grads"][1]).astype(np.float32).astype(np.float64)
+        ss_peer = float(np.sum(g32[hi:] ** 2))
+        tag = call + 1
+        slot = (tag & 1) * 2 + 1  # [parity][learner 1]
+        mbox[0][2 * slot] = ss_peer
+        mbox[0].view(torch.int64)[2 * slot + 1] = tag
+        pkg.vtrace.rmsprop_step_sharded(
+            [theta.data_ptr(), theta_peer.data_ptr()], ms, [g.data_ptr() for g in gs],
+            LR, DECAY, EPS, CLIP, flags=[flags[0].data_ptr(), flags[1].data_ptr()],
+            norm_mailboxes=[m.data_ptr() for m in mbox], self_index=0, n=n, workspace=ws,
+            global_norm_out=norm)
+        torch.cuda.synchronize()
+        th0 = th_ref.copy()
+        th_ref, ms_ref, nr_ref = ro.rmsprop_step(th_ref, ms_ref, total, _f32(LR), _f32(DECAY),
+                                                 _f32(EPS), _f32(CLIP))
+        got_t, got_m = theta.cpu().numpy(), ms.cpu().numpy()
+        _check(got_t[lo:hi], got_m[lo:hi], th0[lo:hi], th_ref[lo:hi], ms_ref[lo:hi])
+        assert np.array_equal(theta_peer.cpu().numpy()[lo:hi], got_t[lo:hi])   # (b)
+        assert np.array_equal(got_t[hi:], inp["params"][hi:])                   # (c)
+        assert np.array_equal(got_m[hi:], inp["mean_square"][hi:])
+        assert np.array_equal(theta_peer.cpu().numpy()[hi:], inp["params"][hi:])
+        assert float(norm.item()) == pytest.approx(nr_ref, rel=1e-6)           # (d)
+        # (keep the oracle's untouched shard equal to the kernel's for the next call)
+        th_ref[hi:], ms_ref[hi:] = inp["params"][hi:], inp["mean_square"][hi:]
+    assert flags[0].tolist() == [3, 3]
