@@ -74,6 +74,21 @@ struct RmsArgs {
   NormSlot* nmail[RMS_MAX_GRADS];       // every learner's norm mailbox [2][ng]
 };
 
+#ifdef RMS_TIMING
+// timing build only (not part of the ABI): globaltimer stamps of CTA 0 / the last CTA per
+// call (ring of 4096 calls): [start, ready published, peers ready seen, norm known,
+// updates stored, done published, peers done seen]
+__device__ unsigned long long rms_stamps[4096][8];
+__device__ __forceinline__ unsigned long long rms_now() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return g;
+}
+#define RMS_STAMP(e, k) (rms_stamps[(e) & 4095][k] = rms_now())
+#else
+#define RMS_STAMP(e, k) ((void)0)
+#endif
+
 // The gradient element i: the sum of the ng buffers in index order (fp32), so every
 // learner that passes the same buffers in the same order gets the same bits.  The
 // buffers may be other GPUs' memory (NVLink peer pointers, e.g. symmetric memory):
@@ -134,13 +149,16 @@ __device__ __forceinline__ void peers_ready(const RmsArgs& a, unsigned int e) {
   RmsHeader* hdr = reinterpret_cast<RmsHeader*>(a.ws);
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
+      RMS_STAMP(e, 0);
       __threadfence_system();
       st_release_sys(a.flags[a.self], e + 1u);
+      RMS_STAMP(e, 1);
       for (int j = 0; j < a.ng; ++j) {
         if (j == a.self) continue;
         while ((int)(ld_acquire_sys(a.flags[j]) - (e + 1u)) < 0) {
         }
       }
+      RMS_STAMP(e, 2);
       st_release_u32(&hdr->go, e + 1u);
     } else {
       while ((int)(ld_acquire_u32(&hdr->go) - (e + 1u)) < 0) {
@@ -158,16 +176,21 @@ __device__ __forceinline__ void peers_done(const RmsArgs& a, unsigned int e) {
   __syncthreads();
   if (threadIdx.x == 0) {
     RmsHeader* hdr = reinterpret_cast<RmsHeader*>(a.ws);
-    __threadfence();
+    // (cumulative after the CTA barrier: the CTA's stores -- peer stores of the sharded
+    // form included -- before this learner's done)
+    if (a.sharded) __threadfence_system();
+    else __threadfence();
     const unsigned int prev = atomicAdd(&hdr->done_ticket, 1u);
     if (prev == gridDim.x - 1) {
       hdr->done_ticket = 0u;
       st_release_sys(a.flags[a.self] + 1, e + 1u);
+      RMS_STAMP(e, 5);
       for (int j = 0; j < a.ng; ++j) {
         if (j == a.self) continue;
         while ((int)(ld_acquire_sys(a.flags[j] + 1) - (e + 1u)) < 0) {
         }
       }
+      RMS_STAMP(e, 6);
     }
   }
 }
@@ -327,6 +350,7 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
     }
   }
   const double norm = global_norm(ss, a, e);
+  if (blockIdx.x == 0 && tid == 0) RMS_STAMP(e, 3);
   const float scale =
       (a.clip > 0.f && norm > (double)a.clip) ? (float)((double)a.clip / norm) : 1.f;
 #pragma unroll
@@ -365,7 +389,7 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
       }
     }
   }
-  if (a.sharded) __threadfence_system();  // the peer stores, before this learner's done
+  if (blockIdx.x == 0 && tid == 0) RMS_STAMP(e, 4);
   peers_done(a, e);
 }
 
@@ -405,7 +429,7 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_kernel(const RmsArgs a
       ss = fma(v, v, ss);
     }
   }
-  const double norm = grid_norm(ss, a, e);
+  const double norm = global_norm(ss, a, e);
   // clip scale c / max(||g||, c) in fp64 (reading r10); 1 when disabled
   const float scale =
       (a.clip > 0.f && norm > (double)a.clip) ? (float)((double)a.clip / norm) : 1.f;
@@ -458,6 +482,12 @@ static bool al(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p)
 using namespace vtb200;
 
 extern "C" {
+
+#ifdef RMS_TIMING
+int vtrace_debug_rms_stamps(unsigned long long* host) {  // timing build only
+  return (int)cudaMemcpyFromSymbol(host, rms_stamps, sizeof(unsigned long long) * 8 * 4096);
+}
+#endif
 
 size_t vtrace_rmsprop_workspace_bytes(int64_t n) {
   if (n < 0) return 0;

@@ -13,4 +13,5 @@ timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > ${P}_bench_
 for cfg in atari dmlab stress toy; do timeout 300 python bench.py --config $cfg --no-cpu-baseline > ${P}_bench_$cfg.json 2>> ${P}_bench.err; done
 timeout 300 python bench.py --path update > ${P}_bench_update.json 2>> ${P}_bench.err
 timeout 300 python bench.py --path head --steps 200 --warmup 5 > ${P}_bench_head.json 2>> ${P}_bench.err
+timeout 300 python bench.py --path head_fused --steps 100 --warmup 5 > ${P}_bench_head_fused.json 2>> ${P}_bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:vtrace_ -c 200 --csv --log-file ${P}_launches.csv python bench.py --steps 50 --warmup 3 --no-cpu-baseline --no-e2e > ${P}_launches.log 2>&1; echo "rc=$?" >> ${P}_launches.log
