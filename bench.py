@@ -622,6 +622,27 @@ def run_reference(args):
 # --path update: the learner's parameter update
 
 
+def _rms_stamp_summary(e0, e1, rank):
+    """(dev) medians of the RMS_TIMING stamps of calls [e0, e1) (the last 4000 at most)."""
+    import ctypes
+    import numpy as np
+    import paper_1802_01561_b200 as pkg
+    lib = pkg.load_library()
+    buf = (ctypes.c_ulonglong * (8 * 4096))()
+    lib.vtrace_debug_rms_stamps.argtypes = [ctypes.c_void_p]
+    lib.vtrace_debug_rms_stamps(ctypes.addressof(buf))
+    st = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).astype(np.int64)
+    ep = np.arange(max(e0, e1 - 4000), e1)
+    a = st[ep % 4096]
+    d = lambda i, j: float(np.median(a[:, j] - a[:, i]) / 1e3)  # noqa: E731
+    print(json.dumps({"rank": rank, "calls": int(len(ep)),
+                      "period_us": float(np.median(np.diff(a[:, 0])) / 1e3),
+                      "ready_pub": d(0, 1), "wait_peers_ready": d(1, 2), "reads_norm": d(2, 3),
+                      "update": d(3, 4), "to_done_pub": d(4, 5), "wait_peers_done": d(5, 6),
+                      "gap_to_next_start": float(np.median(a[1:, 0] - a[:-1, 6]) / 1e3)}),
+          file=sys.stderr, flush=True)
+
+
 def run_update(args):
     """K synchronous learner updates of n parameters: (N > 1) NCCL SUM all-reduce of
     the fp32 gradient, then vtrace_rmsprop_step (clip 40, RMSProp) on every
@@ -770,7 +791,10 @@ def run_update(args):
     if sampler:
         sampler.start()
     tw0 = time.time()
+    e_first = int(ws.tensor[:4].view(torch.int32).item()) if os.environ.get("VT_RMS_STAMPS") else 0
     step_ms = timed(g_full, g_rem)
+    if os.environ.get("VT_RMS_STAMPS"):  # RMS_TIMING builds only: per-call stamps of the region
+        _rms_stamp_summary(e_first, int(ws.tensor[:4].view(torch.int32).item()), rank)
     tw1 = time.time()
     barrier(world)
     if sampler:

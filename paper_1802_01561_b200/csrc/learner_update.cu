@@ -150,7 +150,13 @@ __device__ __forceinline__ void peers_ready(const RmsArgs& a, unsigned int e) {
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
       RMS_STAMP(e, 0);
+      // (no system fence before it: the buffers the peers read were written by earlier
+      // kernels on this stream, complete before this one started, and peer reads over
+      // NVLink are served by this GPU's memory system -- the fence cost ~1-1.5 us a call,
+      // profiles/r2_update_n2_stamps.txt)
+#ifdef RMS_SYSFENCE
       __threadfence_system();
+#endif
       st_release_sys(a.flags[a.self], e + 1u);
       RMS_STAMP(e, 1);
       for (int j = 0; j < a.ng; ++j) {
@@ -579,6 +585,9 @@ static vt_status rmsprop_impl(int64_t n, float* params, float* mean_square,
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (norm exchange)
   attr[0].val.cooperative = 1;  // (measured: no cost over a plain launch)
+#ifdef RMS_NO_COOP
+  attr[0].val.cooperative = 0;  // A/B only
+#endif
   auto launch = [&](auto kern, int grid) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -18,13 +18,14 @@ from paper_1802_01561_b200 import workload as wl  # noqa: E402
 
 def main():
     sharded = len(sys.argv) > 1 and sys.argv[1] == "sharded"
+    R = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # rotated state copies (as bench.py)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
     import torch.distributed._symmetric_memory as symm_mem
     n = wl.UPDATE_SIZES["deep"]
     inp = wl.update_inputs(n, seed=1 + rank, norm=60.0)
-    g = torch.from_numpy(inp["grads"][0]).cuda()
+    gs = [torch.from_numpy(inp["grads"][0]).cuda() for _ in range(R)]
     red = symm_mem.empty(n, dtype=torch.float32, device="cuda")
     ptrs = [int(p) for p in symm_mem.rendezvous(red, dist.group.WORLD.group_name).buffer_ptrs]
     flg = symm_mem.empty(2, dtype=torch.int32, device="cuda")
@@ -37,20 +38,24 @@ def main():
                          device="cuda")
     nmb.zero_()
     nptrs = [int(p) for p in symm_mem.rendezvous(nmb, dist.group.WORLD.group_name).buffer_ptrs]
-    ms = torch.from_numpy(inp["mean_square"]).cuda()
+    mss = [torch.from_numpy(inp["mean_square"]).cuda() for _ in range(R)]
+    ths = [th] + [torch.from_numpy(inp["params"]).cuda() for _ in range(R - 1)]
     ws = pkg.RmspropWorkspace(n)
+    it = [0]
     torch.cuda.synchronize()
     dist.barrier()
     s = torch.cuda.Stream()
 
     def step():
-        torch.mul(g, 1.0, out=red)
+        j = it[0] % R
+        it[0] += 1
+        torch.mul(gs[j], 1.0, out=red)
         if sharded:
-            pkg.vtrace.rmsprop_step_sharded(tptrs, ms, ptrs, 6e-4, 0.99, 0.01, 40.0, flags=fptrs,
-                                            norm_mailboxes=nptrs, self_index=rank, n=n,
-                                            workspace=ws)
+            pkg.vtrace.rmsprop_step_sharded(tptrs, mss[j], ptrs, 6e-4, 0.99, 0.01, 40.0,
+                                            flags=fptrs, norm_mailboxes=nptrs, self_index=rank,
+                                            n=n, workspace=ws)
         else:
-            pkg.rmsprop_step(th, ms, ptrs, 6e-4, 0.99, 0.01, 40.0, workspace=ws,
+            pkg.rmsprop_step(ths[j], mss[j], ptrs, 6e-4, 0.99, 0.01, 40.0, workspace=ws,
                              learner_flags=fptrs, self_index=rank)
 
     with torch.cuda.stream(s):
@@ -64,10 +69,16 @@ def main():
             step()
     torch.cuda.synchronize()
     dist.barrier()
+    import time
+    host_us = []
+    t_all = time.perf_counter()
     with torch.cuda.stream(s):
         for _ in range(8):
+            t0 = time.perf_counter()
             gr.replay()
+            host_us.append((time.perf_counter() - t0) * 1e6)
     torch.cuda.synchronize()
+    wall_us = (time.perf_counter() - t_all) * 1e6
     lib = pkg.load_library()
     buf = (ctypes.c_ulonglong * (8 * 4096))()
     lib.vtrace_debug_rms_stamps.argtypes = [ctypes.c_void_p]
@@ -79,14 +90,18 @@ def main():
         d = lambda i, j: np.median(a[:, j] - a[:, i]) / 1e3  # noqa: E731
         per = np.median(np.diff(a[:, 0])) / 1e3
         gap = np.median(a[1:, 0] - a[:-1, 6]) / 1e3
-        return {"period_us": round(per, 2), "ready_pub": round(d(0, 1), 2),
+        per_mean = float(np.mean(np.diff(a[:, 0]))) / 1e3
+        per_max = float(np.max(np.diff(a[:, 0]))) / 1e3
+        return {"period_us": round(per, 2), "period_mean_us": round(per_mean, 2),
+                "period_max_us": round(per_max, 2), "ready_pub": round(d(0, 1), 2),
                 "wait_peers_ready": round(d(1, 2), 2), "reads_norm": round(d(2, 3), 2),
                 "update": round(d(3, 4), 2), "to_done_pub": round(d(4, 5), 2),
                 "wait_peers_done": round(d(5, 6), 2), "gap_to_next_start": round(gap, 2)}
     # eager calls: epochs 3 (after the setup call) .. 300; graph: the replays' calls
-    out = {"rank": rank, "sharded": sharded, "eager": summary(100, 300),
+    out = {"rank": rank, "sharded": sharded, "R": R, "eager": summary(100, 300),
            "graph_capture_epochs": "replays of 30 steps x 8",
-           "graph": summary(330, 539)}
+           "graph": summary(330, 539), "graph_replay_host_us": [round(x) for x in host_us],
+           "graph_wall_us_per_step": round(wall_us / 240, 2)}
     print(json.dumps(out), flush=True)
     dist.destroy_process_group()
 
