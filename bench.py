@@ -635,8 +635,12 @@ def _rms_stamp_summary(e0, e1, rank):
     ep = np.arange(max(e0, e1 - 4000), e1)
     a = st[ep % 4096]
     d = lambda i, j: float(np.median(a[:, j] - a[:, i]) / 1e3)  # noqa: E731
+    per = np.diff(a[:, 0]) / 1e3
     print(json.dumps({"rank": rank, "calls": int(len(ep)),
-                      "period_us": float(np.median(np.diff(a[:, 0])) / 1e3),
+                      "period_us": float(np.median(per)), "period_mean_us": float(per.mean()),
+                      "period_max_us": float(per.max()),
+                      "gaps_over_100us": int((per > 100).sum()),
+                      "gap_positions": [int(i) for i in np.nonzero(per > 100)[0][:12]],
                       "ready_pub": d(0, 1), "wait_peers_ready": d(1, 2), "reads_norm": d(2, 3),
                       "update": d(3, 4), "to_done_pub": d(4, 5), "wait_peers_done": d(5, 6),
                       "gap_to_next_start": float(np.median(a[1:, 0] - a[:-1, 6]) / 1e3)}),
@@ -773,23 +777,37 @@ def run_update(args):
 
     def timed(gf, gr, allreduce=True):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        barrier(world)  # (the learners sync inside the kernels: start the region together)
         t0.record(s_main)
         with torch.cuda.stream(s_main):
             if gf is None:
                 for i in range(K):
                     step(i, allreduce)
             else:
+                th = []
                 for _ in range(n_full):
+                    h0 = time.perf_counter()
                     gf.replay()
+                    th.append((time.perf_counter() - h0) * 1e6)
                 if gr is not None:
                     gr.replay()
+                if os.environ.get("VT_RMS_STAMPS"):
+                    print(json.dumps({"rank": rank, "graph_replay_host_us": [round(x) for x in th[:12]],
+                                      "host_total_us": round(sum(th))}), file=sys.stderr)
         t1.record(s_main)
         torch.cuda.synchronize()
         return max_over_ranks(t0.elapsed_time(t1), world) / K
 
+    # the clock sampler starts BEFORE the ranks line up: its start (a subprocess) took ~150 ms
+    # on rank 0, during which the other rank's first update waited inside the kernel for
+    # rank 0's ready flag -- 150 ms / 2000 steps was the "graph penalty" of the round-1
+    # N = 2 update numbers (profiles/r2_update_n2_stamps.txt)
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
+    barrier(world)
+    torch.cuda.synchronize()
     tw0 = time.time()
     e_first = int(ws.tensor[:4].view(torch.int32).item()) if os.environ.get("VT_RMS_STAMPS") else 0
     step_ms = timed(g_full, g_rem)
