@@ -915,7 +915,11 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     };
 
     auto group_sync = [&]() {
+#if defined(CB_NOSYNC)
+      // timing A/B only (wrong results): no barrier between the group's X(j) and Y(j)
+#else
       if (C.nts > 1) named_bar(1 + cg, 32 * C.nts);  // the group's X(j) aggregates are out
+#endif
     };
 #if defined(CB_STAGGER) && CB_STAGGER > 0
     // phase offset between the warps of a sub-partition (warps w and w + 4 share one):
