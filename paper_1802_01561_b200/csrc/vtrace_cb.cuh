@@ -527,6 +527,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
   __shared__ double agg[2][CB_MAX_WARPS][4][2];  // [parity][warp][column][G, D]
   __shared__ double wpart[CB_MAX_WARPS + 2][NPART];  // [warps | producer | own CTA sum]
   __shared__ unsigned int s_epoch, s_last;
+  __shared__ __align__(8) uint64_t ep_bar;  // the producer has read the call's epoch
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) CB_STAMP(0);
@@ -541,6 +542,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       mbar_init(&full[s], PLAIN ? 32 : 1);
       mbar_init(&done[s], NW);
     }
+    mbar_init(&ep_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -560,7 +562,10 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       mbar_wait32(done0 + 8u * s, ph);
       if (j == 0) {
         if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (lane == 0) s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+        if (lane == 0) {
+          s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+          mbar_arrive(&ep_bar);
+        }
       }
       io.store(j, s, C.out_mask);
       __syncwarp();
@@ -617,6 +622,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
           // final from here on: read it now, off the tail of the kernel
           if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
           s_epoch = *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) & 0x3fffffffu;
+          mbar_arrive(&ep_bar);
         }
         const int tb = (C.J - 1 - j) * C.Ts;
         const uint32_t sb = sm0 + (uint32_t)s * C.stage;
@@ -982,7 +988,12 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     }
   }
   if (!LOSS || P.partials == nullptr) return;
-  __syncthreads();  // wpart complete; s_epoch set (the producer's first iteration)
+  // The producer leaves once its last stores have read shared memory: the partials tail
+  // runs on the compute warps alone, in parallel with that drain (named barrier 15 over
+  // the NW compute warps; the group barriers use 1..ncg <= 14)
+  if (warp == NW) return;
+  named_bar(15, 32 * NW);  // wpart complete
+  mbar_wait32(smem_u32(&ep_bar), 0u);  // s_epoch set (the producer's first iteration)
   const int S = gridDim.x;
   const unsigned int epoch = s_epoch;
   const unsigned long long tag = ((unsigned long long)epoch << 2) | 3ull;
@@ -1003,14 +1014,14 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       if (s_last) *C.top_count = 0u;  // every ticket of this call is taken: re-arm
     }
   }
-  __syncthreads();
+  named_bar(15, 32 * NW);
   if (!s_last) return;
   if (threadIdx.x == 0) CB_STAMP(5);
   // the last CTA: all its warps request the other CTAs' records at once (warp w2 takes
   // the contiguous CTA range [w2 S / W, (w2 + 1) S / W), lane = (CTA, partial)), re-poll
   // any record whose tag is not this call's yet, add their range in CTA order; warp 0
   // then adds the warps' sums in order: a fixed tree, independent of the arrival order
-  const int W = NW + 1;
+  const int W = NW;
   {
     const int c_lo = warp * S / W, c_hi = (warp + 1) * S / W;
     const int k = lane & (NPART - 1), sub = lane >> 3;  // 4 CTAs per pass, one partial per lane
@@ -1052,7 +1063,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     if (lane < NPART) wpart[warp][lane] = acc_k;
     if (threadIdx.x == 0) CB_STAMP(6);
   }
-  __syncthreads();
+  named_bar(15, 32 * NW);
   if (threadIdx.x == 0) CB_STAMP(7);
   if (warp == 0) {
     // lane k < NPART adds partial k over the warps in order (one short chain per lane,
