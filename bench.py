@@ -377,6 +377,28 @@ def run_ours(args):
     elapsed_max = max_over_ranks(elapsed_ms, world)
     kw_step = dict(kw, overlap_previous=overlap, sm_budget=step_obj.kw["sm_budget"])
 
+    # multi-GPU correctness of the step's collective (untimed): one more step through the
+    # product API against an NCCL all_reduce of the same per-rank partials
+    collective_check = None
+    if world > 1:
+        o = outs[0]
+        pkg.loss_and_grad(*[sets[0][k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw)
+        torch.cuda.synchronize()
+        local = o["partials"].clone()
+        step_obj(sets[0], o)
+        step_obj.join()
+        torch.cuda.synchronize()
+        ref = local.clone()
+        dist.all_reduce(ref, op=dist.ReduceOp.SUM)
+        torch.cuda.synchronize()
+        rel = float(((o["partials"] - ref).abs() / ref.abs().clamp_min(1e-300)).max())
+        agree = torch.tensor([o["partials"].sum().item()], dtype=torch.float64, device="cuda")
+        gathered = [torch.zeros_like(agree) for _ in range(world)]
+        dist.all_gather(gathered, agree)
+        collective_check = {"max_rel_diff_vs_nccl": rel,
+                            "identical_on_every_rank": all(bool(torch.equal(gathered[0], g))
+                                                           for g in gathered[1:])}
+
     # kernel-only timing for the roofline: the same kernels, no collective
     Kk = min(K, 2000)
     gk = None
@@ -506,6 +528,7 @@ def run_ours(args):
                      "kernel": vt.kernel_for(T, B, A, inp["dtype"]), "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
         "gpu_launches": K,  # one fused kernel per step
+        "collective_check": collective_check,
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
