@@ -73,7 +73,8 @@ def parse():
                          "(SURVEY 8(f) NEXT #4: gradient all-reduce at N > 1, global-norm "
                          "clip, RMSProp) instead of the V-trace path; head: the tcgen05 output "
                          "layer [z|V] = hW + b in front of the path (NEXT #3)")
-    ap.add_argument("--update-collective", choices=["symm", "symm_sharded", "nccl"], default="symm",
+    ap.add_argument("--update-collective", choices=["symm", "symm_push", "symm_sharded", "nccl"],
+                    default="symm",
                     help="N > 1 on the update path: symm = the kernel sums every learner's "
                          "gradient over NVLink from symmetric memory (fused); nccl = NCCL "
                          "all_reduce then the single-gradient kernel")
@@ -700,8 +701,9 @@ def run_update(args):
     ws = pkg.RmspropWorkspace(n)
     s_main = torch.cuda.Stream()
 
-    symm = world > 1 and args.update_collective in ("symm", "symm_sharded")
+    symm = world > 1 and args.update_collective in ("symm", "symm_sharded", "symm_push")
     sharded = world > 1 and args.update_collective == "symm_sharded"
+    push = world > 1 and args.update_collective == "symm_push"
     red = hdl = ptrs = None
     if symm:
         # the learners' gradient buffers in symmetric memory: every GPU maps every
@@ -715,6 +717,12 @@ def run_update(args):
         flg.zero_()
         hdl_f = symm_mem.rendezvous(flg, dist.group.WORLD.group_name)
         fptrs = [int(p) for p in hdl_f.buffer_ptrs]
+        if push:
+            # every learner's receive buffer [N][n]: slot j holds learner j's pushed gradient
+            recv = symm_mem.empty(world * n, dtype=torch.float32, device="cuda")
+            hdl_r = symm_mem.rendezvous(recv, dist.group.WORLD.group_name)
+            rptrs = [int(p) for p in hdl_r.buffer_ptrs]
+            lslots = [rptrs[rank] + 4 * j * n for j in range(world)]
         if sharded:
             # every learner's R parameter copies in one symmetric allocation: a learner
             # writes its shard of the new theta into all of them (NVLink stores)
@@ -741,6 +749,13 @@ def run_update(args):
                 # this step's local gradient (the backward's output) -- an SM kernel: a
                 # captured D2D copy_ measured ~70 us per 6.4 MB in graph replay at N = 2
                 torch.mul(grads[j], 1.0, out=red)
+            if push:  # the gradient pushed into every learner's slot, then local reads only
+                if allreduce:
+                    pkg.vtrace.grad_push(grads[j], rptrs, rank)
+                pkg.rmsprop_step(theta[j], ms[j], lslots, lr, decay, eps, clip,
+                                 global_norm_out=norm, workspace=ws, learner_flags=fptrs,
+                                 self_index=rank)
+                return
             if sharded:  # this learner's 1/N of the parameters, new theta to every learner
                 pkg.vtrace.rmsprop_step_sharded(tptrs[j], ms[j], ptrs, lr, decay, eps, clip,
                                                 flags=fptrs, norm_mailboxes=nptrs,
@@ -913,7 +928,11 @@ def run_update(args):
         "config": {"workload": f"learner update, {size} model ({n} parameters)",
                    "n_params": n, "optimizer": "RMSProp momentum 0, decay 0.99, eps 0.01, "
                    "lr 6e-4, clip global norm 40 (P:950-953)",
-                   "collective": (("per step: local gradient into symmetric memory; ONE kernel "
+                   "collective": (("per step: the local gradient pushed into every learner's "
+                                   "receive slot (NVLink stores, vtrace_grad_push); ONE kernel "
+                                   "syncs the learners and sums the local slots (rank order)")
+                                  if push else
+                                  ("per step: local gradient into symmetric memory; ONE kernel "
                                    "per learner updates its 1/N shard from every learner's "
                                    "gradient (NVLink reads), adds the shards' norms through "
                                    "mailboxes and stores the new theta into every replica "

@@ -346,6 +346,22 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
  * register-resident form (148 x 512 x 6 float4 units; else VT_ERR_SHAPE).  Other errors
  * and the call discipline as vtrace_rmsprop_step_learners. */
 size_t vtrace_rmsprop_norm_mailbox_bytes(int32_t num_learners);
+
+/* The push half of a push-based gradient all-gather: learner `self` stores its
+ * gradient into slot `self` of every learner's receive buffer (NVLink stores into peer
+ * memory; posted writes instead of the peers' remote reads), then fences at system scope, so
+ * that a following vtrace_rmsprop_step_learners on the same stream -- given the LOCAL slots
+ * recv[0..N-1] of this learner's own receive buffer as its gradients -- may publish ready and
+ * every learner reads only local memory.  The learners' ready / done protocol of that call is
+ * what makes a slot safe to read and to refill.
+ *   grad         float[n] device (16-byte aligned): this learner's gradient
+ *   recv         host array of num_learners device pointers (16-byte aligned): learner r's
+ *                receive buffer of num_learners * n floats, slot j at recv[r] + j * n
+ *                (peer-mapped, e.g. symmetric memory)
+ * Errors: VT_ERR_INVALID_ARG (NULL, num_learners or self out of range), VT_ERR_SHAPE (n < 0 or
+ * n % 4 != 0), VT_ERR_ALIGNMENT, VT_ERR_DEVICE, VT_ERR_CUDA.  One launch on `stream`. */
+vt_status vtrace_grad_push(const float* grad, float* const* recv, int32_t num_learners,
+                           int32_t self, int64_t n, vt_stream_t stream);
 vt_status vtrace_rmsprop_step_sharded(int64_t n, float* const* params, float* mean_square,
                                       const float* const* grads, uint32_t* const* flags,
                                       double* const* norm_mailboxes, int32_t num_learners,

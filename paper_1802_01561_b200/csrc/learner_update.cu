@@ -399,6 +399,27 @@ __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_reg_kernel(const RmsAr
   peers_done(a, e);
 }
 
+// The push half of a push-based gradient all-gather: slot `self` of every learner's receive
+// buffer <- this learner's gradient (float4 stores, NVLink for the peers), then a system-scope
+// fence by every thread so that the next kernel's ready flag follows the pushed data.
+struct PushArgs {
+  const float4* g;
+  float4* dst[RMS_MAX_GRADS];  // recv[r] + self * n, as float4
+  int ng;
+  long long units;
+};
+
+__global__ void __launch_bounds__(RMS_THREADS) grad_push_kernel(const PushArgs a) {
+  const long long stride = (long long)gridDim.x * RMS_THREADS;
+  for (long long i = (long long)blockIdx.x * RMS_THREADS + threadIdx.x; i < a.units; i += stride) {
+    const float4 v = __ldcs(a.g + i);
+#pragma unroll
+    for (int r = 0; r < RMS_MAX_GRADS; ++r)
+      if (r < a.ng) a.dst[r][i] = v;
+  }
+  __threadfence_system();
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(RMS_THREADS, 1) rmsprop_kernel(const RmsArgs a) {
   const int S = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
@@ -655,6 +676,38 @@ vt_status vtrace_rmsprop_step_learners(int64_t n, float* params, float* mean_squ
   if (!flags) return VT_ERR_INVALID_ARG;
   return rmsprop_impl(n, params, mean_square, grads, num_learners, flags, self, prm,
                       global_norm_out, workspace, workspace_bytes, stream);
+}
+
+vt_status vtrace_grad_push(const float* grad, float* const* recv, int32_t num_learners,
+                           int32_t self, int64_t n, vt_stream_t stream) {
+  if (!grad || !recv) return VT_ERR_INVALID_ARG;
+  if (num_learners < 1 || num_learners > RMS_MAX_GRADS || self < 0 || self >= num_learners)
+    return VT_ERR_INVALID_ARG;
+  if (n < 0 || n % 4) return VT_ERR_SHAPE;
+  if (!al(grad, 16)) return VT_ERR_ALIGNMENT;
+  PushArgs a = {};
+  a.g = reinterpret_cast<const float4*>(grad);
+  a.ng = num_learners;
+  a.units = n / 4;
+  for (int r = 0; r < RMS_MAX_GRADS; ++r) {
+    float* base = recv[r < num_learners ? r : 0];
+    if (!base) return VT_ERR_INVALID_ARG;
+    if (!al(base, 16)) return VT_ERR_ALIGNMENT;
+    a.dst[r] = reinterpret_cast<float4*>(base + (size_t)self * (size_t)n);
+  }
+  int dev = 0, maj = 0, mnr = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&mnr, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+    return VT_ERR_CUDA;
+  if (!(maj == 10 && mnr == 0)) return VT_ERR_DEVICE;
+  if (n == 0) return VT_OK;
+  const int sms = rms_num_sms();
+  if (sms <= 0) return VT_ERR_CUDA;
+  const long long want = (a.units + RMS_THREADS - 1) / RMS_THREADS;
+  const int grid = (int)std::max(1LL, std::min<long long>(want, 4LL * sms));
+  grad_push_kernel<<<grid, RMS_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 
 size_t vtrace_rmsprop_norm_mailbox_bytes(int32_t num_learners) {

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_f
                     "vtrace_output_layer", "vtrace_partials_mailbox_bytes",
                     "vtrace_partials_allreduce", "vtrace_head_workspace_bytes",
                     "vtrace_head_loss_and_grad", "vtrace_rmsprop_norm_mailbox_bytes",
-                    "vtrace_rmsprop_step_sharded")
+                    "vtrace_rmsprop_step_sharded", "vtrace_grad_push")
 
 
 class VtraceError(RuntimeError):
@@ -140,6 +140,9 @@ def load_library(path: str = LIB_PATH):
                                                 ctypes.c_int32, ctypes.POINTER(_RmsParams), P, P,
                                                 ctypes.c_size_t, P]
     lib.vtrace_rmsprop_step_sharded.restype = ctypes.c_int
+    lib.vtrace_grad_push.argtypes = [P, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                     ctypes.c_int32, i64, P]
+    lib.vtrace_grad_push.restype = ctypes.c_int
     lib.vtrace_head_workspace_bytes.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_int32]
     lib.vtrace_head_workspace_bytes.restype = ctypes.c_size_t
     lib.vtrace_head_loss_and_grad.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_int32] + [P] * 8 + [
@@ -562,6 +565,18 @@ def rmsprop_step_sharded(params_ptrs, mean_square, grads_ptrs, learning_rate: fl
         _ptr_array([int(p) for p in norm_mailboxes]), N, int(self_index), ctypes.byref(prm),
         _ptr(global_norm_out), workspace.ptr, workspace.nbytes, _stream(mean_square.device))
     _check(st, "vtrace_rmsprop_step_sharded")
+
+
+def grad_push(grad: torch.Tensor, recv_ptrs, self_index: int):
+    """vtrace_grad_push: this learner's fp32 gradient into slot ``self_index`` of every
+    learner's receive buffer (``recv_ptrs``: one device pointer per learner, each buffer
+    num_learners * n floats).  Marshalling only."""
+    if not (grad.is_cuda and grad.dtype == torch.float32 and grad.is_contiguous()):
+        raise ValueError("grad must be a contiguous fp32 CUDA tensor")
+    st = load_library().vtrace_grad_push(_ptr(grad), _ptr_array([int(p) for p in recv_ptrs]),
+                                         len(recv_ptrs), int(self_index), grad.numel(),
+                                         _stream(grad.device))
+    _check(st, "vtrace_grad_push")
 
 
 def output_layer(hidden: torch.Tensor, w_t: torch.Tensor, bias: torch.Tensor | None = None,

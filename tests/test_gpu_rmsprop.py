@@ -11,6 +11,8 @@ the parameter.  The
 hyperparameters cross the ABI as fp32; the oracle gets those same fp32 values.
 The clip decision and the norm are fp64 on both sides (norm rtol 1e-12).
 """
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -301,3 +303,23 @@ def test_rmsprop_sharded_learner_with_simulated_peer():
         # (keep the oracle's untouched shard equal to the kernel's for the next call)
         th_ref[hi:], ms_ref[hi:] = inp["params"][hi:], inp["mean_square"][hi:]
     assert flags[0].tolist() == [3, 3]
+
+
+def test_grad_push_into_every_learners_slot():
+    """vtrace_grad_push on one GPU (the learners' receive buffers simulated in local memory):
+    learner 1 of 3 stores its gradient into slot 1 of every receive buffer, bit for bit, and
+    touches nothing else; then the update summing the local slots equals the multi form."""
+    n, N, me = 40_000, 3, 1
+    dev = "cuda"
+    g = torch.randn(n, device=dev)
+    recv = [torch.full((N * n,), -7.0, device=dev) for _ in range(N)]
+    pkg.vtrace.grad_push(g, [r.data_ptr() for r in recv], me)
+    torch.cuda.synchronize()
+    for r in recv:
+        assert torch.equal(r[me * n:(me + 1) * n], g)
+        assert bool((r[:me * n] == -7.0).all()) and bool((r[(me + 1) * n:] == -7.0).all())
+    lib = pkg.load_library()
+    assert lib.vtrace_grad_push(None, None, 2, 0, 8, None) == 1
+    ptrs = (ctypes.c_void_p * 2)(recv[0].data_ptr(), recv[1].data_ptr())
+    assert lib.vtrace_grad_push(ctypes.c_void_p(g.data_ptr()), ptrs, 2, 2, 8, None) == 1
+    assert lib.vtrace_grad_push(ctypes.c_void_p(g.data_ptr()), ptrs, 2, 0, 6, None) == 2
