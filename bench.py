@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--collective", choices=["nvlink", "nccl"], default="nvlink",
                     help="N > 1: how the step's 8 partials are summed over the learners: "
                          "vtrace_partials_allreduce over NVLink peer memory (default) or NCCL")
+    ap.add_argument("--no-guard", action="store_true", help=argparse.SUPPRESS)  # (A/B only)
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
     ap.add_argument("--path", choices=["vtrace", "update", "head", "head_fused"], default="vtrace",
@@ -287,7 +288,8 @@ def run_ours(args):
     overlap = not args.no_overlap
     step_obj = learner.LearnerStep(T, B, A, inp["dtype"], overlap=overlap,
                                    reserve_sms=(args.reserve_sms if world > 1 else 0),
-                                   collective=args.collective, **kw)
+                                   collective=args.collective,
+                                   guard_partials=not args.no_guard, **kw)
     ws = step_obj.workspace
     s_main = step_obj.stream
 

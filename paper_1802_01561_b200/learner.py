@@ -113,7 +113,8 @@ class LearnerStep:
 
     def __init__(self, T: int, B: int, A: int, logits_dtype, *, device=None, group=None,
                  overlap: bool = True, reserve_sms: int | None = None,
-                 kernel: Callable | None = None, collective: str = "nvlink", **method_kw):
+                 kernel: Callable | None = None, collective: str = "nvlink",
+                 guard_partials: bool = True, **method_kw):
         self.T, self.B, self.A = int(T), int(B), int(A)
         self.group = group
         self.world, self.rank = _world(group)
@@ -144,6 +145,7 @@ class LearnerStep:
             raise ValueError("collective must be 'nvlink' or 'nccl'")
         self.collective = collective if (self.cuda and self.world > 1) else "none"
         self._pending: dict = {}  # partials data_ptr -> event after its collective
+        self.guard_partials = bool(guard_partials)
         if self.collective == "nvlink":
             self._setup_mailboxes()
 
@@ -178,7 +180,7 @@ class LearnerStep:
             return
         key = out["partials"].data_ptr()
         ev = self._pending.pop(key, None)
-        if ev is not None:  # that buffer's previous collective must have read it
+        if ev is not None and self.guard_partials:  # its previous collective must have read it
             self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
             self._launch(inputs, out)
