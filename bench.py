@@ -63,9 +63,10 @@ def parse():
     ap.add_argument("--reserve-sms", type=int, default=1,
                     help="N > 1: SMs the kernel leaves to the per-step NCCL collective so that "
                          "steps can overlap (0: no overlap at N > 1)")
-    ap.add_argument("--collective", choices=["nvlink", "nccl"], default="nvlink",
+    ap.add_argument("--collective", choices=["nvlink", "fused", "nccl"], default="nvlink",
                     help="N > 1: how the step's 8 partials are summed over the learners: "
-                         "vtrace_partials_allreduce over NVLink peer memory (default) or NCCL")
+                         "vtrace_partials_allreduce over NVLink peer memory (default), inside "
+                         "the V-trace kernel's last CTA (fused), or NCCL")
     ap.add_argument("--no-guard", action="store_true", help=argparse.SUPPRESS)  # (A/B only)
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
@@ -520,7 +521,11 @@ def run_ours(args):
                    "collective": ("none" if world == 1 else
                                   ("vtrace_partials_allreduce: 8 fp64 partials per step through "
                                    "peer-mapped mailboxes over NVLink, one 32-thread kernel"
-                                   if args.collective == "nvlink" else
+                                   if step_obj.collective == "nvlink" else
+                                   "inside the V-trace kernel: its last CTA exchanges the 8 "
+                                   "partials through peer-mapped mailboxes over NVLink "
+                                   "(vtrace_loss_and_grad_learners)"
+                                   if step_obj.collective == "fused" else
                                    "NCCL all_reduce of 8 fp64 partials per step")
                                   + " (side stream"
                                   + (f", {args.reserve_sms} SM reserved)" if args.reserve_sms

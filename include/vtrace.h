@@ -213,6 +213,28 @@ vt_status vtrace_loss_and_grad(int64_t T, int64_t B, int64_t A, vt_dtype logits_
                                float* vs, float* pg_advantages, void* workspace,
                                size_t workspace_bytes, vt_stream_t stream);
 
+/* vtrace_loss_and_grad for one of num_learners synchronous learners (SURVEY
+ * 8(a) a13) with the learners' sum of the partials INSIDE the kernel: the column-block
+ * kernel's last CTA stores this learner's 8 partials into its slot of every learner's
+ * mailbox (NVLink stores into peer memory), waits for every learner's slot of this call in
+ * its own mailbox and writes the sum in learner order to `partials` -- bitwise the same on
+ * every learner; no separate collective.  The call's tag is the workspace's call count, so
+ * every learner must make the same sequence of calls on workspaces initialised together,
+ * and a mailbox serves one such sequence.  mailboxes: host array of num_learners device
+ * pointers (16-byte aligned) to each learner's mailbox of
+ * vtrace_partials_mailbox_bytes(num_learners) bytes, zero-initialised once, peer-mapped.
+ * Shapes that do not take the column-block kernel: VT_ERR_SHAPE (use vtrace_loss_and_grad
+ * + vtrace_partials_allreduce).  A learner that never calls leaves the others waiting at
+ * most 20 s, then its terms read NaN.  Other arguments and errors as vtrace_loss_and_grad. */
+vt_status vtrace_loss_and_grad_learners(
+    int64_t T, int64_t B, int64_t A, vt_dtype logits_dtype, const void* behaviour_policy_logits,
+    const void* target_policy_logits, const int32_t* actions, const float* discounts,
+    const float* rewards, const float* values, const float* bootstrap_value,
+    const vt_vtrace_params* params, const vt_loss_weights* weights, void* grad_target_logits,
+    float* grad_values, double* partials, float* vs, float* pg_advantages, void* workspace,
+    size_t workspace_bytes, double* const* mailboxes, int32_t num_learners, int32_t self,
+    vt_stream_t stream);
+
 /* End-to-end variant for inputs that live in HOST memory (the actors' queue):
  * copies the seven host inputs (pinned memory recommended) into the caller's
  * device staging buffers with cudaMemcpyAsync, runs vtrace_loss_and_grad, and

@@ -906,7 +906,8 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
                                const vt_loss_weights* w, void* dlogits, float* dvalues,
                                double* partials, float* vs, float* pg_adv, float* lr,
                                float* lp, float* lm, void* ws, size_t ws_bytes,
-                               cudaStream_t st) {
+                               cudaStream_t st, double* const* mboxes = nullptr,
+                               int nlearn = 0, int self = 0) {
   if (!mu || !pi || !actions || !disc || !rew || !val || !boot) return VT_ERR_INVALID_ARG;
   if (T <= 0 || B <= 0 || A <= 0 || A > VT_MAX_ACTIONS) return VT_ERR_SHAPE;
   if (T > (1LL << 30) || B > (1LL << 30) || T * B > (1LL << 40) || T * B * A > (1LL << 46))
@@ -969,6 +970,9 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
     }
   }
   P.ws = reinterpret_cast<WsHeader*>(wsb);
+  P.nlearn = nlearn;
+  P.self = self;
+  for (int r = 0; r < 16; ++r) P.mbox[r] = (mboxes && r < nlearn) ? (void*)mboxes[r] : nullptr;
   const WsLayout wl = ws_layout(plan);
   P.recs = reinterpret_cast<TagRec*>(wsb + wl.recs);
   P.cta_partials = reinterpret_cast<double*>(wsb + wl.cta);
@@ -990,6 +994,7 @@ static vt_status common_launch(bool loss, long long T, long long B, long long A,
   const KernelChoice kc = choose_kernel(T, B, A, elem, plan, ptrs16, mu_lp, om, sms,
                                         prm->kernel, &cp);
   if (prm->kernel == VT_KERNEL_COLUMN_BLOCK && kc != K_CB) return VT_ERR_SHAPE;
+  if (nlearn > 1 && kc != K_CB) return VT_ERR_SHAPE;  // (the in-kernel exchange is cb-only)
   if (kc == K_CB && cp.plain) {
     CbMaps cm;
     std::memset(&cm, 0, sizeof(cm));
@@ -1111,6 +1116,25 @@ vt_status vtrace_loss_and_grad(int64_t T, int64_t B, int64_t A, vt_dtype dt, con
   return common_launch(true, T, B, A, dt, mu, pi, actions, discounts, rewards, values, boot,
                        params, weights, dlogits, dvalues, partials, vs, pg_adv, nullptr, nullptr,
                        nullptr, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+vt_status vtrace_loss_and_grad_learners(
+    int64_t T, int64_t B, int64_t A, vt_dtype dt, const void* mu, const void* pi,
+    const int32_t* actions, const float* discounts, const float* rewards, const float* values,
+    const float* boot, const vt_vtrace_params* params, const vt_loss_weights* weights,
+    void* dlogits, float* dvalues, double* partials, float* vs, float* pg_adv, void* ws,
+    size_t ws_bytes, double* const* mailboxes, int32_t num_learners, int32_t self,
+    vt_stream_t stream) {
+  if (!mailboxes || num_learners < 1 || num_learners > 16 || self < 0 || self >= num_learners)
+    return VT_ERR_INVALID_ARG;
+  for (int r = 0; r < num_learners; ++r) {
+    if (!mailboxes[r]) return VT_ERR_INVALID_ARG;
+    if (!aligned(mailboxes[r], 16)) return VT_ERR_ALIGNMENT;
+  }
+  return common_launch(true, T, B, A, dt, mu, pi, actions, discounts, rewards, values, boot,
+                       params, weights, dlogits, dvalues, partials, vs, pg_adv, nullptr, nullptr,
+                       nullptr, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), mailboxes,
+                       num_learners, self);
 }
 
 vt_status vtrace_loss_and_grad_from_host(

@@ -430,6 +430,45 @@ struct CbAcc {
   unsigned int clip;
 };
 
+// The learners' sum of partial k inside the kernel: this
+// learner's value goes into its slot of every learner's mailbox (value, then the call tag with
+// release semantics, NVLink stores), then the learners' slots of this call are added in
+// learner order from the own mailbox -- bitwise the same on every learner.  The tag is the
+// workspace's call epoch + 1 (every learner makes the same calls); slots alternate parity, so
+// a learner one call ahead never overwrites a slot still to be read.  A learner that never
+// publishes makes its term NaN after 20 s (no hang).
+__device__ __forceinline__ double learners_sum(const Params& P, double v, int k, unsigned int epoch) {
+  struct Slot { double v; unsigned long long tag; };
+  const unsigned long long tag = (unsigned long long)epoch + 1ull;
+  const int par = (int)(tag & 1ull), n = P.nlearn;
+  for (int r = 0; r < n; ++r) {
+    Slot* d = reinterpret_cast<Slot*>(P.mbox[r]) + ((size_t)(par * n + P.self) * NPART + k);
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(&d->v), "d"(v) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&d->tag), "l"(tag) : "memory");
+  }
+  const Slot* own = reinterpret_cast<const Slot*>(P.mbox[P.self]) + (size_t)par * n * NPART + k;
+  double s = 0.0;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < n; ++r) {
+    const Slot* q = own + (size_t)r * NPART;
+    bool late = false;
+    while (true) {
+      unsigned long long t;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(t) : "l"(&q->tag) : "memory");
+      if (t == tag) break;
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 20ull * 1000 * 1000 * 1000) { late = true; break; }
+      __nanosleep(20);
+    }
+    double x;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(x) : "l"(&q->v) : "memory");
+    s += late ? __longlong_as_double(0x7ff8000000000000ll) : x;
+  }
+  return s;
+}
+
 // ---------------------------------------------------------------------------
 // The kernel.  GEN: a Section 5.2.2 variant / App. E.3 q estimate / behaviour
 // log-probs (false: plain V-trace, that logic compiled out); MULP: the behaviour is
@@ -1075,6 +1114,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
     const double bl = __shfl_sync(0xffffffffu, x, VT_P_BASELINE_LOSS);
     const double en = __shfl_sync(0xffffffffu, x, VT_P_ENTROPY_SUM);
     if (lane == VT_P_TOTAL_LOSS) x = pg + P.c_v * bl - P.c_e * en;
+    if (P.nlearn > 1 && lane < NPART) x = learners_sum(P, x, lane, epoch);
     if (lane < NPART) P.partials[lane] = x;
     if (lane == 0) *reinterpret_cast<volatile unsigned int*>(&P.ws->epoch) = (epoch + 1u) & 0x3fffffffu;
     if (lane == 0) CB_STAMP(4);

@@ -104,6 +104,11 @@ struct Params {
   int timing_iters;
   int stride_q, stride_r;  // gridDim.x = stride_q * G + stride_r
   KLayout L;
+  // learners (vtrace_loss_and_grad_learners): the column-block kernel's last CTA adds the
+  // learners' partials through peer-mapped mailboxes ({value, tag} [2][nlearn][8])
+  int nlearn;              // <= 1: no exchange
+  int self;
+  void* mbox[16];
 };
 
 struct TmaMaps {

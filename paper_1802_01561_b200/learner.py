@@ -141,13 +141,29 @@ class LearnerStep:
             self.comm_stream = torch.cuda.Stream(self.device)
         else:
             self.stream = self.comm_stream = None
-        if collective not in ("nvlink", "nccl"):
-            raise ValueError("collective must be 'nvlink' or 'nccl'")
+        if collective not in ("nvlink", "nccl", "fused"):
+            raise ValueError("collective must be 'nvlink', 'fused' or 'nccl'")
         self.collective = collective if (self.cuda and self.world > 1) else "none"
+        if self.collective == "fused" and kernel is not None:
+            raise ValueError("collective='fused' runs the library kernel")
+        if self.collective == "fused":
+            from . import vtrace
+            if not vtrace.kernel_for(T, B, A, self.workspace_dtype(logits_dtype)).startswith(
+                    "vtrace_cb_kernel"):
+                self.collective = "nvlink"  # (the in-kernel exchange is column-block only)
         self._pending: dict = {}  # partials data_ptr -> event after its collective
         self.guard_partials = bool(guard_partials)
-        if self.collective == "nvlink":
+        if self.collective in ("nvlink", "fused"):
             self._setup_mailboxes()
+        if self.collective == "fused":
+            self.kw.update(mailboxes=self._mbox_ptrs, self_index=self.rank)
+
+    @staticmethod
+    def workspace_dtype(logits_dtype):
+        from . import vtrace
+        if isinstance(logits_dtype, int):
+            return logits_dtype
+        return {torch.float32: vtrace.VT_FLOAT32, torch.bfloat16: vtrace.VT_BFLOAT16}[logits_dtype]
 
     def _setup_mailboxes(self):
         """Every learner's mailbox in symmetric memory (peer-mapped over NVLink)."""
@@ -184,7 +200,7 @@ class LearnerStep:
             self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
             self._launch(inputs, out)
-        if self.world > 1:
+        if self.world > 1 and self.collective != "fused":
             self.comm_stream.wait_stream(self.stream)
             with torch.cuda.stream(self.comm_stream):
                 if self.collective == "nvlink":

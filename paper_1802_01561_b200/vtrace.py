@@ -39,7 +39,8 @@ EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_f
                     "vtrace_output_layer", "vtrace_partials_mailbox_bytes",
                     "vtrace_partials_allreduce", "vtrace_head_workspace_bytes",
                     "vtrace_head_loss_and_grad", "vtrace_rmsprop_norm_mailbox_bytes",
-                    "vtrace_rmsprop_step_sharded", "vtrace_grad_push")
+                    "vtrace_rmsprop_step_sharded", "vtrace_grad_push",
+                    "vtrace_loss_and_grad_learners")
 
 
 class VtraceError(RuntimeError):
@@ -98,6 +99,10 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_loss_and_grad.argtypes = [i64, i64, i64, ctypes.c_int] + [P] * 7 + [
         ctypes.POINTER(_Params), ctypes.POINTER(_Weights)] + [P] * 5 + [P, ctypes.c_size_t, P]
     lib.vtrace_loss_and_grad.restype = ctypes.c_int
+    lib.vtrace_loss_and_grad_learners.argtypes = [i64, i64, i64, ctypes.c_int] + [P] * 7 + [
+        ctypes.POINTER(_Params), ctypes.POINTER(_Weights)] + [P] * 5 + [
+        P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int32, P]
+    lib.vtrace_loss_and_grad_learners.restype = ctypes.c_int
     lib.vtrace_loss_and_grad_from_host.argtypes = [i64, i64, i64, ctypes.c_int] + [P] * 14 + [
         ctypes.POINTER(_Params), ctypes.POINTER(_Weights)] + [P] * 4 + [P, ctypes.c_size_t, P]
     lib.vtrace_loss_and_grad_from_host.restype = ctypes.c_int
@@ -308,10 +313,12 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
                   reward_mode=0, correction=CORRECTION_VTRACE, epsilon=1e-6, q_from_values=0,
                   baseline_cost=0.5, entropy_cost=0.01, overlap_previous=False,
                   workspace: Workspace | None = None, with_targets=True, out: dict | None = None,
-                  kernel=KERNEL_AUTO, sm_budget=0):
+                  kernel=KERNEL_AUTO, sm_budget=0, mailboxes=None, self_index: int = 0):
     """vtrace_loss_and_grad.  Returns dict: grad_target_logits [T,B,A] (logits
     dtype), grad_values [T,B] fp32, partials [8] fp64 (device), and, if
-    with_targets, vs and pg_advantages [T,B] fp32."""
+    with_targets, vs and pg_advantages [T,B] fp32.  With ``mailboxes`` (one peer-mapped
+    device pointer per learner) it is vtrace_loss_and_grad_learners: ``partials`` is the
+    sum over the learners, exchanged inside the kernel (``self_index`` = this learner)."""
     lib = load_library()
     T, B, A, mu_lp = _shapes(behaviour_logits, target_logits, actions, discounts, rewards, values,
                              bootstrap_value)
@@ -333,6 +340,16 @@ def loss_and_grad(behaviour_logits, target_logits, actions, discounts, rewards, 
     p = params(rho_bar, c_bar, pg_rho_bar, lambda_, reward_mode, correction, epsilon, q_from_values,
                mu_lp, int(overlap_previous), kernel, sm_budget)
     w = _Weights(float(baseline_cost), float(entropy_cost))
+    if mailboxes is not None:
+        mb = _ptr_array([int(m) for m in mailboxes])
+        st = lib.vtrace_loss_and_grad_learners(
+            T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions),
+            _ptr(discounts), _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p),
+            ctypes.byref(w), _ptr(out["grad_target_logits"]), _ptr(out["grad_values"]),
+            _ptr(out["partials"]), _ptr(out.get("vs")), _ptr(out.get("pg_advantages")), ws.ptr,
+            ws.nbytes, mb, len(mailboxes), int(self_index), _stream(dev))
+        _check(st, "vtrace_loss_and_grad_learners")
+        return out
     st = lib.vtrace_loss_and_grad(
         T, B, A, dt, _ptr(behaviour_logits), _ptr(target_logits), _ptr(actions), _ptr(discounts),
         _ptr(rewards), _ptr(values), _ptr(bootstrap_value), ctypes.byref(p), ctypes.byref(w),

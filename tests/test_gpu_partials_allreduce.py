@@ -47,3 +47,42 @@ def test_partials_allreduce_learners_on_one_gpu(n):
 def test_partials_allreduce_in_place_many_calls():
     """Both mailbox parities, many calls in a row, output over the input."""
     _run(2, calls=40, inplace=True, seed=11)
+
+
+@pytest.mark.gpu
+def test_learners_sum_inside_the_vtrace_kernel_with_simulated_peer():
+    """vtrace_loss_and_grad_learners on one GPU, learner 0 of 2: the peer is simulated by its
+    slots in learner 0's mailbox, written before each call with the call's tag (the
+    workspace's call count + 1).  The kernel's partials must be (own, bitwise as the plain
+    call) + (peer) in learner order, the gradients unchanged, and learner 0's own slot must
+    land in the peer's mailbox."""
+    import paper_1802_01561_b200 as pkg
+    from paper_1802_01561_b200 import workload as wl
+    inp = wl.make_inputs("large", T=24, B=512)
+    T, B, A = inp["T"], inp["B"], inp["A"]
+    assert pkg.kernel_for(T, B, A, inp["dtype"]).startswith("vtrace_cb_kernel")
+    d = pkg.tensors_from_workload(inp, "cuda")
+    args = [d[k] for k in vt.INPUT_NAMES]
+    ws_plain = pkg.Workspace(T, B, A, inp["dtype"])
+    ws = pkg.Workspace(T, B, A, inp["dtype"])
+    nb = vt.partials_mailbox_bytes(2)
+    mb = [torch.zeros(nb // 8, dtype=torch.float64, device="cuda") for _ in range(2)]
+    g = torch.Generator().manual_seed(3)
+    for call in range(4):
+        plain = pkg.loss_and_grad(*args, workspace=ws_plain, reward_mode=inp["reward_mode"])
+        peer = torch.randn(8, dtype=torch.float64, generator=g) * 100
+        tag = call + 1
+        base = ((tag & 1) * 2 + 1) * 8  # slots [parity][learner 1][k]
+        for k in range(8):
+            mb[0][2 * (base + k)] = float(peer[k])
+            mb[0].view(torch.int64)[2 * (base + k) + 1] = tag
+        out = pkg.loss_and_grad(*args, workspace=ws, reward_mode=inp["reward_mode"],
+                                mailboxes=[m.data_ptr() for m in mb], self_index=0)
+        torch.cuda.synchronize()
+        own = plain["partials"].cpu()
+        assert torch.equal(out["partials"].cpu(), (0.0 + own) + peer)
+        assert torch.equal(out["grad_target_logits"], plain["grad_target_logits"])
+        assert torch.equal(out["grad_values"], plain["grad_values"])
+        mine = ((tag & 1) * 2 + 0) * 8  # learner 0's slots in the peer's mailbox
+        got = torch.tensor([float(mb[1][2 * (mine + k)]) for k in range(8)], dtype=torch.float64)
+        assert torch.equal(got, own)
