@@ -63,11 +63,14 @@ def parse():
     ap.add_argument("--reserve-sms", type=int, default=1,
                     help="N > 1: SMs the kernel leaves to the per-step NCCL collective so that "
                          "steps can overlap (0: no overlap at N > 1)")
-    ap.add_argument("--collective", choices=["nvlink", "fused", "nccl"], default="nvlink",
+    ap.add_argument("--collective", choices=["nvlink", "fused", "nccl", "off"], default="nvlink",
                     help="N > 1: how the step's 8 partials are summed over the learners: "
                          "vtrace_partials_allreduce over NVLink peer memory (default), inside "
                          "the V-trace kernel's last CTA (fused), or NCCL")
     ap.add_argument("--no-guard", action="store_true", help=argparse.SUPPRESS)  # (A/B only)
+    ap.add_argument("--exchange-every", type=int, default=8,
+                    help="N > 1, --collective nvlink: steps whose partials are exchanged together "
+                         "(one side-stream kernel per batch; 1 = every step)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
     ap.add_argument("--path", choices=["vtrace", "update", "head", "head_fused"], default="vtrace",
@@ -290,7 +293,10 @@ def run_ours(args):
     step_obj = learner.LearnerStep(T, B, A, inp["dtype"], overlap=overlap,
                                    reserve_sms=(args.reserve_sms if world > 1 else 0),
                                    collective=args.collective,
-                                   guard_partials=not args.no_guard, **kw)
+                                   guard_partials=not args.no_guard,
+                                   exchange_every=(args.exchange_every
+                                                   if args.collective == "nvlink" else 1),
+                                   **kw)
     ws = step_obj.workspace
     s_main = step_obj.stream
 
@@ -384,7 +390,7 @@ def run_ours(args):
     # multi-GPU correctness of the step's collective (untimed): one more step through the
     # product API against an NCCL all_reduce of the same per-rank partials
     collective_check = None
-    if world > 1:
+    if world > 1 and step_obj.collective != "off":
         o = outs[0]
         pkg.loss_and_grad(*[sets[0][k] for k in vt.INPUT_NAMES], workspace=ws, out=o, **kw)
         torch.cuda.synchronize()
@@ -521,6 +527,8 @@ def run_ours(args):
                    "collective": ("none" if world == 1 else
                                   ("vtrace_partials_allreduce: 8 fp64 partials per step through "
                                    "peer-mapped mailboxes over NVLink, one 32-thread kernel"
+                                   + (f" per {step_obj.exchange_every} steps (batched)"
+                                      if step_obj.exchange_every > 1 else " per step")
                                    if step_obj.collective == "nvlink" else
                                    "inside the V-trace kernel: its last CTA exchanges the 8 "
                                    "partials through peer-mapped mailboxes over NVLink "

@@ -89,7 +89,86 @@ __global__ void __launch_bounds__(32) partials_allreduce_kernel(const double* __
   if (k == 0) *reinterpret_cast<volatile unsigned long long*>(counter) = tag;
 }
 
+// The batched form: `batch` steps' partials in one call (thread t: step t / 8, partial t % 8);
+// slots [parity][learner][step][k].  One call per `batch` steps keeps the side stream's
+// per-step launches off the learners' kernel chain.
+constexpr int kMaxBatch = 32;
+
+struct PartialsPtrs {
+  double* p[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(256) partials_allreduce_batch_kernel(PartialsPtrs parts,
+                                                                       int batch, Mailboxes mb,
+                                                                       int n, int self,
+                                                                       unsigned long long* counter) {
+  const int t = threadIdx.x;
+  const unsigned long long tag = *reinterpret_cast<volatile unsigned long long*>(counter) + 1ull;
+  const int par = (int)(tag & 1ull);
+  const int per = batch * VT_P_COUNT;
+  double s = 0.0;
+  if (t < per) {
+    const double v = parts.p[t / VT_P_COUNT][t % VT_P_COUNT];
+    for (int r = 0; r < n; ++r) {
+      Slot* d = mb.p[r] + ((size_t)(par * n + self) * per + t);
+      st_relaxed_f64(&d->v, v);
+      st_release_u64(&d->tag, tag);
+    }
+    const Slot* own = mb.p[self] + (size_t)par * n * per + t;
+    const unsigned long long t0 = now_ns();
+    for (int r = 0; r < n; ++r) {
+      const Slot* q = own + (size_t)r * per;
+      bool late = false;
+      while (ld_acquire_u64(&q->tag) != tag) {
+        __nanosleep(20);
+        if (now_ns() - t0 > kTimeoutNs) {
+          late = true;
+          break;
+        }
+      }
+      s += late ? __longlong_as_double(0x7ff8000000000000ll) : ld_relaxed_f64(&q->v);
+    }
+  }
+  __syncthreads();
+  if (t < per) parts.p[t / VT_P_COUNT][t % VT_P_COUNT] = s;
+  if (t == 0) *reinterpret_cast<volatile unsigned long long*>(counter) = tag;
+}
+
 }  // namespace vtpa
+
+extern "C" size_t vtrace_partials_mailbox_bytes_batched(int32_t num_learners, int32_t batch) {
+  if (num_learners < 1 || num_learners > vtpa::kMaxLearners || batch < 1 || batch > vtpa::kMaxBatch)
+    return 0;
+  return (size_t)2 * (size_t)num_learners * (size_t)batch * VT_P_COUNT * sizeof(vtpa::Slot);
+}
+
+extern "C" vt_status vtrace_partials_allreduce_batched(double* const* partials, int32_t batch,
+                                                       double* const* mailboxes,
+                                                       int32_t num_learners, int32_t self,
+                                                       uint64_t* counter, vt_stream_t stream) {
+  using namespace vtpa;
+  if (!partials || !mailboxes || !counter) return VT_ERR_INVALID_ARG;
+  if (batch < 1 || batch > kMaxBatch) return VT_ERR_INVALID_ARG;
+  if (num_learners < 1 || num_learners > kMaxLearners || self < 0 || self >= num_learners)
+    return VT_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(counter) & 7) return VT_ERR_ALIGNMENT;
+  PartialsPtrs pp{};
+  for (int m = 0; m < batch; ++m) {
+    if (!partials[m]) return VT_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(partials[m]) & 7) return VT_ERR_ALIGNMENT;
+    pp.p[m] = partials[m];
+  }
+  Mailboxes mb{};
+  for (int r = 0; r < num_learners; ++r) {
+    if (!mailboxes[r]) return VT_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(mailboxes[r]) & 15) return VT_ERR_ALIGNMENT;
+    mb.p[r] = reinterpret_cast<Slot*>(mailboxes[r]);
+  }
+  const int threads = ((batch * VT_P_COUNT + 31) / 32) * 32;
+  partials_allreduce_batch_kernel<<<1, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      pp, batch, mb, num_learners, self, reinterpret_cast<unsigned long long*>(counter));
+  return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
+}
 
 extern "C" size_t vtrace_partials_mailbox_bytes(int32_t num_learners) {
   if (num_learners < 1 || num_learners > vtpa::kMaxLearners) return 0;

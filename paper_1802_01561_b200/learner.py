@@ -105,7 +105,12 @@ class LearnerStep:
     collective:   how the partials are summed over the learners at N > 1 on GPUs:
                   "nvlink" (default) -- vtrace_partials_allreduce, one 32-thread kernel
                   that exchanges the 64 bytes through peer-mapped mailboxes in
-                  symmetric memory; "nccl" -- torch.distributed.all_reduce.
+                  symmetric memory; "fused" -- inside the V-trace kernel's last CTA
+                  (vtrace_loss_and_grad_learners); "nccl" -- torch.distributed.all_reduce.
+    exchange_every: with "nvlink", exchange the partials of this many steps together
+                  (vtrace_partials_allreduce_batched, one side-stream kernel per batch; each
+                  step's sums are still produced, in place, once its batch is exchanged;
+                  join() exchanges a partial batch).
     A step's kernel never overwrites a partials buffer whose previous collective is
     still pending: it waits for that collective's event (with buffers rotated over R
     sets, the collective of R steps ago).
@@ -114,7 +119,7 @@ class LearnerStep:
     def __init__(self, T: int, B: int, A: int, logits_dtype, *, device=None, group=None,
                  overlap: bool = True, reserve_sms: int | None = None,
                  kernel: Callable | None = None, collective: str = "nvlink",
-                 guard_partials: bool = True, **method_kw):
+                 guard_partials: bool = True, exchange_every: int = 1, **method_kw):
         self.T, self.B, self.A = int(T), int(B), int(A)
         self.group = group
         self.world, self.rank = _world(group)
@@ -141,8 +146,9 @@ class LearnerStep:
             self.comm_stream = torch.cuda.Stream(self.device)
         else:
             self.stream = self.comm_stream = None
-        if collective not in ("nvlink", "nccl", "fused"):
-            raise ValueError("collective must be 'nvlink', 'fused' or 'nccl'")
+        if collective not in ("nvlink", "nccl", "fused", "off"):
+            raise ValueError("collective must be 'nvlink', 'fused', 'nccl' (or 'off': A/B only, "
+                             "no exchange)")
         self.collective = collective if (self.cuda and self.world > 1) else "none"
         if self.collective == "fused" and kernel is not None:
             raise ValueError("collective='fused' runs the library kernel")
@@ -153,6 +159,12 @@ class LearnerStep:
                 self.collective = "nvlink"  # (the in-kernel exchange is column-block only)
         self._pending: dict = {}  # partials data_ptr -> event after its collective
         self.guard_partials = bool(guard_partials)
+        self.exchange_every = int(exchange_every)
+        if not 1 <= self.exchange_every <= 32:
+            raise ValueError("exchange_every must be in 1..32")
+        if self.exchange_every > 1 and self.collective == "nccl":
+            raise ValueError("exchange_every > 1 needs collective='nvlink'")
+        self._batch: list = []  # (key, partials) of the steps not exchanged yet
         if self.collective in ("nvlink", "fused"):
             self._setup_mailboxes()
         if self.collective == "fused":
@@ -170,7 +182,8 @@ class LearnerStep:
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
         from . import vtrace
-        nbytes = vtrace.partials_mailbox_bytes(self.world)
+        nbytes = (vtrace.partials_mailbox_bytes(self.world) if self.exchange_every == 1 else
+                  vtrace.partials_mailbox_bytes_batched(self.world, self.exchange_every))
         if nbytes <= 0:
             raise ValueError(f"collective='nvlink' supports up to 16 learners, not {self.world}")
         with torch.cuda.device(self.device):
@@ -195,12 +208,21 @@ class LearnerStep:
             allreduce_partials(out["partials"], self.group)
             return
         key = out["partials"].data_ptr()
+        if any(k == key for k, _ in self._batch):  # (reused before its exchange: flush first)
+            self._flush()
         ev = self._pending.pop(key, None)
         if ev is not None and self.guard_partials:  # its previous collective must have read it
             self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
             self._launch(inputs, out)
-        if self.world > 1 and self.collective != "fused":
+        if self.world > 1 and self.collective == "nvlink" and self.exchange_every > 1:
+            # the steps' partials exchanged together, one side-stream kernel per
+            # exchange_every steps (each step's sums still produced, in place)
+            self._batch.append((key, out["partials"]))
+            if len(self._batch) == self.exchange_every:
+                self._flush()
+            return
+        if self.world > 1 and self.collective not in ("fused", "off"):
             self.comm_stream.wait_stream(self.stream)
             with torch.cuda.stream(self.comm_stream):
                 if self.collective == "nvlink":
@@ -213,9 +235,26 @@ class LearnerStep:
                 ev.record(self.comm_stream)
             self._pending[key] = ev
 
+    def _flush(self):
+        """Exchange the batched steps' partials (side stream, one kernel)."""
+        if not self._batch:
+            return
+        from . import vtrace
+        self.comm_stream.wait_stream(self.stream)
+        with torch.cuda.stream(self.comm_stream):
+            vtrace.partials_allreduce_batched([p for _, p in self._batch], self._mbox_ptrs,
+                                              self.rank, self._counter)
+            ev = torch.cuda.Event()
+            ev.record(self.comm_stream)
+        for k, _ in self._batch:
+            self._pending[k] = ev
+        self._batch = []
+
     def join(self):
-        """The main stream waits for the outstanding collectives."""
+        """The main stream waits for the outstanding collectives (a partial batch is
+        exchanged first: every learner joins at the same points)."""
         if self.cuda and self.world > 1:
+            self._flush()
             self.stream.wait_stream(self.comm_stream)
             self._pending.clear()
 

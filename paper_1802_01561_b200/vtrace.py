@@ -40,7 +40,8 @@ EXPORTED_SYMBOLS = ("vtrace_workspace_bytes", "vtrace_workspace_init", "vtrace_f
                     "vtrace_partials_allreduce", "vtrace_head_workspace_bytes",
                     "vtrace_head_loss_and_grad", "vtrace_rmsprop_norm_mailbox_bytes",
                     "vtrace_rmsprop_step_sharded", "vtrace_grad_push",
-                    "vtrace_loss_and_grad_learners")
+                    "vtrace_loss_and_grad_learners", "vtrace_partials_mailbox_bytes_batched",
+                    "vtrace_partials_allreduce_batched")
 
 
 class VtraceError(RuntimeError):
@@ -136,6 +137,13 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_partials_allreduce.argtypes = [P, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
                                               ctypes.c_int32, P, P, P]
     lib.vtrace_partials_allreduce.restype = ctypes.c_int
+    lib.vtrace_partials_mailbox_bytes_batched.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    lib.vtrace_partials_mailbox_bytes_batched.restype = ctypes.c_size_t
+    lib.vtrace_partials_allreduce_batched.argtypes = [ctypes.POINTER(ctypes.c_void_p),
+                                                      ctypes.c_int32,
+                                                      ctypes.POINTER(ctypes.c_void_p),
+                                                      ctypes.c_int32, ctypes.c_int32, P, P]
+    lib.vtrace_partials_allreduce_batched.restype = ctypes.c_int
     lib.vtrace_rmsprop_norm_mailbox_bytes.argtypes = [ctypes.c_int32]
     lib.vtrace_rmsprop_norm_mailbox_bytes.restype = ctypes.c_size_t
     lib.vtrace_rmsprop_step_sharded.argtypes = [i64, ctypes.POINTER(ctypes.c_void_p), P,
@@ -741,3 +749,27 @@ def head_loss_and_grad(hidden, w_t, bias, behaviour_logits, actions, discounts, 
         _ptr(out["partials"]), ws.ptr, ws.nbytes, _stream(dev))
     _check(st, "vtrace_head_loss_and_grad")
     return out
+
+
+def partials_mailbox_bytes_batched(num_learners: int, batch: int) -> int:
+    return int(load_library().vtrace_partials_mailbox_bytes_batched(int(num_learners), int(batch)))
+
+
+def partials_allreduce_batched(partials_list, mailbox_ptrs, self_index: int,
+                               counter: torch.Tensor):
+    """Sum over the learners of several steps' [8] fp64 partials, in place, one kernel
+    (vtrace_partials_allreduce_batched).  Marshalling only."""
+    if not 1 <= len(partials_list) <= 32:
+        raise ValueError("partials_allreduce_batched: 1..32 partials tensors")
+    dev = partials_list[0].device
+    for t in partials_list:
+        if t.dtype != torch.float64 or t.numel() != 8 or not t.is_contiguous() or t.device != dev:
+            raise ValueError("partials_allreduce_batched: contiguous float64 tensors of 8")
+    if counter.dtype != torch.int64 or counter.numel() != 1 or counter.device != dev:
+        raise ValueError("partials_allreduce_batched: counter must be one int64 on the device")
+    pa = _ptr_array([t.data_ptr() for t in partials_list])
+    mb = _ptr_array([int(p) for p in mailbox_ptrs])
+    st = load_library().vtrace_partials_allreduce_batched(pa, len(partials_list), mb,
+                                                          len(mailbox_ptrs), int(self_index),
+                                                          _ptr(counter), _stream(dev))
+    _check(st, "vtrace_partials_allreduce_batched")

@@ -86,3 +86,37 @@ def test_learners_sum_inside_the_vtrace_kernel_with_simulated_peer():
         mine = ((tag & 1) * 2 + 0) * 8  # learner 0's slots in the peer's mailbox
         got = torch.tensor([float(mb[1][2 * (mine + k)]) for k in range(8)], dtype=torch.float64)
         assert torch.equal(got, own)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,batches", [(2, [8, 8, 3]), (4, [1, 32, 5])])
+def test_partials_allreduce_batched(n, batches):
+    """vtrace_partials_allreduce_batched: several steps' partials summed over the learners
+    in one kernel, in place, learner order, bitwise identical on every learner; batch sizes
+    vary from call to call (every learner the same) within the mailbox's maximum."""
+    dev = torch.device("cuda", 0)
+    bmax = max(batches)
+    nb = vt.partials_mailbox_bytes_batched(n, bmax)
+    assert nb == 2 * n * bmax * 8 * 16
+    mbs = [torch.zeros(nb // 8, dtype=torch.float64, device=dev) for _ in range(n)]
+    ptrs = [m.data_ptr() for m in mbs]
+    counters = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(n)]
+    streams = [torch.cuda.Stream(dev) for _ in range(n)]
+    g = torch.Generator().manual_seed(7 + n)
+    for call, m in enumerate(batches):
+        parts = [[(torch.randn(8, dtype=torch.float64, generator=g) * 10 ** (r % 3)).to(dev)
+                  for _ in range(m)] for r in range(n)]
+        host = [[p.cpu() for p in pr] for pr in parts]
+        torch.cuda.synchronize()
+        for r in reversed(range(n)):
+            with torch.cuda.stream(streams[r]):
+                vt.partials_allreduce_batched(parts[r], ptrs, r, counters[r])
+        torch.cuda.synchronize()
+        for s in range(m):
+            expect = torch.zeros(8, dtype=torch.float64)
+            for r in range(n):
+                expect = expect + host[r][s]
+            for r in range(n):
+                assert torch.equal(parts[r][s].cpu(), expect), (call, s, r)
+    for c in counters:
+        assert int(c.item()) == len(batches)
