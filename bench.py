@@ -68,9 +68,10 @@ def parse():
                          "vtrace_partials_allreduce over NVLink peer memory (default), inside "
                          "the V-trace kernel's last CTA (fused), or NCCL")
     ap.add_argument("--no-guard", action="store_true", help=argparse.SUPPRESS)  # (A/B only)
-    ap.add_argument("--exchange-every", type=int, default=8,
+    ap.add_argument("--exchange-every", type=int, default=1,
                     help="N > 1, --collective nvlink: steps whose partials are exchanged together "
-                         "(one side-stream kernel per batch; 1 = every step)")
+                         "in one kernel on the step's stream (A/B; 1 = every step on the side "
+                         "stream, the default)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
     ap.add_argument("--path", choices=["vtrace", "update", "head", "head_fused"], default="vtrace",

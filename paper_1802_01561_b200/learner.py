@@ -107,10 +107,13 @@ class LearnerStep:
                   that exchanges the 64 bytes through peer-mapped mailboxes in
                   symmetric memory; "fused" -- inside the V-trace kernel's last CTA
                   (vtrace_loss_and_grad_learners); "nccl" -- torch.distributed.all_reduce.
-    exchange_every: with "nvlink", exchange the partials of this many steps together
-                  (vtrace_partials_allreduce_batched, one side-stream kernel per batch; each
-                  step's sums are still produced, in place, once its batch is exchanged;
-                  join() exchanges a partial batch).
+    exchange_every: with "nvlink" and > 1, exchange the partials of this many steps
+                  together in one kernel on the step's own stream
+                  (vtrace_partials_allreduce_batched; each step's sums are still produced, in
+                  place, once its batch is exchanged; join() exchanges a partial batch).
+                  Measured slower than the per-step side-stream exchange (the step's stream
+                  then waits for the slowest learner every batch):
+                  default 1.
     A step's kernel never overwrites a partials buffer whose previous collective is
     still pending: it waits for that collective's event (with buffers rotated over R
     sets, the collective of R steps ago).
@@ -210,18 +213,18 @@ class LearnerStep:
         key = out["partials"].data_ptr()
         if any(k == key for k, _ in self._batch):  # (reused before its exchange: flush first)
             self._flush()
+        if self.collective == "nvlink" and self.exchange_every > 1 and self.world > 1:
+            with torch.cuda.stream(self.stream):
+                self._launch(inputs, out)
+            self._batch.append((key, out["partials"]))
+            if len(self._batch) == self.exchange_every:
+                self._flush()
+            return
         ev = self._pending.pop(key, None)
         if ev is not None and self.guard_partials:  # its previous collective must have read it
             self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
             self._launch(inputs, out)
-        if self.world > 1 and self.collective == "nvlink" and self.exchange_every > 1:
-            # the steps' partials exchanged together, one side-stream kernel per
-            # exchange_every steps (each step's sums still produced, in place)
-            self._batch.append((key, out["partials"]))
-            if len(self._batch) == self.exchange_every:
-                self._flush()
-            return
         if self.world > 1 and self.collective not in ("fused", "off"):
             self.comm_stream.wait_stream(self.stream)
             with torch.cuda.stream(self.comm_stream):
@@ -236,18 +239,15 @@ class LearnerStep:
             self._pending[key] = ev
 
     def _flush(self):
-        """Exchange the batched steps' partials (side stream, one kernel)."""
+        """Exchange the batched steps' partials: one kernel on the step's own stream (no
+        cross-stream edges in a captured graph; the stream order keeps a buffer from being
+        refilled before its exchange)."""
         if not self._batch:
             return
         from . import vtrace
-        self.comm_stream.wait_stream(self.stream)
-        with torch.cuda.stream(self.comm_stream):
+        with torch.cuda.stream(self.stream):
             vtrace.partials_allreduce_batched([p for _, p in self._batch], self._mbox_ptrs,
                                               self.rank, self._counter)
-            ev = torch.cuda.Event()
-            ev.record(self.comm_stream)
-        for k, _ in self._batch:
-            self._pending[k] = ev
         self._batch = []
 
     def join(self):
