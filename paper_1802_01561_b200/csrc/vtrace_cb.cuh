@@ -148,6 +148,32 @@ __device__ __forceinline__ void mbar_wait_sleep32(uint32_t addr, uint32_t phase)
   }
 }
 
+// the producer's wait for a stage's release (A/B: CB_PROD_WAIT 0 = try_wait loop,
+// 1 = try_wait with a suspend-time hint of CB_PROD_HINT ns, 2 = test_wait + nanosleep)
+#ifndef CB_PROD_WAIT
+#define CB_PROD_WAIT 0
+#endif
+#ifndef CB_PROD_HINT
+#define CB_PROD_HINT 500
+#endif
+__device__ __forceinline__ void mbar_wait_prod32(uint32_t addr, uint32_t phase) {
+#if CB_PROD_WAIT == 1
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITP_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITP_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase), "r"((uint32_t)CB_PROD_HINT)
+      : "memory");
+#elif CB_PROD_WAIT == 2
+  mbar_wait_sleep32(addr, phase);
+#else
+  mbar_wait32(addr, phase);
+#endif
+}
+
 __device__ __forceinline__ void mbar_arrive32(uint32_t addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
@@ -654,7 +680,7 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int j = 0; j < C.J; ++j) {
-        mbar_wait32(done0 + 8u * s, ph);
+        mbar_wait_prod32(done0 + 8u * s, ph);
         if (j == 0) {
           // (programmatic dependent launch: the first global write waits for the previous
           // kernel on the stream).  The call's epoch (it tags the partial-sum records) is
