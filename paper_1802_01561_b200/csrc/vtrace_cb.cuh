@@ -438,10 +438,16 @@ __device__ __forceinline__ void cb_stats(const LT* zrow, const LT* mrow, int a,
 
 // What X(j) hands to Y(j) for one lane's row (a3-a8 results that do not need the carry).
 
+#ifndef CB_KEEPZ
+#define CB_KEEPZ 1  // keep the target row's packed bf16 words in registers for a11 (A/B: 0)
+#endif
 template <int A_CT>
 struct CbSt {
 #if !CB_EBUF
   float2 e[(A_CT + 1) / 2];  // the target row's exps (a11 reuses them)
+#endif
+#if CB_KEEPZ
+  uint32_t zw[(A_CT + 1) / 2];  // (bf16, even A) the target row's packed words
 #endif
   double G, D;               // suffix composition of this row's step with the warp's later steps
   double td, rho_pg;         // r_t + gamma_t V_{t+1} - V_t; rho_pg_t
@@ -842,6 +848,12 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       S.pa = ea_c * inv_S;                         // pi(a), relative accuracy
       S.za = za;
       S.ea_raw = R.ea_raw;
+#if CB_KEEPZ
+      if constexpr (sizeof(LT) == 2 && A_CT % 2 == 0) {
+#pragma unroll
+        for (int k = 0; k < NPc; ++k) S.zw[k] = reinterpret_cast<const uint32_t*>(zrow)[k];
+      }
+#endif
       S.a = a;
       S.row_ok = row_ok;
       if constexpr (!LOSS) {  // carry-free outputs of vtrace_from_logits
@@ -921,7 +933,18 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
         const float2 k1 = f2(ce * S.inv_S), k0 = f2(alpha * S.inv_S);
         LT* zw = reinterpret_cast<LT*>(sb + C.pi + zoff);
         float2 zr[NPc];
+#if CB_KEEPZ
+        if constexpr (sizeof(LT) == 2 && A_CT % 2 == 0) {
+#pragma unroll
+          for (int k = 0; k < NPc; ++k)
+            zr[k] = make_float2(__uint_as_float(__byte_perm(S.zw[k], 0u, 0x1044)),
+                                __uint_as_float(S.zw[k] & 0xffff0000u));
+        } else {
+          cb_load_pairs<LT, A_CT>(zw, zr);
+        }
+#else
         cb_load_pairs<LT, A_CT>(zw, zr);  // the target row again (smem)
+#endif
 #if CB_EBUF
         float2 er[NPc];
         {
