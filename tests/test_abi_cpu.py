@@ -272,3 +272,47 @@ def test_head_loss_and_grad_host_checks(lib):
     assert call(h=ctypes.c_void_p(base + 8)) == 5
     assert call(nbytes=16) == 6
     assert call(ws=None) == 6
+
+
+def test_round2_entry_points_host_checks(lib):
+    """Host-side argument checks of the round-2 entry points, before any device work:
+    vtrace_partials_allreduce_batched, vtrace_grad_push, vtrace_rmsprop_step_sharded,
+    vtrace_loss_and_grad_learners (NULL -> 1, shape -> 2, alignment -> 5)."""
+    P = ctypes.c_void_p
+    p = P(4096)
+    two = (ctypes.c_void_p * 2)(8192, 12288)
+    # batched partials sum
+    f = lib.vtrace_partials_allreduce_batched
+    assert lib.vtrace_partials_mailbox_bytes_batched(2, 0) == 0
+    assert lib.vtrace_partials_mailbox_bytes_batched(2, 33) == 0
+    assert lib.vtrace_partials_mailbox_bytes_batched(2, 4) == 2 * 2 * 4 * 8 * 16
+    assert f(None, 1, two, 2, 0, p, None) == 1
+    assert f(two, 0, two, 2, 0, p, None) == 1
+    assert f(two, 33, two, 2, 0, p, None) == 1
+    assert f(two, 2, two, 2, 2, p, None) == 1
+    assert f(two, 2, two, 2, 0, P(4100), None) == 5
+    assert f((ctypes.c_void_p * 2)(8192, 12292), 2, two, 2, 0, p, None) == 5
+    # gradient push
+    g = lib.vtrace_grad_push
+    assert g(None, two, 2, 0, 8, None) == 1
+    assert g(p, None, 2, 0, 8, None) == 1
+    assert g(p, two, 2, 2, 8, None) == 1
+    assert g(p, two, 2, 0, 6, None) == 2
+    assert g(P(4100), two, 2, 0, 8, None) == 5
+    # sharded update
+    prm = vt._RmsParams(6e-4, 0.99, 0.01, 40.0)
+    h = lib.vtrace_rmsprop_step_sharded
+    fl = (ctypes.c_void_p * 2)(16384, 16392)
+    assert h(8, None, p, two, fl, two, 2, 0, ctypes.byref(prm), None, None, 0, None) == 1
+    assert h(8, two, p, two, None, two, 2, 0, ctypes.byref(prm), None, None, 0, None) == 1
+    assert h(8, two, p, two, fl, None, 2, 0, ctypes.byref(prm), None, None, 0, None) == 1
+    assert h(8, two, p, two, fl, two, 2, 3, ctypes.byref(prm), None, None, 0, None) == 1
+    # learners' V-trace
+    w = vt._Weights(0.5, 0.01)
+    q = vt.params()
+    k = lib.vtrace_loss_and_grad_learners
+    args = [10, 8, 18, 1] + [p] * 7 + [ctypes.byref(q), ctypes.byref(w)] + [p] * 5 + [p, 0]
+    assert k(*args, None, 2, 0, None) == 1
+    assert k(*args, two, 0, 0, None) == 1
+    assert k(*args, two, 2, 2, None) == 1
+    assert k(*args, (ctypes.c_void_p * 2)(8192, 12296), 2, 0, None) == 5
