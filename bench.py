@@ -68,10 +68,10 @@ def parse():
                          "vtrace_partials_allreduce over NVLink peer memory (default), inside "
                          "the V-trace kernel's last CTA (fused), or NCCL")
     ap.add_argument("--no-guard", action="store_true", help=argparse.SUPPRESS)  # (A/B only)
-    ap.add_argument("--exchange-every", type=int, default=1,
+    ap.add_argument("--exchange-every", type=int, default=0,
                     help="N > 1, --collective nvlink: steps whose partials are exchanged together "
-                         "in one kernel on the step's stream (A/B; 1 = every step on the side "
-                         "stream, the default)")
+                         "in one side-stream kernel (1 = every step; 0 = auto: 4 when at least 8 "
+                         "input sets rotate, else 1)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="plain stream order between steps (no programmatic dependent launch)")
     ap.add_argument("--path", choices=["vtrace", "update", "head", "head_fused"], default="vtrace",
@@ -295,8 +295,9 @@ def run_ours(args):
                                    reserve_sms=(args.reserve_sms if world > 1 else 0),
                                    collective=args.collective,
                                    guard_partials=not args.no_guard,
-                                   exchange_every=(args.exchange_every
-                                                   if args.collective == "nvlink" else 1),
+                                   exchange_every=(1 if args.collective != "nvlink" else
+                                                   args.exchange_every if args.exchange_every > 0
+                                                   else (4 if R >= 8 else 1)),
                                    **kw)
     ws = step_obj.workspace
     s_main = step_obj.stream

@@ -416,18 +416,20 @@ vt_status vtrace_partials_allreduce(const double* partials, double* const* mailb
                                    int32_t num_learners, int32_t self, uint64_t* counter,
                                    double* out, vt_stream_t stream);
 
-/* The same sum for `batch` steps at once (1..32): partials[m] (host array of device
- * pointers, 8-byte aligned) is step m's double[VT_P_COUNT], replaced in place by the sum over
- * the learners.  One launch per `batch` steps: in a CUDA graph the side stream's per-step
- * launch costs the learners' kernel chain ~2.5 us a step at N = 4.
- * Mailboxes of vtrace_partials_mailbox_bytes_batched(num_learners, batch_max) bytes,
- * zero-initialised once; every learner makes the same sequence of calls with the same batch
- * sizes (batch <= batch_max); a mailbox serves one such sequence.  Errors as
- * vtrace_partials_allreduce (batch out of range: VT_ERR_INVALID_ARG). */
-size_t vtrace_partials_mailbox_bytes_batched(int32_t num_learners, int32_t batch);
+/* The same sum for `batch` steps at once: partials[m] (host array of device pointers,
+ * 8-byte aligned) is step m's double[VT_P_COUNT], replaced in place by the sum over the
+ * learners.  One launch per `batch` steps: in a CUDA graph the side stream's per-step launch
+ * costs the learners' kernel chain ~2.5 us a step at N = 4.  Mailboxes
+ * of vtrace_partials_mailbox_bytes_batched(num_learners, batch_max) bytes (batch_max 1..32),
+ * zero-initialised once; every call passes that batch_max and a batch of 1..batch_max steps;
+ * every learner makes the same sequence of calls with the same batch sizes; a mailbox serves
+ * one such sequence.  Errors as vtrace_partials_allreduce (batch or batch_max out of range:
+ * VT_ERR_INVALID_ARG). */
+size_t vtrace_partials_mailbox_bytes_batched(int32_t num_learners, int32_t batch_max);
 vt_status vtrace_partials_allreduce_batched(double* const* partials, int32_t batch,
-                                           double* const* mailboxes, int32_t num_learners,
-                                           int32_t self, uint64_t* counter, vt_stream_t stream);
+                                           int32_t batch_max, double* const* mailboxes,
+                                           int32_t num_learners, int32_t self, uint64_t* counter,
+                                           vt_stream_t stream);
 
 /* ---- NEXT #3, first half: the output layer in front of the path ----
  * [z^pi | V] = h W + b over all M = T*B time-folded steps (time folded into the

@@ -99,15 +99,18 @@ struct PartialsPtrs {
 };
 
 __global__ void __launch_bounds__(256) partials_allreduce_batch_kernel(PartialsPtrs parts,
-                                                                       int batch, Mailboxes mb,
-                                                                       int n, int self,
+                                                                       int batch, int batch_max,
+                                                                       Mailboxes mb, int n,
+                                                                       int self,
                                                                        unsigned long long* counter) {
   const int t = threadIdx.x;
   const unsigned long long tag = *reinterpret_cast<volatile unsigned long long*>(counter) + 1ull;
   const int par = (int)(tag & 1ull);
-  const int per = batch * VT_P_COUNT;
+  // (slots laid out for the mailbox's largest batch: a call's region of either parity is the
+  // same whatever its own batch size, so calls of different sizes never overlap)
+  const int per = batch_max * VT_P_COUNT;
   double s = 0.0;
-  if (t < per) {
+  if (t < batch * VT_P_COUNT) {
     const double v = parts.p[t / VT_P_COUNT][t % VT_P_COUNT];
     for (int r = 0; r < n; ++r) {
       Slot* d = mb.p[r] + ((size_t)(par * n + self) * per + t);
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(256) partials_allreduce_batch_kernel(PartialsP
     }
   }
   __syncthreads();
-  if (t < per) parts.p[t / VT_P_COUNT][t % VT_P_COUNT] = s;
+  if (t < batch * VT_P_COUNT) parts.p[t / VT_P_COUNT][t % VT_P_COUNT] = s;
   if (t == 0) *reinterpret_cast<volatile unsigned long long*>(counter) = tag;
 }
 
@@ -143,12 +146,14 @@ extern "C" size_t vtrace_partials_mailbox_bytes_batched(int32_t num_learners, in
 }
 
 extern "C" vt_status vtrace_partials_allreduce_batched(double* const* partials, int32_t batch,
+                                                       int32_t batch_max,
                                                        double* const* mailboxes,
                                                        int32_t num_learners, int32_t self,
                                                        uint64_t* counter, vt_stream_t stream) {
   using namespace vtpa;
   if (!partials || !mailboxes || !counter) return VT_ERR_INVALID_ARG;
-  if (batch < 1 || batch > kMaxBatch) return VT_ERR_INVALID_ARG;
+  if (batch_max < 1 || batch_max > kMaxBatch || batch < 1 || batch > batch_max)
+    return VT_ERR_INVALID_ARG;
   if (num_learners < 1 || num_learners > kMaxLearners || self < 0 || self >= num_learners)
     return VT_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(counter) & 7) return VT_ERR_ALIGNMENT;
@@ -166,7 +171,8 @@ extern "C" vt_status vtrace_partials_allreduce_batched(double* const* partials, 
   }
   const int threads = ((batch * VT_P_COUNT + 31) / 32) * 32;
   partials_allreduce_batch_kernel<<<1, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      pp, batch, mb, num_learners, self, reinterpret_cast<unsigned long long*>(counter));
+      pp, batch, batch_max, mb, num_learners, self,
+      reinterpret_cast<unsigned long long*>(counter));
   return cudaGetLastError() == cudaSuccess ? VT_OK : VT_ERR_CUDA;
 }
 

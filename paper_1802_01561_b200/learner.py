@@ -108,12 +108,9 @@ class LearnerStep:
                   symmetric memory; "fused" -- inside the V-trace kernel's last CTA
                   (vtrace_loss_and_grad_learners); "nccl" -- torch.distributed.all_reduce.
     exchange_every: with "nvlink" and > 1, exchange the partials of this many steps
-                  together in one kernel on the step's own stream
-                  (vtrace_partials_allreduce_batched; each step's sums are still produced, in
-                  place, once its batch is exchanged; join() exchanges a partial batch).
-                  Measured slower than the per-step side-stream exchange (the step's stream
-                  then waits for the slowest learner every batch):
-                  default 1.
+                  together in one side-stream kernel (vtrace_partials_allreduce_batched;
+                  each step's sums are still produced, in place, once its batch is
+                  exchanged; join() exchanges a partial batch).
     A step's kernel never overwrites a partials buffer whose previous collective is
     still pending: it waits for that collective's event (with buffers rotated over R
     sets, the collective of R steps ago).
@@ -168,6 +165,8 @@ class LearnerStep:
         if self.exchange_every > 1 and self.collective == "nccl":
             raise ValueError("exchange_every > 1 needs collective='nvlink'")
         self._batch: list = []  # (key, partials) of the steps not exchanged yet
+        self._batch_id = 0      # batches exchanged so far (side stream, in order)
+        self._waited = 0        # the last batch the step's stream has waited for
         if self.collective in ("nvlink", "fused"):
             self._setup_mailboxes()
         if self.collective == "fused":
@@ -214,6 +213,14 @@ class LearnerStep:
         if any(k == key for k, _ in self._batch):  # (reused before its exchange: flush first)
             self._flush()
         if self.collective == "nvlink" and self.exchange_every > 1 and self.world > 1:
+            # batched exchange on the side stream; a kernel waits only for the first batch
+            # not yet waited for that last read its buffer (batches finish in order on the
+            # side stream, so one wait covers every earlier batch): in a captured graph only
+            # one kernel in exchange_every has a cross-stream edge in and one an edge out
+            pend = self._pending.pop(key, None)
+            if pend is not None and self.guard_partials and pend[0] > self._waited:
+                self.stream.wait_event(pend[1])
+                self._waited = pend[0]
             with torch.cuda.stream(self.stream):
                 self._launch(inputs, out)
             self._batch.append((key, out["partials"]))
@@ -239,15 +246,21 @@ class LearnerStep:
             self._pending[key] = ev
 
     def _flush(self):
-        """Exchange the batched steps' partials: one kernel on the step's own stream (no
-        cross-stream edges in a captured graph; the stream order keeps a buffer from being
-        refilled before its exchange)."""
+        """Exchange the batched steps' partials: one kernel on the side stream after the
+        batch's last kernel."""
         if not self._batch:
             return
         from . import vtrace
-        with torch.cuda.stream(self.stream):
+        self.comm_stream.wait_stream(self.stream)
+        with torch.cuda.stream(self.comm_stream):
             vtrace.partials_allreduce_batched([p for _, p in self._batch], self._mbox_ptrs,
-                                              self.rank, self._counter)
+                                              self.rank, self._counter,
+                                              batch_max=self.exchange_every)
+            ev = torch.cuda.Event()
+            ev.record(self.comm_stream)
+        self._batch_id += 1
+        for k, _ in self._batch:
+            self._pending[k] = (self._batch_id, ev)
         self._batch = []
 
     def join(self):
@@ -257,6 +270,7 @@ class LearnerStep:
             self._flush()
             self.stream.wait_stream(self.comm_stream)
             self._pending.clear()
+            self._waited = self._batch_id
 
     def run(self, batches: Sequence[tuple[dict, dict]]):
         """Enqueue the steps over (inputs, out) pairs, then join."""

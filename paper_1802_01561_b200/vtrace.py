@@ -140,7 +140,7 @@ def load_library(path: str = LIB_PATH):
     lib.vtrace_partials_mailbox_bytes_batched.argtypes = [ctypes.c_int32, ctypes.c_int32]
     lib.vtrace_partials_mailbox_bytes_batched.restype = ctypes.c_size_t
     lib.vtrace_partials_allreduce_batched.argtypes = [ctypes.POINTER(ctypes.c_void_p),
-                                                      ctypes.c_int32,
+                                                      ctypes.c_int32, ctypes.c_int32,
                                                       ctypes.POINTER(ctypes.c_void_p),
                                                       ctypes.c_int32, ctypes.c_int32, P, P]
     lib.vtrace_partials_allreduce_batched.restype = ctypes.c_int
@@ -756,7 +756,7 @@ def partials_mailbox_bytes_batched(num_learners: int, batch: int) -> int:
 
 
 def partials_allreduce_batched(partials_list, mailbox_ptrs, self_index: int,
-                               counter: torch.Tensor):
+                               counter: torch.Tensor, batch_max: int = 32):
     """Sum over the learners of several steps' [8] fp64 partials, in place, one kernel
     (vtrace_partials_allreduce_batched).  Marshalling only."""
     if not 1 <= len(partials_list) <= 32:
@@ -769,7 +769,7 @@ def partials_allreduce_batched(partials_list, mailbox_ptrs, self_index: int,
         raise ValueError("partials_allreduce_batched: counter must be one int64 on the device")
     pa = _ptr_array([t.data_ptr() for t in partials_list])
     mb = _ptr_array([int(p) for p in mailbox_ptrs])
-    st = load_library().vtrace_partials_allreduce_batched(pa, len(partials_list), mb,
+    st = load_library().vtrace_partials_allreduce_batched(pa, len(partials_list), int(batch_max), mb,
                                                           len(mailbox_ptrs), int(self_index),
                                                           _ptr(counter), _stream(dev))
     _check(st, "vtrace_partials_allreduce_batched")

@@ -286,12 +286,13 @@ def test_round2_entry_points_host_checks(lib):
     assert lib.vtrace_partials_mailbox_bytes_batched(2, 0) == 0
     assert lib.vtrace_partials_mailbox_bytes_batched(2, 33) == 0
     assert lib.vtrace_partials_mailbox_bytes_batched(2, 4) == 2 * 2 * 4 * 8 * 16
-    assert f(None, 1, two, 2, 0, p, None) == 1
-    assert f(two, 0, two, 2, 0, p, None) == 1
-    assert f(two, 33, two, 2, 0, p, None) == 1
-    assert f(two, 2, two, 2, 2, p, None) == 1
-    assert f(two, 2, two, 2, 0, P(4100), None) == 5
-    assert f((ctypes.c_void_p * 2)(8192, 12292), 2, two, 2, 0, p, None) == 5
+    assert f(None, 1, 4, two, 2, 0, p, None) == 1
+    assert f(two, 0, 4, two, 2, 0, p, None) == 1
+    assert f(two, 5, 4, two, 2, 0, p, None) == 1   # batch > batch_max
+    assert f(two, 2, 33, two, 2, 0, p, None) == 1
+    assert f(two, 2, 4, two, 2, 2, p, None) == 1
+    assert f(two, 2, 4, two, 2, 0, P(4100), None) == 5
+    assert f((ctypes.c_void_p * 2)(8192, 12292), 2, 4, two, 2, 0, p, None) == 5
     # gradient push
     g = lib.vtrace_grad_push
     assert g(None, two, 2, 0, 8, None) == 1

@@ -110,7 +110,7 @@ def test_partials_allreduce_batched(n, batches):
         torch.cuda.synchronize()
         for r in reversed(range(n)):
             with torch.cuda.stream(streams[r]):
-                vt.partials_allreduce_batched(parts[r], ptrs, r, counters[r])
+                vt.partials_allreduce_batched(parts[r], ptrs, r, counters[r], batch_max=bmax)
         torch.cuda.synchronize()
         for s in range(m):
             expect = torch.zeros(8, dtype=torch.float64)
@@ -120,3 +120,34 @@ def test_partials_allreduce_batched(n, batches):
                 assert torch.equal(parts[r][s].cpu(), expect), (call, s, r)
     for c in counters:
         assert int(c.item()) == len(batches)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3])
+def test_partials_allreduce_batched_back_to_back(n):
+    """Batched calls of different sizes queued back to back on every learner's stream (no
+    host synchronisation between calls, so one learner can run a call ahead of another): the
+    mailbox regions of the two parities must not overlap whatever the batch sizes."""
+    dev = torch.device("cuda", 0)
+    sizes = [8, 1, 5, 8, 3, 8, 2, 7, 8, 1]
+    bmax = 8
+    mbs = [torch.zeros(vt.partials_mailbox_bytes_batched(n, bmax) // 8, dtype=torch.float64,
+                       device=dev) for _ in range(n)]
+    ptrs = [m.data_ptr() for m in mbs]
+    counters = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(n)]
+    streams = [torch.cuda.Stream(dev) for _ in range(n)]
+    g = torch.Generator().manual_seed(40 + n)
+    calls = [[[(torch.randn(8, dtype=torch.float64, generator=g)).to(dev) for _ in range(m)]
+              for r in range(n)] for m in sizes]
+    expect = [[sum((c[r][s].cpu() for r in range(n)), torch.zeros(8, dtype=torch.float64))
+               for s in range(len(c[0]))] for c in calls]
+    torch.cuda.synchronize()
+    for r in reversed(range(n)):
+        with torch.cuda.stream(streams[r]):
+            for c in calls:
+                vt.partials_allreduce_batched(c[r], ptrs, r, counters[r], batch_max=bmax)
+    torch.cuda.synchronize()
+    for i, c in enumerate(calls):
+        for s in range(len(c[0])):
+            for r in range(n):
+                assert torch.equal(c[r][s].cpu(), expect[i][s]), (i, s, r)
