@@ -52,7 +52,10 @@ bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out
   const long long grid = (G4 + ncg - 1) / ncg;
   if (grid > (1LL << 20)) return false;
   const long long K8 = (T + 7) / 8;  // 8-step chunks
-  int nts = (int)std::max<long long>(1, std::min<long long>(CB_MAX_WARPS / ncg, K8));
+#ifndef CB_MAXNTS
+#define CB_MAXNTS 14  // A/B: cap on the time slots per column group
+#endif
+  int nts = (int)std::max<long long>(1, std::min<long long>(std::min(CB_MAX_WARPS / ncg, CB_MAXNTS), K8));
   const long long J0 = (K8 + nts - 1) / nts;
   nts = (int)((K8 + J0 - 1) / J0);  // same number of iterations, fewest idle slots
   const int Bc = 4 * ncg;
