@@ -15,6 +15,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1802_01561_b200 as pkg  # noqa: E402
 from paper_1802_01561_b200 import workload as wl  # noqa: E402
 
+if os.environ.get("KT_LIB"):  # A/B variant library (tools/ab_build.py)
+    pkg.vtrace.load_library(os.environ["KT_LIB"])
+
 PEAK = 6552.3
 try:
     PEAK = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
