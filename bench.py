@@ -540,7 +540,9 @@ def run_ours(args):
                                   + " (side stream"
                                   + (f", {args.reserve_sms} SM reserved)" if args.reserve_sms
                                      else ")")),
-                   "step": "paper_1802_01561_b200.learner.LearnerStep"},
+                   "step": "paper_1802_01561_b200.learner.LearnerStep",
+                   **({"collective_fallback": step_obj.collective_fallback}
+                      if getattr(step_obj, "collective_fallback", None) else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": vt.kernel_for(T, B, A, inp["dtype"]), "kernel_ms": kernel_ms,

@@ -167,8 +167,14 @@ class LearnerStep:
         self._batch: list = []  # (key, partials) of the steps not exchanged yet
         self._batch_id = 0      # batches exchanged so far (side stream, in order)
         self._waited = 0        # the last batch the step's stream has waited for
+        self.collective_fallback = None
         if self.collective in ("nvlink", "fused"):
-            self._setup_mailboxes()
+            try:
+                self._setup_mailboxes()
+            except Exception as e:  # noqa: BLE001 -- no peer-mapped memory: NCCL, stated
+                # (symmetric memory failing is a property of the node, the same on every rank)
+                self.collective_fallback = f"{type(e).__name__}: {e}"[:200]
+                self.collective, self.exchange_every = "nccl", 1
         if self.collective == "fused":
             self.kw.update(mailboxes=self._mbox_ptrs, self_index=self.rank)
 
