@@ -80,7 +80,23 @@ __device__ __forceinline__ unsigned long long cb_now() {
 #define CB_STAMP(k) ((void)0)
 #endif
 
-constexpr int CB_MAX_WARPS = 14;   // compute warps per CTA (+1 producer: <= 128 registers)
+// Compute warps per CTA (+1 producer), per logits dtype; the register cap is
+// 64K / (32 (warps + 1)): 14 -> 128 registers (bf16: `large` keeps every value in registers),
+// 18 -> 107 (fp32: a few spilled bytes, but `stress` gets 9 time slots per column group
+// instead of 7 -- 28 iterations instead of 36: 80.5 -> 76.1 us, profiles/r2_cb_maxw_ab.txt)
+#ifndef CB_MAXW_BF16
+#define CB_MAXW_BF16 14
+#endif
+#ifndef CB_MAXW_F32
+#define CB_MAXW_F32 18
+#endif
+#if defined(VT_CB_PART) && VT_CB_PART == 1
+constexpr int CB_MAX_WARPS = CB_MAXW_F32;
+#else
+constexpr int CB_MAX_WARPS = CB_MAXW_BF16;
+#endif
+constexpr int cb_max_warps(int elem) { return elem == 4 ? CB_MAXW_F32 : CB_MAXW_BF16; }
+static_assert(CB_MAXW_BF16 <= 20 && CB_MAXW_F32 <= 20, "at most 20 compute warps (>= 97 registers)");
 constexpr int CB_MAX_STAGES = 4;
 
 struct CbParams {

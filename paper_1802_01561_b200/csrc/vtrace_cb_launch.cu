@@ -26,7 +26,7 @@ namespace vtb200 {
 //   g    column groups (of 4) per logits TMA segment: 4 g A elem must be a multiple
 //        of 16 bytes (bf16 with odd A: g = 2)
 //   ncg  column groups per CTA = ceil(B/4 / sms) rounded up to g: one CTA per SM
-//   nts  warps per column group (time slots): as many as 16 warps allow, at most the
+//   nts  warps per column group (time slots): as many as cb_max_warps allows, at most the
 //        number of 8-step chunks, spread so that the iterations are evenly filled
 // False if the shape does not fit the kernel (then the look-back kernel runs).
 bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out_mask, int sms,
@@ -46,16 +46,17 @@ bool cb_plan(long long T, long long B, int A, int elem, bool mu_lp, unsigned out
   if ((T + 256) * B >= (1LL << 31)) return false;  // 32-bit row arithmetic
   if (!cb_supported_a(A)) return false;
   const long long G4 = (B + 3) / 4;
-  int ncg = (int)std::min<long long>((G4 + sms - 1) / sms, CB_MAX_WARPS);
+  const int maxw = cb_max_warps(elem);  // the instantiation's compute warps (its register cap)
+  int ncg = (int)std::min<long long>((G4 + sms - 1) / sms, maxw);
   ncg = (ncg + g - 1) / g * g;
-  if (ncg > CB_MAX_WARPS) ncg -= g;
+  if (ncg > maxw) ncg -= g;
   const long long grid = (G4 + ncg - 1) / ncg;
   if (grid > (1LL << 20)) return false;
   const long long K8 = (T + 7) / 8;  // 8-step chunks
 #ifndef CB_MAXNTS
 #define CB_MAXNTS 14  // A/B: cap on the time slots per column group
 #endif
-  int nts = (int)std::max<long long>(1, std::min<long long>(std::min(CB_MAX_WARPS / ncg, CB_MAXNTS), K8));
+  int nts = (int)std::max<long long>(1, std::min<long long>(std::min(maxw / ncg, CB_MAXNTS), K8));
   const long long J0 = (K8 + nts - 1) / nts;
   nts = (int)((K8 + J0 - 1) / J0);  // same number of iterations, fewest idle slots
   const int Bc = 4 * ncg;

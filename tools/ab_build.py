@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""A/B variant libraries (dev tool): recompiles only the bf16 column-block unit with extra
+"""A/B variant libraries (dev tool): recompiles the column-block units with extra
 -D flags and links it with the other in-tree objects into ab/libvtrace_<tag>.so.
 
 usage: python tools/ab_build.py <tag> [DEF[=V] ...]     (run the in-tree build first)
@@ -15,10 +15,16 @@ from paper_1802_01561_b200 import _build as b  # noqa: E402
 tag, defs = sys.argv[1], sys.argv[2:]
 out = os.path.join(b.ROOT, "ab")
 os.makedirs(out, exist_ok=True)
-obj = os.path.join(out, f"cb_bf16_{tag}.o")
-subprocess.check_call([b.NVCC, *b.FLAGS, "-DVT_CB_PART=0", *["-D" + d for d in defs], "-c", "-o", obj,
-                       b.SOURCES[1]])
-objs = [os.path.join(b.CSRC, o) for _, o, _ in b.UNITS if o != "vtrace_cb_bf16.o"] + [obj]
+# both column-block units (bf16 holds the host plan, fp32 the other kernels), in parallel
+new = {}
+procs = []
+for part, name in ((0, "vtrace_cb_bf16.o"), (1, "vtrace_cb_f32.o")):
+    new[name] = os.path.join(out, f"{tag}_{name}")
+    procs.append(subprocess.Popen([b.NVCC, *b.FLAGS, f"-DVT_CB_PART={part}", *["-D" + d for d in defs],
+                                   "-c", "-o", new[name], b.SOURCES[1]]))
+if any(p.wait() != 0 for p in procs):
+    sys.exit("compile failed")
+objs = [new.get(o, os.path.join(b.CSRC, o)) for _, o, _ in b.UNITS]
 so = os.path.join(out, f"libvtrace_{tag}.so")
 subprocess.check_call([b.NVCC, *b.ARCH, "-shared", "-o", so, *objs])
 print(so)
