@@ -309,13 +309,31 @@ __device__ __forceinline__ void load_row(const LT* row, float (&z)[A_CT]) {
 
 // a / b in fp64 for b in [1, 2^30] (a row sum): MUFU reciprocal seed, two Newton steps
 // and one residual correction (within an ulp; no slow-path branch as in div.rn.f64).
+// The short-chain forms (one Newton step here, Estrin in exp64) pay where a kernel is bound
+// by its warps' dependent chains: the bf16 column-block kernel (14 warps; large 26.85 ->
+// 26.34 us), the look-back and fused-head kernels.  The fp32 column-block unit (18 warps,
+// VT_CB_PART == 1) is issue-bound and keeps the forms with fewer instructions (stress
+// 76.7 vs 76.1 us) -- profiles/r2_ratio_chain_ab.txt.
+#if defined(VT_CB_PART) && VT_CB_PART == 1
+#define VT_SHORT_CHAIN_DEFAULT 0
+#else
+#define VT_SHORT_CHAIN_DEFAULT 1
+#endif
+#ifndef VT_DDIV_NEWTON
+#define VT_DDIV_NEWTON (VT_SHORT_CHAIN_DEFAULT ? 1 : 2)  // Newton steps on the reciprocal seed
+#endif
 __device__ __forceinline__ double ddiv_pos(double a, double b) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  // one step squares the seed's error (~2^-44 after it); the residual correction of the
+  // quotient below squares it again, so the result is within an ulp either way (and
+  // a / a == 1 exactly: the on-policy ratio), with two fewer dependent DFMAs on the chain
   double e = fma(-b, r, 1.0);
   r = fma(r, e, r);
+#if VT_DDIV_NEWTON > 1
   e = fma(-b, r, 1.0);
   r = fma(r, e, r);
+#endif
   const double q = a * r;
   return fma(fma(-b, q, a), r, q);
 }
@@ -346,6 +364,9 @@ __device__ __forceinline__ StepWeights step_weights(const Params& P, double rati
 // x = n ln2 + r, |r| <= ln2/2, then a degree-6 polynomial fitted to exp on
 // that interval as 1 + r q(r) (max relative error 2.2e-9; the path needs ~1e-8,
 // DESIGN.md; exp(0) = 1 exactly).
+#ifndef VT_EXP64_ESTRIN
+#define VT_EXP64_ESTRIN VT_SHORT_CHAIN_DEFAULT  // 0 = Horner
+#endif
 __device__ __forceinline__ double exp64(double x) {
   const double LOG2E = 1.4426950408889634;
   const double LN2_HI = 6.93147180369123816490e-01;
@@ -357,13 +378,23 @@ __device__ __forceinline__ double exp64(double x) {
   int ni = __double2loint(t);
   double r = fma(-n, LN2_HI, x);
   r = fma(-n, LN2_LO, r);
-  // p(r) = 1 + r q(r): exact at r = 0, so exp(0) == 1 bitwise (on-policy ratio)
+  // p(r) = 1 + r q(r): exact at r = 0, so exp(0) == 1 bitwise (on-policy ratio).
+  // q by Estrin's scheme (three independent pairs, then two steps in r^2): 3 dependent
+  // DFMAs instead of Horner's 5 on the ratio's chain (the kernels are latency-bound there)
+#if VT_EXP64_ESTRIN
+  const double r2 = r * r;
+  const double q01 = fma(4.99999953509942752e-01, r, 1.00000003609212618e+00);
+  const double q23 = fma(4.16677243209218270e-02, r, 1.66664209451321627e-01);
+  const double q45 = fma(1.38592910771707131e-03, r, 8.37476397493414765e-03);
+  const double q = fma(fma(q45, r2, q23), r2, q01);
+#else
   double q = 1.38592910771707131e-03;
   q = fma(q, r, 8.37476397493414765e-03);
   q = fma(q, r, 4.16677243209218270e-02);
   q = fma(q, r, 1.66664209451321627e-01);
   q = fma(q, r, 4.99999953509942752e-01);
   q = fma(q, r, 1.00000003609212618e+00);
+#endif
   const double p = fma(q, r, 1.0);
   // scale by 2^n: add n to the exponent field (p in [0.7, 1.5], |n| <= 1010)
   int hi = __double2hiint(p) + (ni << 20);
