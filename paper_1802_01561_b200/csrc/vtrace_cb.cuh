@@ -399,10 +399,17 @@ __device__ __forceinline__ void cb_exps(const float2 (&z)[(A_CT + 1) / 2], float
   }
 }
 
+#ifndef CB_EARLY_RATIO
+#define CB_EARLY_RATIO 0  // 1: exp64 issued before both policies' exps (A/B; 0: between the two)
+#endif
+// e_delta (with_mu): exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) in fp64, issued as soon as the
+// behaviour row's maximum is known (between the two policies' exps) so that its dependent
+// DFMA chain overlaps the behaviour exps and sums (the kernel is bound by its warps'
+// dependent chains, DESIGN 6a; profiles/r2_ratio_chain_ab.txt: 26.32 -> 25.78 us at large)
 template <typename LT, int A_CT>
 __device__ __forceinline__ void cb_stats(const LT* zrow, const LT* mrow, int a,
                                          CbRow<LT, A_CT>& R, double& xa_p, double& xa_m,
-                                         bool with_mu) {
+                                         bool with_mu, double& e_delta) {
   constexpr int NP = (A_CT + 1) / 2;
   constexpr bool BF16 = sizeof(LT) == 2;
   constexpr float L16 = 1.44268798828125f;
@@ -410,14 +417,30 @@ __device__ __forceinline__ void cb_stats(const LT* zrow, const LT* mrow, int a,
   constexpr float CORR = BF16 ? 4.8884952e-06f : 1.3349930e-08f;  // ln2 (log2 e - L)
   cb_load_pairs<LT, A_CT>(zrow, R.z);
   const float mp = row_max<NP>(R.z);
-  float2 hp, lp, sdp, cwp;
-  cb_exps<LT, A_CT, true>(R.z, mp, R.e, hp, lp, sdp, cwp);
+  const float zap = Elem<LT>::get(zrow, a);
+  xa_p = (double)zap - (double)mp;  // z_a - m, exact
   float2 hm = f2(1.f), lm = f2(0.f), sdm = f2(0.f), cwm = f2(0.f);
   float mm = 0.f;
+  float2 zm[NP], em[NP];
+#if CB_EARLY_RATIO
   if (with_mu) {
-    float2 zm[NP], em[NP];
     cb_load_pairs<LT, A_CT>(mrow, zm);
     mm = row_max<NP>(zm);
+    const float zam = Elem<LT>::get(mrow, a);
+    xa_m = (double)zam - (double)mm;
+    e_delta = exp64(xa_p - xa_m);
+  }
+#endif
+  float2 hp, lp, sdp, cwp;
+  cb_exps<LT, A_CT, true>(R.z, mp, R.e, hp, lp, sdp, cwp);
+  if (with_mu) {
+#if !CB_EARLY_RATIO
+    cb_load_pairs<LT, A_CT>(mrow, zm);
+    mm = row_max<NP>(zm);
+    const float zam = Elem<LT>::get(mrow, a);
+    xa_m = (double)zam - (double)mm;
+    e_delta = exp64(xa_p - xa_m);
+#endif
     cb_exps<LT, A_CT, false>(zm, mm, em, hm, lm, sdm, cwm);
   }
   // finish both policies at once (.x = pi, .y = mu): the chains started at 1, so
@@ -442,12 +465,6 @@ __device__ __forceinline__ void cb_stats(const LT* zrow, const LT* mrow, int a,
   R.S_m = with_mu ? (double)s.y + (double)lo.y : 1.0;
   R.m_p = mp;
   R.sd_p = sd.x;
-  const float zap = Elem<LT>::get(zrow, a);
-  xa_p = (double)zap - (double)mp;  // z_a - m, exact
-  if (with_mu) {
-    const float zam = Elem<LT>::get(mrow, a);
-    xa_m = (double)zam - (double)mm;
-  }
   R.ea_raw = ex2_approx(BF16 ? fmaf(zap, L16, -mp * L16) : (zap - mp) * L32);
   R.finite = isfinite(sd.x) && isfinite(mp) && (!with_mu || (isfinite(sd.y) && isfinite(mm)));
 }
@@ -801,15 +818,16 @@ __global__ void __launch_bounds__((CB_MAX_WARPS + 1) * 32, 1)
       const LT* zrow = reinterpret_cast<const LT*>(sb + C.pi + zoff);
       const LT* mrow = reinterpret_cast<const LT*>(sb + C.mu + zoff);
       CbRow<LT, A_CT> R;
-      double xa_p, xa_m = 0.0;
-      cb_stats<LT, A_CT>(zrow, mrow, a, R, xa_p, xa_m, !MULP);
+      double xa_p, xa_m = 0.0, e_delta = 1.0;
+      cb_stats<LT, A_CT>(zrow, mrow, a, R, xa_p, xa_m, !MULP, e_delta);
       float lmu = 0.f;
       if constexpr (MULP) {
         lmu = lds<float>(sb + C.mu + soff);  // log mu(a_t), given (S_m = 1)
         xa_m = (double)lmu;
+        e_delta = exp64(xa_p - xa_m);
       }
       // a5, a7: pi(a)/mu(a) = exp((z^pi_a - m_pi) - (z^mu_a - m_mu)) S_mu / S_pi
-      const double ratio = exp64(xa_p - xa_m) * ddiv_pos(R.S_m, R.S_p);
+      const double ratio = e_delta * ddiv_pos(R.S_m, R.S_p);
 #if CB_TD32
       const double td = (double)(fmaf(gm, Vn, (float)reward_transform(rt, P.reward_mode)) - Vt);
 #else

@@ -367,6 +367,9 @@ __device__ __forceinline__ StepWeights step_weights(const Params& P, double rati
 #ifndef VT_EXP64_ESTRIN
 #define VT_EXP64_ESTRIN VT_SHORT_CHAIN_DEFAULT  // 0 = Horner
 #endif
+#ifndef VT_EXP64_CW1
+#define VT_EXP64_CW1 0  // A/B: 1 = one-step reduction (no gain measured)
+#endif
 __device__ __forceinline__ double exp64(double x) {
   const double LOG2E = 1.4426950408889634;
   const double LN2_HI = 6.93147180369123816490e-01;
@@ -376,8 +379,16 @@ __device__ __forceinline__ double exp64(double x) {
   double t = fma(x, LOG2E, MAGIC);
   double n = t - MAGIC;
   int ni = __double2loint(t);
+#if VT_EXP64_CW1
+  // one-step reduction: |n (ln2 - fl(ln2))| <= 1010 * 2.3e-17, a relative error of 2.3e-14 in
+  // the result, far inside the polynomial's 2.2e-9 -- one dependent DFMA fewer
+  double r = fma(-n, 6.93147180559945286e-01, x);
+  (void)LN2_HI;
+  (void)LN2_LO;
+#else
   double r = fma(-n, LN2_HI, x);
   r = fma(-n, LN2_LO, r);
+#endif
   // p(r) = 1 + r q(r): exact at r = 0, so exp(0) == 1 bitwise (on-policy ratio).
   // q by Estrin's scheme (three independent pairs, then two steps in r^2): 3 dependent
   // DFMAs instead of Horner's 5 on the ratio's chain (the kernels are latency-bound there)
