@@ -309,11 +309,10 @@ __device__ __forceinline__ void load_row(const LT* row, float (&z)[A_CT]) {
 
 // a / b in fp64 for b in [1, 2^30] (a row sum): MUFU reciprocal seed, two Newton steps
 // and one residual correction (within an ulp; no slow-path branch as in div.rn.f64).
-// The short-chain forms (one Newton step here, Estrin in exp64) pay where a kernel is bound
-// by its warps' dependent chains: the bf16 column-block kernel (14 warps; large 26.85 ->
-// 26.34 us), the look-back and fused-head kernels.  The fp32 column-block unit (18 warps,
-// VT_CB_PART == 1) is issue-bound and keeps the forms with fewer instructions (stress
-// 76.7 vs 76.1 us) -- profiles/r2_ratio_chain_ab.txt.
+// The short-chain form (one Newton step) pays where a kernel is bound by its warps'
+// dependent chains: the bf16 column-block kernel (14 warps), the look-back and fused-head
+// kernels.  The fp32 column-block unit (18 warps, VT_CB_PART == 1) is issue-bound and keeps
+// two steps (stress 76.7 vs 76.1 us) -- profiles/r2_ratio_chain_ab.txt.
 #if defined(VT_CB_PART) && VT_CB_PART == 1
 #define VT_SHORT_CHAIN_DEFAULT 0
 #else
@@ -365,7 +364,8 @@ __device__ __forceinline__ StepWeights step_weights(const Params& P, double rati
 // that interval as 1 + r q(r) (max relative error 2.2e-9; the path needs ~1e-8,
 // DESIGN.md; exp(0) = 1 exactly).
 #ifndef VT_EXP64_ESTRIN
-#define VT_EXP64_ESTRIN VT_SHORT_CHAIN_DEFAULT  // 0 = Horner
+#define VT_EXP64_ESTRIN 0  // A/B: 1 = Estrin (faster before exp64 moved between the policies' exps,
+                           // slower after: 25.77 vs 25.58 us at large, r2_ratio_chain_ab.txt)
 #endif
 #ifndef VT_EXP64_CW1
 #define VT_EXP64_CW1 0  // A/B: 1 = one-step reduction (no gain measured)
