@@ -184,6 +184,16 @@ class ClockSampler:
             self.proc.kill()
 
     def summary(self, t0=None, t1=None):
+        out = self._summary(t0, t1)
+        if out["samples"] == 0 and t0 is not None:
+            # a timed region shorter than the 50 ms sampling period (e.g. --steps 20) can
+            # fall between two samples: take the samples within 100 ms of it (the GPU is under
+            # the same load then: the untimed graph pre-roll runs right before it), stated
+            out = self._summary(t0 - 0.1, t1 + 0.04)
+            out["window"] = "timed region +- 100 ms (shorter than the 50 ms sampling period)"
+        return out
+
+    def _summary(self, t0=None, t1=None):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ts, line in self.lines:
